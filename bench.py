@@ -1,0 +1,362 @@
+"""Benchmark: MLMC random-walk estimator for e^{tA}v on BASELINE config 2 (C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--rows-per-step R] [--config c2]
+
+Workload (BASELINE.json configs[1]): 2-D 5-point Laplacian on a 1024x1024 grid
+(n = 1,048,576, 5.2M nnz, fp64), t = 0.5, v uniform [0,1) from the reference's Philox stream,
+every component estimated to eps = 1e-3 by the reference's MLMC driver (Algorithm 1, one
+decision sequence per component, row seed 1000 + row).  A STEP is one complete driver solve
+of a batch of R components; batches walk a seeded permutation of all 2^20 rows, so steps
+cover C2 without repeating.  Each rank solves its own R-row batch (weak scaling: rows shard
+across ranks with no data-path collective; only the timings are reduced).
+
+Timed region (`value`): tables already resident in HBM; K steps bracketed by barrier +
+torch.cuda.synchronize(), CUDA events recorded on the library's own stream; max over ranks.
+L2 is flushed (256 MB write) before every step inside the timed region.
+`e2e`: the same work through the public API from HOST buffers -- context creation from the
+host CSR + u (H2D), the solve, results back to host -- per step, CUDA events on the current
+stream around the call.
+
+`--impl reference`: the UNMODIFIED reference (oracle/_ref/libexpmc_ref.so, compiled from
+/root/reference by oracle/Makefile) runs its own mlmc_driver per component on all host
+cores (OpenMP), rank 0 only, each step a bounded sample of rows of the same batches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "random-walk transitions/sec and exp(tA)v rows/sec at target ε; % gather roofline"
+UNIT = "transitions/s"
+ALG_BYTES_PER_JUMP = 64    # destination row record (32 B sector) + edge record sector
+ALG_BYTES_PER_SAMPLE = 32  # terminal u[state] sector
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--rows-per-step", type=int, default=0, help="components per rank per step (0: default)")
+    p.add_argument("--ref-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def batch_rows(n, step, rank, world, r):
+    """Rows of (step, rank): consecutive slices of a fixed permutation of all rows."""
+    perm = np.random.default_rng(20190429).permutation(n)
+    k = (step * world + rank) * r
+    idx = (np.arange(k, k + r) % n)
+    return np.sort(perm[idx]).astype(np.int64)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for nm, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return None
+
+
+# ------------------------------------------------------------------------------ reference arm
+def reference_rows(ref_chain, cfg, rows, seconds, threads, max_rows):
+    """Reference mlmc_driver on rows one at a time until the budget runs out."""
+    jumps = samples = done = 0
+    t0 = time.perf_counter()
+    for r in rows[:max_rows]:
+        (res,) = ref_chain.driver_rows(cfg.u, cfg.beta, [int(r)], [1000 + int(r)], epsilon=cfg.epsilon, threads=threads)
+        jumps += res["total_jumps"]
+        samples += res["total_samples"]
+        done += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    return jumps, samples, done, time.perf_counter() - t0
+
+
+def run_reference(args, cfg, rank, world, r):
+    if rank != 0:
+        return 0
+    from oracle import CSR, Reference, have_reference
+
+    if not have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libexpmc_ref.so not built"}))
+        return 0
+    threads = os.cpu_count() or 1
+    ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
+    per_step = max(1.0, args.ref_seconds / max(1, args.steps))
+    for w in range(args.warmup):
+        reference_rows(ref, cfg, batch_rows(cfg.a.n, w, 0, 1, r), min(per_step, 2.0), threads, 4)
+    tj = ts = tr = 0
+    tt = 0.0
+    for s in range(args.steps):
+        j, smp, done, dt = reference_rows(ref, cfg, batch_rows(cfg.a.n, args.warmup + s, 0, 1, r), per_step, threads, r)
+        tj += j
+        ts += smp
+        tr += done
+        tt += dt
+    value = tj / tt
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": cfg.description, "sample": f"{tr} components (as-shipped mlmc_driver per row)",
+                   "parallelism": f"OpenMP {threads} threads, rank 0 only"},
+        "rows_per_s": tr / tt, "samples_per_s": ts / tt,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{tr} C2 components, as-shipped reference mlmc_driver, {tt:.1f} s"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    from paper_1904_12754_b200 import configs
+
+    cfg = configs.make_config(args.config)
+    r = args.rows_per_step or (1 << 16)
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world, r)
+
+    import torch
+
+    import paper_1904_12754_b200 as P
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    opts = P.MlmcOptions(epsilon=cfg.epsilon)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ctx = P.Context(cfg.a, cfg.u, device=local)
+    ext = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local))
+
+    def solve(step):
+        rows = batch_rows(cfg.a.n, step, rank, world, r)
+        res, _ = P.mlmc_driver_rows(ctx, cfg.beta, rows, configs.row_seeds(rows), opts, want_levels=False)
+        return res
+
+    for w in range(args.warmup):
+        with torch.cuda.stream(ext):
+            flush.fill_(w & 0xFF)
+        solve(w)
+    torch.cuda.synchronize()
+
+    ctx.reset_counters()
+    clocks = Clocks(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(ext)
+    results = []
+    for s in range(args.steps):
+        with torch.cuda.stream(ext):
+            flush.fill_(s & 0xFF)
+        results.append(solve(args.warmup + s))
+    ev1.record(ext)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_local = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms_local)
+    ctr = ctx.counters()
+    res = np.concatenate(results)
+    jumps = sum_over_ranks(ctr["jumps"])
+    samples = sum_over_ranks(ctr["samples"])
+    rows_done = sum_over_ranks(len(res))
+    conv = sum_over_ranks(int(res["converged"].sum()))
+    value = jumps / (ms * 1e-3)
+
+    # roofline of the dominant kernel (k_sample): algorithmic bytes / summed launch time
+    alg_bytes = ctr["jumps"] * ALG_BYTES_PER_JUMP + ctr["samples"] * ALG_BYTES_PER_SAMPLE
+    kern_s = ctr["sampler_ms"] * 1e-3
+    achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
+    peaks, peak_src = load_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = load_traffic()
+    gather_l2 = gather_hbm = None
+    if rank == 0:
+        try:
+            gather_l2 = P.bench_gather(local, 64 << 20)
+            gather_hbm = P.bench_gather(local, 8 << 30)
+        except Exception:
+            pass
+    gpu_launches = ctr["kernel_launches"] + 2 * args.steps  # + the L2 flush fill per step (torch)
+
+    # e2e through the public API from host buffers
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        jumps_e = 0
+        h2d = d2h = 0
+        e0.record()
+        for s in range(args.steps):
+            with P.Context(cfg.a, cfg.u, device=local) as c2:
+                rows = batch_rows(cfg.a.n, args.warmup + s, rank, world, r)
+                P.mlmc_driver_rows(c2, cfg.beta, rows, configs.row_seeds(rows), opts, want_levels=False)
+                k = c2.counters()
+                jumps_e += k["jumps"]
+                h2d += k["h2d_bytes"] + rows.nbytes * 2  # rows + seeds read by the driver
+                d2h += k["d2h_bytes"]
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms_e = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": sum_over_ranks(jumps_e) / (ms_e * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
+               "ms_per_step": ms_e / args.steps,
+               "includes": "table build from host CSR+u (H2D), driver solve, per-round H2D/D2H, results to host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import CSR, Reference, have_reference
+
+            if have_reference():
+                threads = os.cpu_count() or 1
+                ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
+                j, smp, done, dt = reference_rows(ref, cfg, batch_rows(cfg.a.n, args.warmup, 0, 1, r),
+                                                  args.ref_seconds, threads, r)
+                cpu = {"value": j / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"{done} C2 components of the first timed batch through the as-shipped reference "
+                                 f"mlmc_driver (OpenMP, {dt:.1f} s)", "rows_per_s": done / dt}
+        except Exception as exc:  # baseline failure must not hide the GPU line
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2 (BASELINE configs[1]): {cfg.description}; one step = full MLMC driver "
+                                   f"solve of {r} components per rank",
+                       "rows_per_rank_per_step": r, "epsilon": cfg.epsilon, "t": cfg.beta,
+                       "l2": "flushed (256 MB write) before every step; C2 tables (~100 MB) are L2-sized",
+                       "parallelism": f"rows sharded over {world} rank(s), no data-path collective"},
+            "rows_per_s": rows_done / (ms * 1e-3), "samples_per_s": samples / (ms * 1e-3),
+            "converged_rows": int(conv), "rows": int(rows_done),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_sample", "sampler_launches": ctr["sampler_launches"],
+                         "kernel_ms": ctr["sampler_ms"], "step_share": ctr["sampler_ms"] / ms_local,
+                         "alg_bytes": f"{ALG_BYTES_PER_JUMP} B/transition + {ALG_BYTES_PER_SAMPLE} B/sample",
+                         "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
+                         "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches), "clocks": clk,
+        }
+        print(json.dumps(line))
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,198 @@
+/* expmc_b200 -- C-ABI of the B200-native MLMC random-walk estimator for e^{tA}v.
+ *
+ * Drop-in boundary for the hot path of arXiv 1904.12754's reference (`expmc`,
+ * /root/reference/proj/core): everything the reference does between "a decomposed matrix
+ * and a vector are ready" and "LevelStats / MlmcResult come back" runs behind these entry
+ * points on one GPU.  Plain pointers and sizes only; all buffers passed in are caller-owned
+ * HOST memory, read or written during the call.  A context owns all device memory of one
+ * GPU (one context per process per GPU; multi-GPU = one process per GPU).
+ *
+ * Error convention: every int-returning call returns EXPMC_OK (0) or a status whose value
+ * names the C++ exception type the reference throws for the same input, so the C++ shim
+ * (expmc_b200.hpp) can rethrow it.  expmc_last_error() gives the message (thread-local).
+ *
+ * Thread safety: a context is driven by one host thread at a time (the reference driver is
+ * sequential too).  Results are a pure function of (matrix, vector, level,
+ * entry, seed, sample-index range): independent of launch geometry and GPU count.
+ */
+#ifndef EXPMC_B200_H
+#define EXPMC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EXPMC_OK 0
+#define EXPMC_EINVAL 1    /* std::invalid_argument */
+#define EXPMC_ERANGE 2    /* std::out_of_range     */
+#define EXPMC_EDOMAIN 3   /* std::domain_error     */
+#define EXPMC_ECUDA 4     /* CUDA runtime failure (no CPU fallback exists) */
+#define EXPMC_ENOTIMPL 5  /* mode not built yet (forward / fem sampling)   */
+#define EXPMC_EINTERNAL 9
+
+/* Sampling lanes of the reference's Philox key (mlmc.cpp:94-96). */
+#define EXPMC_LANE_ENTRY 0u
+
+typedef struct expmc_ctx expmc_ctx;
+
+/* Square sparse matrix in canonical CSR, exactly what expmc::SparseMatrix stores
+ * (sparse.hpp:21-75): row_ptr[0]=0, non-decreasing, row_ptr[n]=nnz; columns strictly
+ * increasing inside a row and in [0,n); finite values. */
+typedef struct {
+    int64_t n;
+    int64_t nnz;
+    const int64_t* row_ptr;
+    const int64_t* col;
+    const double* val;
+} expmc_csr;
+
+typedef struct {
+    int64_t n;
+    int64_t n_edges;      /* off-diagonal chain edges (ChainDecomposition::jump_target.size()) */
+    double d_max;         /* ChainDecomposition::d_max (exact) */
+    double d_bar;         /* ChainDecomposition::d_bar (device tree sum; ~1 ulp from the reference) */
+    int32_t device;
+    int32_t num_sms;
+    uint64_t table_bytes; /* device bytes of the packed row + edge tables */
+} expmc_ctx_info;
+
+/* One run_level request (mlmc.hpp:86-88): extend level `level` of the entry-mode problem
+ * for row `entry` by sample indices [first_index, first_index + count) under `seed`. */
+typedef struct {
+    int64_t entry;
+    uint64_t seed;
+    uint64_t first_index;
+    uint64_t count;
+    int32_t level;
+    int32_t base_level; /* nonzero: plain fine functional P_l (l == l0); zero: P_l - P_{l-1} */
+} expmc_level_req;
+
+/* LevelStats (mlmc.hpp:18-31) increment, plus the number of CTMC jumps (transitions). */
+typedef struct {
+    double sum;
+    double sum_sq;
+    uint64_t samples;
+    uint64_t cost; /* model units: exponential draws + fine steps (paths.hpp:22-23) */
+    uint64_t jumps;
+} expmc_level_stats;
+
+/* MlmcOptions (mlmc.hpp:59-67); `seed` is used by expmc_mlmc_driver only (the row API takes
+ * one seed per row); `threads` is accepted and ignored. */
+typedef struct {
+    double epsilon;
+    uint64_t seed;
+    int32_t threads;
+    int32_t l0_override;
+    uint64_t warmup;
+    int32_t max_levels_above_l0;
+    int32_t max_iterations;
+} expmc_options;
+
+/* MlmcResult (mlmc.hpp:33-43) without the per-level vector (returned separately). */
+typedef struct {
+    double estimate;
+    double statistical_error;
+    double bias_estimate;
+    int32_t l0;
+    int32_t L;
+    uint64_t total_cost;
+    int32_t converged;
+    int32_t nlevels;
+    uint64_t total_jumps;
+    uint64_t total_samples;
+} expmc_result;
+
+/* One entry of MlmcResult::levels (LevelStats, mlmc.hpp:18-24). */
+typedef struct {
+    int32_t level;
+    int32_t pad;
+    double sum;
+    double sum_sq;
+    uint64_t samples;
+    uint64_t cost;
+} expmc_level_record;
+
+/* Counters since context creation (or the last reset). */
+typedef struct {
+    uint64_t kernel_launches;  /* every kernel this library launched */
+    uint64_t sampler_launches; /* launches of the path-sampler kernel */
+    double sampler_ms;         /* summed CUDA-event duration of the sampler launches */
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint64_t samples;
+    uint64_t jumps;
+    uint64_t fine_steps;
+    uint64_t rounds;           /* batched driver rounds (kernel batches) */
+} expmc_counters;
+
+const char* expmc_last_error(void);
+const char* expmc_version(void);
+int expmc_device_count(int* out);
+
+/* Build the sampling tables of A on `device` and bind the vector u (length n).
+ * Replaces: decompose(A) (chain.cpp:75, decompose_impl chain.cpp:15-71) + the per-level
+ * LevelSampler threshold table (paths.cpp:84-91) + MlmcProblem{dec, u} (mlmc.hpp:50-57).
+ * Errors as decompose / SparseMatrix: non-finite entry -> EXPMC_EINVAL, column outside
+ * [0,n) -> EXPMC_ERANGE, non-canonical CSR -> EXPMC_EINVAL. */
+int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx** out);
+void expmc_ctx_destroy(expmc_ctx* ctx);
+int expmc_ctx_get_info(const expmc_ctx* ctx, expmc_ctx_info* out);
+/* Rebind u (MlmcProblem::u): length n. */
+int expmc_ctx_set_vector(expmc_ctx* ctx, const double* u);
+/* Export the decomposition (ChainDecomposition, chain.hpp:27-40): d, rate [n], row_ptr [n+1],
+ * jump_cdf, jump_target [n_edges], sign [n_edges]; any pointer may be NULL. */
+int expmc_ctx_export_tables(const expmc_ctx* ctx, double* d, double* rate, int64_t* row_ptr,
+                            double* jump_cdf, int64_t* jump_target, uint8_t* sign);
+int expmc_ctx_get_counters(const expmc_ctx* ctx, expmc_counters* out);
+/* The context's CUDA stream (cudaStream_t as void*), for timing with events on the stream
+ * the sampler kernels are launched on. */
+int expmc_ctx_get_stream(const expmc_ctx* ctx, void** stream);
+int expmc_ctx_reset_counters(expmc_ctx* ctx);
+
+/* run_level (mlmc.hpp:86-88; run_level_ex mlmc.cpp:76-148), entry mode, ONE request.
+ * Errors as the reference: level outside [0,62] or beta <= 0 -> EXPMC_EINVAL; entry outside
+ * [0,n) -> EXPMC_ERANGE; coupled (base_level == 0) at level 0 -> EXPMC_EINVAL. */
+int expmc_run_level(expmc_ctx* ctx, int64_t entry, double beta, int32_t level, int32_t base_level,
+                    uint64_t first_index, uint64_t additional, uint64_t seed,
+                    expmc_level_stats* out);
+
+/* Batched run_level: nreq independent requests (any mix of rows/levels/ranges) in one GPU
+ * pass; out[i] is bit-for-bit what expmc_run_level would return for req[i]. */
+int expmc_run_level_batch(expmc_ctx* ctx, double beta, uint32_t lane, int64_t nreq,
+                          const expmc_level_req* req, expmc_level_stats* out);
+
+/* Per-sample functionals (LevelSampler::single / ::coupled, paths.cpp:99-141) for golden
+ * parity: sample i uses stream_for(req[i].seed, req[i].level, req[i].first_index, lane).
+ * base_level != 0 -> eta_fine = value, eta_coarse = 0.  req[i].count is ignored. */
+int expmc_sample_debug(expmc_ctx* ctx, double beta, uint32_t lane, int64_t nreq,
+                       const expmc_level_req* req, double* eta_fine, double* eta_coarse,
+                       uint64_t* cost, uint64_t* jumps, int64_t* end_state);
+
+/* mlmc_driver (mlmc.hpp:94; mlmc.cpp:170-260) for ONE entry, options->seed as the seed. */
+int expmc_mlmc_driver(expmc_ctx* ctx, int64_t entry, double beta, const expmc_options* options,
+                      expmc_result* out, expmc_level_record* levels, int32_t max_levels);
+
+/* mlmc_driver for nrows entries at once: row r runs the reference's Algorithm-1 decision
+ * sequence with seed row_seed[r]; all rows advance in lock-step rounds, each round one
+ * batched GPU pass.  levels: nrows x max_levels records (nullable). */
+int expmc_mlmc_driver_rows(expmc_ctx* ctx, double beta, const expmc_options* options,
+                           int64_t nrows, const int64_t* rows, const uint64_t* row_seed,
+                           expmc_result* out, expmc_level_record* levels, int32_t max_levels);
+
+/* Roofline denominator: random 32-B-sector gather throughput of `device` over a buffer of
+ * `bytes` (L2-resident or HBM-sized), `loads_per_thread` independent sector loads per thread,
+ * best of `reps` launches.  Writes achieved GB/s (32 B per load / kernel time). */
+int expmc_bench_gather(int device, uint64_t bytes, int32_t loads_per_thread, int32_t reps, double* gbps);
+
+/* Host-side driver helpers, identical to the reference (no GPU needed). */
+int expmc_initial_level(double beta, double d_max, int32_t* out);             /* mlmc.cpp:19-23 */
+int expmc_optimal_allocation(int64_t nlevels, const double* variances,        /* mlmc.cpp:25-43 */
+                             const double* unit_costs, double epsilon, uint64_t* out);
+int expmc_bias_estimate(int64_t n, const double* coupled_means, double* out); /* mlmc.cpp:45-51 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXPMC_B200_H */

@@ -1,0 +1,308 @@
+// TEST INFRASTRUCTURE ONLY -- never linked into the product.
+//
+// extern "C" shim over the UNMODIFIED reference library (/root/reference/proj/core),
+// compiled in place by oracle/Makefile into oracle/_ref/libexpmc_ref.so.  It lets the
+// Python tests, the golden-vector generator and bench.py's CPU baseline call the
+// reference's own code path:
+//   RngStream / stream_for          rng.hpp:21-79
+//   decompose                       chain.cpp:75 -> decompose_impl chain.cpp:15-71
+//   LevelSampler::single / coupled  paths.cpp:84-141
+//   run_level                       mlmc.cpp:163-168 (run_level_ex 76-148)
+//   mlmc_driver                     mlmc.cpp:170-260
+//   dense_expmv / strang_reference  oracle.cpp:31-60, 79-99
+//   smallw / pref                   netgen.cpp:30-107
+// Exceptions map to status codes: 1 invalid_argument, 2 out_of_range, 3 domain_error, 9 other.
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "expmc/chain.hpp"
+#include "expmc/mlmc.hpp"
+#include "expmc/netgen.hpp"
+#include "expmc/oracle.hpp"
+#include "expmc/paths.hpp"
+#include "expmc/rng.hpp"
+#include "expmc/sparse.hpp"
+
+using namespace expmc;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 9;
+    }
+}
+
+struct RefMatrix {
+    SparseMatrix a;
+    ChainDecomposition dec;
+};
+
+SparseMatrix from_csr(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val) {
+    std::vector<Triplet> trips;
+    trips.reserve(static_cast<std::size_t>(row_ptr[n]));
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) trips.push_back({i, col[k], val[k]});
+    return SparseMatrix::from_triplets(n, std::move(trips));
+}
+
+void export_csr(const SparseMatrix& m, int64_t* row_ptr, int64_t* col, double* val) {
+    const auto rp = m.row_ptr();
+    const auto ci = m.col_idx();
+    const auto vv = m.values();
+    std::memcpy(row_ptr, rp.data(), rp.size() * sizeof(int64_t));
+    std::memcpy(col, ci.data(), ci.size() * sizeof(int64_t));
+    std::memcpy(val, vv.data(), vv.size() * sizeof(double));
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_uniforms(uint64_t seed, uint32_t level, uint64_t sample, uint32_t lane, int64_t count,
+                  double* out) {
+    RngStream s = stream_for(seed, level, sample, lane);
+    for (int64_t i = 0; i < count; ++i) out[i] = s.next_uniform();
+}
+
+int ref_matrix_create(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                      void** out) {
+    return guarded([&] {
+        auto* m = new RefMatrix;
+        try {
+            m->a = from_csr(n, row_ptr, col, val);
+            m->dec = decompose(m->a);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+void ref_matrix_destroy(void* h) { delete static_cast<RefMatrix*>(h); }
+
+// sizes: n, nnz of the canonical CSR, number of chain edges
+void ref_matrix_sizes(void* h, int64_t* n, int64_t* nnz, int64_t* edges) {
+    auto* m = static_cast<RefMatrix*>(h);
+    *n = m->a.size();
+    *nnz = m->a.nnz();
+    *edges = static_cast<int64_t>(m->dec.jump_target.size());
+}
+
+void ref_matrix_csr(void* h, int64_t* row_ptr, int64_t* col, double* val) {
+    export_csr(static_cast<RefMatrix*>(h)->a, row_ptr, col, val);
+}
+
+void ref_matrix_decomposition(void* h, double* d, double* rate, int64_t* row_ptr, double* cdf,
+                              int64_t* target, uint8_t* sign, double* weight, double* d_max,
+                              double* d_bar) {
+    const ChainDecomposition& dec = static_cast<RefMatrix*>(h)->dec;
+    std::memcpy(d, dec.d.data(), dec.d.size() * sizeof(double));
+    std::memcpy(rate, dec.rate.data(), dec.rate.size() * sizeof(double));
+    std::memcpy(row_ptr, dec.row_ptr.data(), dec.row_ptr.size() * sizeof(int64_t));
+    std::memcpy(cdf, dec.jump_cdf.data(), dec.jump_cdf.size() * sizeof(double));
+    std::memcpy(target, dec.jump_target.data(), dec.jump_target.size() * sizeof(int64_t));
+    std::memcpy(sign, dec.sign.data(), dec.sign.size());
+    std::memcpy(weight, dec.jump_weight.data(), dec.jump_weight.size() * sizeof(double));
+    *d_max = dec.d_max;
+    *d_bar = dec.d_bar;
+}
+
+// Per-sample functionals through LevelSampler (paths.cpp:99-141), entry mode,
+// stream_for(seed, level, sample_idx[i], lane).  base != 0 -> single (value in fine,
+// coarse = 0), else coupled.
+int ref_samples(void* h, const double* u, int64_t entry, double beta, int level, int base,
+                uint64_t seed, uint32_t lane, int64_t count, const uint64_t* sample_idx,
+                double* fine, double* coarse, uint64_t* cost) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        const index_t steps = index_t{1} << level;
+        const double dt = beta / static_cast<double>(steps);
+        const LevelSampler sampler(m->dec, dt, steps);
+        const std::span<const double> uu(u, static_cast<std::size_t>(m->dec.n));
+        for (int64_t i = 0; i < count; ++i) {
+            RngStream s = stream_for(seed, static_cast<uint32_t>(level), sample_idx[i], lane);
+            if (base) {
+                const FunctionalSample f = sampler.single(uu, entry, s);
+                fine[i] = f.value;
+                coarse[i] = 0.0;
+                cost[i] = f.cost;
+            } else {
+                const CoupledSample c = sampler.coupled(uu, entry, s);
+                fine[i] = c.eta_fine;
+                coarse[i] = c.eta_coarse;
+                cost[i] = c.cost;
+            }
+        }
+    });
+}
+
+// run_level (mlmc.hpp:86-88), entry mode.
+int ref_run_level(void* h, const double* u, int64_t entry, double beta, int level, int base,
+                  uint64_t first, uint64_t count, uint64_t seed, int threads, double* sum,
+                  double* sum_sq, uint64_t* samples, uint64_t* cost) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.entry = entry;
+        p.beta = beta;
+        const LevelStats st = run_level(p, level, base != 0, first, count, seed, threads);
+        *sum = st.sum;
+        *sum_sq = st.sum_sq;
+        *samples = st.samples;
+        *cost = st.cost;
+    });
+}
+
+struct RefOptions {
+    double epsilon;
+    uint64_t seed;
+    int32_t threads;
+    int32_t l0_override;
+    uint64_t warmup;
+    int32_t max_levels_above_l0;
+    int32_t max_iterations;
+};
+
+struct RefResult {
+    double estimate;
+    double statistical_error;
+    double bias_estimate;
+    int32_t l0;
+    int32_t L;
+    uint64_t total_cost;
+    int32_t converged;
+    int32_t nlevels;
+};
+
+struct RefLevel {
+    int32_t level;
+    int32_t pad;
+    double sum;
+    double sum_sq;
+    uint64_t samples;
+    uint64_t cost;
+};
+
+// mlmc_driver (mlmc.cpp:170-260) for each row of `rows`, row r with seed row_seed[r].
+// levels_out: nrows x max_levels records (nullable).
+int ref_mlmc_driver_rows(void* h, const double* u, double beta, const RefOptions* o, int64_t nrows,
+                         const int64_t* rows, const uint64_t* row_seed, RefResult* out,
+                         RefLevel* levels_out, int32_t max_levels) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.beta = beta;
+        MlmcOptions opt;
+        opt.epsilon = o->epsilon;
+        opt.threads = o->threads;
+        opt.l0_override = o->l0_override;
+        opt.warmup = o->warmup;
+        opt.max_levels_above_l0 = o->max_levels_above_l0;
+        opt.max_iterations = o->max_iterations;
+        for (int64_t r = 0; r < nrows; ++r) {
+            p.entry = rows[r];
+            opt.seed = row_seed[r];
+            const MlmcResult res = mlmc_driver(p, opt);
+            RefResult& q = out[r];
+            q.estimate = res.estimate;
+            q.statistical_error = res.statistical_error;
+            q.bias_estimate = res.bias_estimate;
+            q.l0 = res.l0;
+            q.L = res.L;
+            q.total_cost = res.total_cost;
+            q.converged = res.converged ? 1 : 0;
+            q.nlevels = static_cast<int32_t>(res.levels.size());
+            if (levels_out) {
+                for (std::size_t l = 0; l < res.levels.size() && l < static_cast<std::size_t>(max_levels); ++l) {
+                    RefLevel& lv = levels_out[r * max_levels + static_cast<int64_t>(l)];
+                    lv.level = res.levels[l].level;
+                    lv.pad = 0;
+                    lv.sum = res.levels[l].sum;
+                    lv.sum_sq = res.levels[l].sum_sq;
+                    lv.samples = res.levels[l].samples;
+                    lv.cost = res.levels[l].cost;
+                }
+            }
+        }
+    });
+}
+
+int ref_initial_level(double beta, double d_max, int* out) {
+    return guarded([&] { *out = initial_level(beta, d_max); });
+}
+
+int ref_optimal_allocation(int64_t n, const double* v, const double* c, double eps, uint64_t* out) {
+    return guarded([&] {
+        const auto m = optimal_allocation(std::span<const double>(v, static_cast<std::size_t>(n)),
+                                          std::span<const double>(c, static_cast<std::size_t>(n)), eps);
+        for (std::size_t i = 0; i < m.size(); ++i) out[i] = m[i];
+    });
+}
+
+int ref_bias_estimate(int64_t n, const double* means, double* out) {
+    return guarded([&] { *out = bias_estimate(std::span<const double>(means, static_cast<std::size_t>(n))); });
+}
+
+int ref_dense_expmv(void* h, const double* u, double beta, double* out) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        const auto x = dense_expmv(m->a, std::span<const double>(u, static_cast<std::size_t>(m->a.size())), beta);
+        std::memcpy(out, x.data(), x.size() * sizeof(double));
+    });
+}
+
+int ref_strang_reference(void* h, const double* u, double beta, int64_t steps, double* out) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        const auto x = strang_reference(m->dec, std::span<const double>(u, static_cast<std::size_t>(m->dec.n)), beta, steps);
+        std::memcpy(out, x.data(), x.size() * sizeof(double));
+    });
+}
+
+// Graph generators (netgen.cpp): returns a matrix handle.
+int ref_pref(int64_t n, int64_t d, uint64_t seed, void** out) {
+    return guarded([&] {
+        auto* m = new RefMatrix;
+        m->a = pref(n, d, seed);
+        m->dec = decompose(m->a);
+        *out = m;
+    });
+}
+
+int ref_smallw(int64_t n, int64_t k, double p, uint64_t seed, void** out) {
+    return guarded([&] {
+        auto* m = new RefMatrix;
+        m->a = smallw(n, k, p, seed);
+        m->dec = decompose(m->a);
+        *out = m;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,32 @@
+"""B200-native MLMC random-walk estimator for e^{tA}v (hot path of arXiv 1904.12754).
+
+The compute path is the in-tree CUDA library ``_lib/libexpmc_b200.so`` (sm_100a) behind the
+C-ABI ``include/expmc_b200.h``; this package is its Python host mirror of the reference's
+C++ API (``api``) plus the synthetic config inputs (``configs``).  Importing it fails loudly
+when the library has not been built: there is no CPU fallback.
+"""
+from .api import (  # noqa: F401
+    Context,
+    CudaError,
+    DomainError,
+    ExpmcError,
+    InvalidArgument,
+    LevelStats,
+    MlmcOptions,
+    MlmcProblem,
+    MlmcResult,
+    NotImplementedMode,
+    OutOfRange,
+    SparseMatrix,
+    bench_gather,
+    bias_estimate,
+    device_count,
+    initial_level,
+    mlmc_driver,
+    mlmc_driver_rows,
+    optimal_allocation,
+    run_level,
+    version,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,406 @@
+"""Host API mirroring the reference's C++ interface for the MLMC path (names, argument
+meaning and error behaviour of expmc::run_level / mlmc_driver, mlmc.hpp:15-98), backed by the
+CUDA library through the C-ABI (include/expmc_b200.h).
+
+    reference (C++)                               here (Python over the C-ABI)
+    ---------------------------------------       -------------------------------------------
+    SparseMatrix::from_triplets (sparse.cpp:12)   SparseMatrix.from_triplets
+    decompose(A) (chain.cpp:75)                   Context(A, u, device)  (tables built on GPU)
+    MlmcProblem{dec, u, entry, beta} (mlmc.hpp:50) MlmcProblem(ctx, entry, beta)
+    run_level(p, l, base, first, add, seed)       run_level(p, l, base, first, add, seed)
+    mlmc_driver(p, opts) (mlmc.cpp:170)           mlmc_driver(p, opts)
+    --                                            mlmc_driver_rows(ctx, beta, rows, seeds, opts)
+    initial_level / optimal_allocation /          initial_level / optimal_allocation /
+      bias_estimate (mlmc.cpp:19-51)                bias_estimate (same host C++ as the driver)
+
+Exceptions: std::invalid_argument -> InvalidArgument(ValueError), std::out_of_range ->
+OutOfRange(IndexError), std::domain_error -> DomainError(ArithmeticError); CUDA failures ->
+CudaError.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+class ExpmcError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ExpmcError, ValueError):
+    pass
+
+
+class OutOfRange(ExpmcError, IndexError):
+    pass
+
+
+class DomainError(ExpmcError, ArithmeticError):
+    pass
+
+
+class CudaError(ExpmcError):
+    pass
+
+
+class NotImplementedMode(ExpmcError, NotImplementedError):
+    pass
+
+
+_ERR = {L.EXPMC_EINVAL: InvalidArgument, L.EXPMC_ERANGE: OutOfRange, L.EXPMC_EDOMAIN: DomainError,
+        L.EXPMC_ECUDA: CudaError, L.EXPMC_ENOTIMPL: NotImplementedMode}
+
+
+def _check(rc: int) -> None:
+    if rc != L.EXPMC_OK:
+        raise _ERR.get(rc, ExpmcError)(L.lib.expmc_last_error().decode())
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def version() -> str:
+    return L.lib.expmc_version().decode()
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(L.lib.expmc_device_count(C.byref(n)))
+    return n.value
+
+
+# --------------------------------------------------------------------------------- matrices
+@dataclass
+class SparseMatrix:
+    """Canonical CSR as expmc::SparseMatrix stores it (sparse.hpp:21-75)."""
+
+    n: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1]) if len(self.row_ptr) else 0
+
+    @staticmethod
+    def from_triplets(n: int, rows, cols, vals) -> "SparseMatrix":
+        """sparse.cpp:12-49: indices checked (out_of_range), values finite (invalid_argument),
+        sorted by (row, col), duplicates summed in input order, zero sums dropped."""
+        if n < 0:
+            raise InvalidArgument("matrix dimension must be nonnegative")
+        r = np.asarray(rows, np.int64)
+        c = np.asarray(cols, np.int64)
+        v = np.asarray(vals, np.float64)
+        if r.size and (r.min() < 0 or r.max() >= n or c.min() < 0 or c.max() >= n):
+            raise OutOfRange("triplet index outside [0, n)")
+        if v.size and not np.isfinite(v).all():
+            raise InvalidArgument("matrix entry is NaN or Inf")
+        order = np.lexsort((c, r))  # stable: duplicates keep input order
+        r, c, v = r[order], c[order], v[order]
+        if r.size:
+            key = r * n + c
+            start = np.flatnonzero(np.r_[True, key[1:] != key[:-1]])
+            # sequential summation of each duplicate run, left to right (sparse.cpp:33-37)
+            sums = v[start].copy()
+            dup = np.flatnonzero(np.diff(np.r_[start, key.size]) > 1)
+            for g in dup:
+                s = v[start[g]]
+                for k in range(start[g] + 1, (start[g + 1] if g + 1 < start.size else key.size)):
+                    s = s + v[k]
+                sums[g] = s
+            keep = sums != 0.0
+            r, c, v = r[start][keep], c[start][keep], sums[keep]
+        rp = np.zeros(n + 1, np.int64)
+        np.add.at(rp, r + 1, 1)
+        return SparseMatrix(n, np.cumsum(rp).astype(np.int64), c.astype(np.int64), v.astype(np.float64))
+
+    @staticmethod
+    def from_dense(d) -> "SparseMatrix":
+        d = np.asarray(d, np.float64)
+        r, c = np.nonzero(d)
+        return SparseMatrix.from_triplets(d.shape[0], r, c, d[r, c])
+
+    @staticmethod
+    def identity(n: int) -> "SparseMatrix":
+        i = np.arange(n)
+        return SparseMatrix.from_triplets(n, i, i, np.ones(n))
+
+    def transposed(self) -> "SparseMatrix":
+        r = np.repeat(np.arange(self.n, dtype=np.int64), np.diff(self.row_ptr))
+        return SparseMatrix.from_triplets(self.n, self.col, r, self.val)
+
+    def multiply(self, x):
+        x = np.asarray(x, np.float64)
+        r = np.repeat(np.arange(self.n), np.diff(self.row_ptr))
+        y = np.zeros(self.n)
+        np.add.at(y, r, self.val * x[self.col])
+        return y
+
+
+# --------------------------------------------------------------------------------- stats
+@dataclass
+class LevelStats:
+    """mlmc.hpp:18-31 (+ jumps: accepted CTMC transitions)."""
+
+    level: int = 0
+    sum: float = 0.0
+    sum_sq: float = 0.0
+    samples: int = 0
+    cost: int = 0
+    jumps: int = 0
+
+    def mean(self) -> float:
+        return self.sum / self.samples if self.samples else 0.0
+
+    def variance(self) -> float:  # mlmc.cpp:13-17
+        if self.samples < 2:
+            return 0.0
+        m = self.mean()
+        return max(0.0, self.sum_sq / self.samples - m * m)
+
+    def unit_cost(self) -> float:
+        return self.cost / self.samples if self.samples else 0.0
+
+
+@dataclass
+class MlmcOptions:
+    """mlmc.hpp:59-67."""
+
+    epsilon: float = 1e-3
+    seed: int = 0
+    threads: int = 0
+    l0_override: int = -1
+    warmup: int = 1000
+    max_levels_above_l0: int = 30
+    max_iterations: int = 200
+
+    def _c(self) -> L.OptionsC:
+        return L.OptionsC(self.epsilon, self.seed, self.threads, self.l0_override, self.warmup,
+                          self.max_levels_above_l0, self.max_iterations)
+
+
+@dataclass
+class MlmcResult:
+    """mlmc.hpp:33-43 (+ total_jumps / total_samples)."""
+
+    estimate: float = 0.0
+    statistical_error: float = 0.0
+    bias_estimate: float = 0.0
+    quadrature_bound: float = 0.0
+    levels: list = field(default_factory=list)
+    l0: int = 0
+    L: int = 0
+    total_cost: int = 0
+    converged: bool = False
+    total_jumps: int = 0
+    total_samples: int = 0
+
+
+# --------------------------------------------------------------------------------- context
+class Context:
+    """Device-resident sampling tables of A plus the bound vector u on one GPU
+    (decompose + LevelSampler tables + MlmcProblem::u)."""
+
+    def __init__(self, a: SparseMatrix, u, device: int = 0):
+        self._h = C.c_void_p()
+        u = np.ascontiguousarray(u, np.float64)
+        if u.shape != (a.n,):
+            raise InvalidArgument("vector length does not match decomposition")
+        rp = np.ascontiguousarray(a.row_ptr, np.int64)
+        col = np.ascontiguousarray(a.col, np.int64)
+        val = np.ascontiguousarray(a.val, np.float64)
+        csr = L.Csr(a.n, int(rp[-1]) if len(rp) else 0, _ptr(rp), _ptr(col), _ptr(val))
+        _check(L.lib.expmc_ctx_create(C.byref(csr), _ptr(u), device, C.byref(self._h)))
+        info = L.CtxInfo()
+        _check(L.lib.expmc_ctx_get_info(self._h, C.byref(info)))
+        self.n = info.n
+        self.n_edges = info.n_edges
+        self.d_max = info.d_max
+        self.d_bar = info.d_bar
+        self.device = info.device
+        self.num_sms = info.num_sms
+        self.table_bytes = info.table_bytes
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            L.lib.expmc_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_vector(self, u):
+        u = np.ascontiguousarray(u, np.float64)
+        if u.shape != (self.n,):
+            raise InvalidArgument("vector length does not match decomposition")
+        _check(L.lib.expmc_ctx_set_vector(self._h, _ptr(u)))
+
+    def decomposition(self) -> dict:
+        n, m = self.n, self.n_edges
+        d, rate = np.empty(n), np.empty(n)
+        rp = np.empty(n + 1, np.int64)
+        cdf, tgt, sign = np.empty(m), np.empty(m, np.int64), np.empty(m, np.uint8)
+        _check(L.lib.expmc_ctx_export_tables(self._h, _ptr(d), _ptr(rate), _ptr(rp), _ptr(cdf), _ptr(tgt), _ptr(sign)))
+        return dict(d=d, rate=rate, row_ptr=rp, jump_cdf=cdf, jump_target=tgt, sign=sign, d_max=self.d_max,
+                    d_bar=self.d_bar)
+
+    def counters(self) -> dict:
+        c = L.CountersC()
+        _check(L.lib.expmc_ctx_get_counters(self._h, C.byref(c)))
+        return {k: getattr(c, k) for k, _ in L.CountersC._fields_}
+
+    @property
+    def stream_ptr(self) -> int:
+        """cudaStream_t the sampler kernels run on (for CUDA-event timing on that stream)."""
+        p = C.c_void_p()
+        _check(L.lib.expmc_ctx_get_stream(self._h, C.byref(p)))
+        return p.value or 0
+
+    def reset_counters(self):
+        _check(L.lib.expmc_ctx_reset_counters(self._h))
+
+    # ---- batched primitives
+    def run_level_batch(self, beta: float, entry, level, base_level, first_index, count, seed) -> np.ndarray:
+        """Vectorised run_level: every argument broadcasts to the request count.  Returns a
+        structured array (sum, sum_sq, samples, cost, jumps)."""
+        e, lv, b, f, c, s = np.broadcast_arrays(np.asarray(entry, np.int64), np.asarray(level, np.int32),
+                                                np.asarray(base_level, np.int32), np.asarray(first_index, np.uint64),
+                                                np.asarray(count, np.uint64), np.asarray(seed, np.uint64))
+        k = e.size
+        req = np.zeros(k, _REQ_DT)
+        req["entry"], req["seed"], req["first_index"] = e.ravel(), s.ravel(), f.ravel()
+        req["count"], req["level"], req["base_level"] = c.ravel(), lv.ravel(), b.ravel()
+        out = np.zeros(k, _STATS_DT)
+        _check(L.lib.expmc_run_level_batch(self._h, beta, L.LANE_ENTRY, k, _ptr(req), _ptr(out)))
+        return out
+
+    def sample_debug(self, beta: float, entry, level, base_level, seed, sample_idx) -> dict:
+        e, lv, b, s, i = np.broadcast_arrays(np.asarray(entry, np.int64), np.asarray(level, np.int32),
+                                             np.asarray(base_level, np.int32), np.asarray(seed, np.uint64),
+                                             np.asarray(sample_idx, np.uint64))
+        k = e.size
+        req = np.zeros(k, _REQ_DT)
+        req["entry"], req["seed"], req["first_index"] = e.ravel(), s.ravel(), i.ravel()
+        req["count"], req["level"], req["base_level"] = 1, lv.ravel(), b.ravel()
+        fine, coarse = np.empty(k), np.empty(k)
+        cost, jumps, end = np.empty(k, np.uint64), np.empty(k, np.uint64), np.empty(k, np.int64)
+        _check(L.lib.expmc_sample_debug(self._h, beta, L.LANE_ENTRY, k, _ptr(req), _ptr(fine), _ptr(coarse),
+                                        _ptr(cost), _ptr(jumps), _ptr(end)))
+        return dict(fine=fine, coarse=coarse, cost=cost, jumps=jumps, end_state=end)
+
+
+_REQ_DT = np.dtype([("entry", np.int64), ("seed", np.uint64), ("first_index", np.uint64), ("count", np.uint64),
+                    ("level", np.int32), ("base_level", np.int32)])
+_STATS_DT = np.dtype([("sum", np.float64), ("sum_sq", np.float64), ("samples", np.uint64), ("cost", np.uint64),
+                      ("jumps", np.uint64)])
+_RESULT_DT = np.dtype([("estimate", np.float64), ("statistical_error", np.float64), ("bias_estimate", np.float64),
+                       ("l0", np.int32), ("L", np.int32), ("total_cost", np.uint64), ("converged", np.int32),
+                       ("nlevels", np.int32), ("total_jumps", np.uint64), ("total_samples", np.uint64)])
+LEVEL_RECORD_DT = np.dtype([("level", np.int32), ("pad", np.int32), ("sum", np.float64), ("sum_sq", np.float64),
+                            ("samples", np.uint64), ("cost", np.uint64)])
+assert _REQ_DT.itemsize == C.sizeof(L.LevelReq)
+assert _STATS_DT.itemsize == C.sizeof(L.LevelStatsC)
+assert _RESULT_DT.itemsize == C.sizeof(L.ResultC)
+assert LEVEL_RECORD_DT.itemsize == C.sizeof(L.LevelRecordC)
+
+
+@dataclass
+class MlmcProblem:
+    """mlmc.hpp:50-57, entry mode: the context carries dec and u."""
+
+    ctx: Context
+    entry: int = 0
+    beta: float = 1.0
+
+
+def run_level(problem: MlmcProblem, level: int, base_level: bool, first_index: int, additional: int,
+              seed: int, threads: int = 0) -> LevelStats:
+    """mlmc.hpp:86-88."""
+    out = L.LevelStatsC()
+    _check(L.lib.expmc_run_level(problem.ctx.handle, problem.entry, problem.beta, level, int(bool(base_level)),
+                                 first_index, additional, seed, C.byref(out)))
+    return LevelStats(level, out.sum, out.sum_sq, out.samples, out.cost, out.jumps)
+
+
+def _result(r, levels) -> MlmcResult:
+    lv = [LevelStats(int(x["level"]), float(x["sum"]), float(x["sum_sq"]), int(x["samples"]), int(x["cost"]))
+          for x in levels]
+    return MlmcResult(float(r["estimate"]), float(r["statistical_error"]), float(r["bias_estimate"]), 0.0, lv,
+                      int(r["l0"]), int(r["L"]), int(r["total_cost"]), bool(r["converged"]), int(r["total_jumps"]),
+                      int(r["total_samples"]))
+
+
+def mlmc_driver(problem: MlmcProblem, options: MlmcOptions = MlmcOptions(), max_levels: int = 64) -> MlmcResult:
+    """mlmc.hpp:94, mlmc.cpp:170-260."""
+    res = np.zeros(1, _RESULT_DT)
+    lv = np.zeros(max_levels, LEVEL_RECORD_DT)
+    o = options._c()
+    _check(L.lib.expmc_mlmc_driver(problem.ctx.handle, problem.entry, problem.beta, C.byref(o),
+                                   C.cast(_ptr(res), C.POINTER(L.ResultC)), _ptr(lv), max_levels))
+    return _result(res[0], lv[: int(res[0]["nlevels"])])
+
+
+def mlmc_driver_rows(ctx: Context, beta: float, rows, row_seeds, options: MlmcOptions = MlmcOptions(),
+                     max_levels: int = 64, want_levels: bool = True):
+    """All-components estimator: one reference mlmc_driver decision sequence per row, all rows
+    batched on the GPU.  Returns (results structured array, levels [nrows, max_levels] or None)."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    seeds = np.ascontiguousarray(row_seeds, np.uint64)
+    if seeds.shape != rows.shape:
+        raise InvalidArgument("one seed per row required")
+    res = np.zeros(rows.size, _RESULT_DT)
+    lv = np.zeros((rows.size, max_levels), LEVEL_RECORD_DT) if want_levels else None
+    o = options._c()
+    _check(L.lib.expmc_mlmc_driver_rows(ctx.handle, beta, C.byref(o), rows.size, _ptr(rows), _ptr(seeds), _ptr(res),
+                                        _ptr(lv), max_levels))
+    return res, lv
+
+
+def bench_gather(device: int, nbytes: int, loads_per_thread: int = 64, reps: int = 5) -> float:
+    """Random 32-B sector gather throughput (GB/s) over an nbytes buffer: the roofline
+    denominator of the sampler's table reads."""
+    out = C.c_double()
+    _check(L.lib.expmc_bench_gather(device, nbytes, loads_per_thread, reps, C.byref(out)))
+    return out.value
+
+
+def initial_level(beta: float, d_max: float) -> int:
+    out = C.c_int32()
+    _check(L.lib.expmc_initial_level(beta, d_max, C.byref(out)))
+    return out.value
+
+
+def optimal_allocation(variances, unit_costs, epsilon: float) -> np.ndarray:
+    v = np.ascontiguousarray(variances, np.float64)
+    c = np.ascontiguousarray(unit_costs, np.float64)
+    if v.shape != c.shape:
+        raise InvalidArgument("variance and cost arrays differ in length")
+    out = np.empty(v.size, np.uint64)
+    _check(L.lib.expmc_optimal_allocation(v.size, _ptr(v), _ptr(c), epsilon, _ptr(out)))
+    return out
+
+
+def bias_estimate(coupled_means) -> float:
+    m = np.ascontiguousarray(coupled_means, np.float64)
+    out = C.c_double()
+    _check(L.lib.expmc_bias_estimate(m.size, _ptr(m), C.byref(out)))
+    return out.value

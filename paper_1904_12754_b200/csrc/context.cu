@@ -1,0 +1,506 @@
+// C-ABI: device context (tables), batched run_level, per-sample debug path.
+//
+// expmc_ctx_create      <- decompose (chain.cpp:75) + LevelSampler tables (paths.cpp:84-91)
+// expmc_run_level[_batch] <- run_level / run_level_ex (mlmc.hpp:86-88, mlmc.cpp:76-168)
+// expmc_sample_debug    <- LevelSampler::single / ::coupled per sample (paths.cpp:99-141)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+using namespace expmc_b200;
+
+struct expmc_ctx {
+    int device = 0;
+    int num_sms = 0;
+    int sampler_grid = 0;
+    cudaStream_t stream = nullptr;
+    int64_t n = 0;
+    uint64_t nedges = 0;
+    double d_max = 0.0, d_bar = 0.0;
+    RowRec* rows = nullptr;
+    EdgeRec* edges = nullptr;
+
+    // batch buffers (grown on demand)
+    DevItem* d_items = nullptr;
+    uint64_t* d_chunk0 = nullptr;
+    Partial* d_totals = nullptr;
+    size_t cap_items = 0;
+    DevItem* h_items = nullptr;  // pinned
+    uint64_t* h_chunk0 = nullptr;
+    Partial* h_totals = nullptr;
+    size_t cap_h = 0;
+    Partial* d_partials = nullptr;
+    uint64_t cap_partials = 0;
+    unsigned* d_counter = nullptr;
+    SampleOut* d_dbg = nullptr;
+    size_t cap_dbg = 0;
+
+    std::vector<cudaEvent_t> ev;
+    expmc_counters ctr{};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+constexpr uint64_t kWindowChunks = uint64_t{1} << 22;  // chunk partials per sampler launch (128 MB)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return EXPMC_OK;
+    } catch (const Status& s) {
+        g_err = s.what();
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return EXPMC_EINTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return EXPMC_EINTERNAL;
+    }
+}
+
+void need(bool ok, int code, const char* msg) {
+    if (!ok) throw Status(code, msg);
+}
+
+template <class T>
+void dev_alloc(T** p, size_t count) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+}
+
+template <class T>
+void host_alloc(T** p, size_t count) {
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    cuda_check(cudaMallocHost(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)), "cudaMallocHost");
+}
+
+void ensure_items(expmc_ctx* c, size_t nitems) {
+    if (nitems + 1 > c->cap_items) {
+        const size_t cap = std::max<size_t>(nitems + 1, c->cap_items * 2);
+        dev_alloc(&c->d_items, cap);
+        dev_alloc(&c->d_chunk0, cap);
+        dev_alloc(&c->d_totals, cap);
+        c->cap_items = cap;
+    }
+    if (nitems + 1 > c->cap_h) {
+        const size_t cap = std::max<size_t>(nitems + 1, c->cap_h * 2);
+        host_alloc(&c->h_items, cap);
+        host_alloc(&c->h_chunk0, cap);
+        host_alloc(&c->h_totals, cap);
+        c->cap_h = cap;
+    }
+}
+
+void bind(const expmc_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+DevItem make_item(const expmc_level_req& r, double beta, uint32_t lane) {
+    DevItem it{};
+    const uint64_t steps = uint64_t{1} << r.level;
+    it.seed = r.seed;
+    it.first = r.first_index;
+    it.count = r.count;
+    it.dt = beta / static_cast<double>(steps);  // mlmc.cpp:81
+    it.nsteps = steps;
+    it.entry = static_cast<uint32_t>(r.entry);
+    it.key3 = (static_cast<uint32_t>(r.level) & 0xFFFFFFu) | (lane << 24);  // rng.hpp:29
+    it.base = r.base_level ? 1u : 0u;
+    return it;
+}
+
+// validate_problem (mlmc.cpp:150-159) + run_level_ex's level check (mlmc.cpp:79) + the
+// coupled even-step check (paths.cpp:119).
+void validate_req(const expmc_ctx* c, const expmc_level_req& r, double beta) {
+    need(r.entry >= 0 && r.entry < c->n, EXPMC_ERANGE, "entry index outside matrix");
+    need(beta > 0.0, EXPMC_EINVAL, "beta must be positive");
+    need(r.level >= 0 && r.level <= 62, EXPMC_EINVAL, "level outside [0, 62]");
+    need(beta / static_cast<double>(uint64_t{1} << r.level) > 0.0, EXPMC_EINVAL, "step size must be positive");
+    if (!r.base_level && r.level == 0 && r.count > 0)
+        throw Status(EXPMC_EINVAL, "coupled sampling needs an even step count");
+}
+
+}  // namespace
+
+namespace expmc_b200 {
+
+void set_error(const std::string& m) { g_err = m; }
+
+void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
+                     expmc_level_stats* out) {
+    bind(c);
+    std::vector<int64_t> slot;  // request index of each item
+    slot.reserve(static_cast<size_t>(nreq));
+    for (int64_t i = 0; i < nreq; ++i) {
+        validate_req(c, req[i], beta);
+        out[i] = expmc_level_stats{0.0, 0.0, 0, 0, 0};
+        if (req[i].count > 0) slot.push_back(i);
+    }
+    const size_t nitems = slot.size();
+    if (nitems == 0) return;
+    c->ctr.rounds += 1;
+    need(nitems < (size_t{1} << 31), EXPMC_EINVAL, "too many run_level requests in one batch");
+    ensure_items(c, nitems);
+    uint64_t total = 0;
+    for (size_t k = 0; k < nitems; ++k) {
+        const expmc_level_req& r = req[slot[k]];
+        c->h_items[k] = make_item(r, beta, lane);
+        c->h_chunk0[k] = total;
+        const uint64_t first_chunk = r.first_index / kChunk;
+        const uint64_t last_chunk = (r.first_index + r.count - 1) / kChunk;  // parallel.hpp:36-38
+        total += last_chunk - first_chunk + 1;
+    }
+    c->h_chunk0[nitems] = total;
+    cuda_check(cudaMemcpyAsync(c->d_items, c->h_items, nitems * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
+               "H2D items");
+    cuda_check(cudaMemcpyAsync(c->d_chunk0, c->h_chunk0, (nitems + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                               c->stream),
+               "H2D chunk0");
+    c->ctr.h2d_bytes += nitems * sizeof(DevItem) + (nitems + 1) * sizeof(uint64_t);
+    cuda_check(cudaMemsetAsync(c->d_totals, 0, nitems * sizeof(Partial), c->stream), "memset totals");
+    if (!c->d_partials) {
+        c->cap_partials = kWindowChunks;
+        dev_alloc(&c->d_partials, c->cap_partials);
+        dev_alloc(&c->d_counter, 1);
+    }
+    const int warps_per_block = sampler_threads() / 32;
+    size_t nev = 0;
+    for (uint64_t g0 = 0; g0 < total; g0 += c->cap_partials) {
+        const uint64_t g1 = std::min(total, g0 + c->cap_partials);
+        cuda_check(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), c->stream), "memset counter");
+        SamplerArgs a;
+        a.rows = c->rows;
+        a.edges = c->edges;
+        a.items = c->d_items;
+        a.chunk0 = c->d_chunk0;
+        a.nitems = static_cast<uint32_t>(nitems);
+        a.g_begin = g0;
+        a.g_end = g1;
+        a.partials = c->d_partials;
+        a.counter = c->d_counter;
+        const uint64_t want_blocks = (g1 - g0 + warps_per_block - 1) / warps_per_block;
+        const int grid = static_cast<int>(std::min<uint64_t>(c->sampler_grid, want_blocks));
+        while (c->ev.size() < 2 * (nev + 1)) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+            c->ev.push_back(e);
+        }
+        cuda_check(cudaEventRecord(c->ev[2 * nev], c->stream), "event");
+        launch_sampler(a, grid, c->stream);
+        cuda_check(cudaEventRecord(c->ev[2 * nev + 1], c->stream), "event");
+        ++nev;
+        launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, c->d_partials, c->d_totals, c->stream);
+        c->ctr.kernel_launches += 2;
+        c->ctr.sampler_launches += 1;
+    }
+    cuda_check(cudaMemcpyAsync(c->h_totals, c->d_totals, nitems * sizeof(Partial), cudaMemcpyDeviceToHost, c->stream),
+               "D2H totals");
+    c->ctr.d2h_bytes += nitems * sizeof(Partial);
+    cuda_check(cudaStreamSynchronize(c->stream), "sampler");
+    for (size_t k = 0; k < nev; ++k) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, c->ev[2 * k], c->ev[2 * k + 1]), "event time");
+        c->ctr.sampler_ms += ms;
+    }
+    for (size_t k = 0; k < nitems; ++k) {
+        const expmc_level_req& r = req[slot[k]];
+        expmc_level_stats& o = out[slot[k]];
+        o.sum = c->h_totals[k].sum;
+        o.sum_sq = c->h_totals[k].sum_sq;
+        o.samples = r.count;
+        o.cost = c->h_totals[k].cost;
+        o.jumps = c->h_totals[k].jumps;
+        c->ctr.samples += r.count;
+        c->ctr.jumps += o.jumps;
+        c->ctr.fine_steps += r.count << r.level;
+    }
+}
+
+}  // namespace expmc_b200
+
+extern "C" {
+
+const char* expmc_last_error(void) { return g_err.c_str(); }
+
+const char* expmc_version(void) { return "expmc_b200 0.1.0 (sm_100a, reference-order sampler)"; }
+
+int expmc_device_count(int* out) {
+    return guarded([&] {
+        const cudaError_t e = cudaGetDeviceCount(out);
+        if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {  // CPU-only host: zero devices
+            cudaGetLastError();
+            *out = 0;
+            return;
+        }
+        cuda_check(e, "cudaGetDeviceCount");
+    });
+}
+
+int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx** out) {
+    return guarded([&] {
+        need(A != nullptr && out != nullptr, EXPMC_EINVAL, "null argument");
+        const int64_t n = A->n;
+        need(n >= 0, EXPMC_EINVAL, "matrix dimension must be nonnegative");
+        need(n < (int64_t{1} << 31), EXPMC_EINVAL, "matrix dimension must be < 2^31");
+        need(n == 0 || (A->row_ptr && u), EXPMC_EINVAL, "null CSR or vector");
+        if (n > 0) {
+            need(A->row_ptr[0] == 0 && A->row_ptr[n] == A->nnz && A->nnz >= 0, EXPMC_EINVAL,
+                 "CSR row_ptr must start at 0 and end at nnz");
+            need(A->nnz == 0 || (A->col && A->val), EXPMC_EINVAL, "null CSR arrays");
+        }
+        auto* c = new expmc_ctx;
+        try {
+            c->device = device;
+            bind(c);
+            cuda_check(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
+            cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+            c->sampler_grid = c->num_sms * sampler_blocks_per_sm();
+            c->n = n;
+            if (n > 0) {
+                const int64_t nnz = A->nnz;
+                int64_t *d_rp = nullptr, *d_col = nullptr;
+                double *d_val = nullptr, *d_u = nullptr, *d_st = nullptr;
+                uint64_t *d_deg = nullptr, *d_begin = nullptr;
+                unsigned* d_err = nullptr;
+                void* tmp = nullptr;
+                auto cleanup = [&] {
+                    cudaFree(d_rp); cudaFree(d_col); cudaFree(d_val); cudaFree(d_u);
+                    cudaFree(d_deg); cudaFree(d_begin); cudaFree(d_err); cudaFree(tmp); cudaFree(d_st);
+                };
+                try {
+                    dev_alloc(&d_rp, n + 1);
+                    dev_alloc(&d_col, nnz);
+                    dev_alloc(&d_val, nnz);
+                    dev_alloc(&d_u, n);
+                    dev_alloc(&d_deg, n);
+                    dev_alloc(&d_begin, n);
+                    dev_alloc(&d_err, 1);
+                    dev_alloc(&d_st, 2);
+                    cuda_check(cudaMemcpyAsync(d_rp, A->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream), "H2D");
+                    if (nnz) {
+                        cuda_check(cudaMemcpyAsync(d_col, A->col, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream), "H2D");
+                        cuda_check(cudaMemcpyAsync(d_val, A->val, nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+                    }
+                    cuda_check(cudaMemcpyAsync(d_u, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+                    c->ctr.h2d_bytes += (n + 1) * 8 + nnz * 16 + n * 8;
+                    cuda_check(cudaMemsetAsync(d_err, 0, sizeof(unsigned), c->stream), "memset");
+                    launch_count_edges(n, d_rp, d_col, d_val, d_deg, d_err, c->stream);
+                    unsigned err = 0;
+                    cuda_check(cudaMemcpyAsync(&err, d_err, sizeof err, cudaMemcpyDeviceToHost, c->stream), "D2H");
+                    cuda_check(cudaStreamSynchronize(c->stream), "count edges");
+                    need(!(err & 2u), EXPMC_ERANGE, "triplet index outside [0, n)");
+                    need(!(err & 1u), EXPMC_EINVAL, "matrix entry is NaN or Inf");
+                    need(!(err & 4u), EXPMC_EINVAL, "CSR is not canonical (sorted, duplicate-free columns)");
+                    const size_t tb = std::max(scan_temp_bytes(n), dstat_temp_bytes(n));
+                    cuda_check(cudaMalloc(&tmp, tb), "cudaMalloc");
+                    exclusive_scan_u64(d_deg, d_begin, n, tmp, tb, c->stream);
+                    uint64_t last[2];
+                    cuda_check(cudaMemcpyAsync(&last[0], d_begin + (n - 1), 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+                    cuda_check(cudaMemcpyAsync(&last[1], d_deg + (n - 1), 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+                    cuda_check(cudaStreamSynchronize(c->stream), "scan");
+                    c->nedges = last[0] + last[1];
+                    need(c->nedges < (uint64_t{1} << 32), EXPMC_EINVAL, "more than 2^32 chain edges");
+                    dev_alloc(&c->rows, n);
+                    dev_alloc(&c->edges, c->nedges);
+                    launch_fill_tables(n, d_rp, d_col, d_val, d_u, d_begin, c->rows, c->edges, c->stream);
+                    d_stats(c->rows, n, d_st, tmp, tb, c->stream);
+                    double st[2];
+                    cuda_check(cudaMemcpyAsync(st, d_st, sizeof st, cudaMemcpyDeviceToHost, c->stream), "D2H");
+                    c->ctr.d2h_bytes += 32;
+                    c->ctr.kernel_launches += 5;
+                    cuda_check(cudaStreamSynchronize(c->stream), "build tables");
+                    c->d_max = st[0];                            // chain.cpp:70
+                    c->d_bar = st[1] / static_cast<double>(n);   // chain.cpp:71 (tree-summed)
+                } catch (...) {
+                    cleanup();
+                    throw;
+                }
+                cleanup();
+            }
+        } catch (...) {
+            expmc_ctx_destroy(c);
+            throw;
+        }
+        *out = c;
+    });
+}
+
+void expmc_ctx_destroy(expmc_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->rows);
+    cudaFree(c->edges);
+    cudaFree(c->d_items);
+    cudaFree(c->d_chunk0);
+    cudaFree(c->d_totals);
+    cudaFree(c->d_partials);
+    cudaFree(c->d_counter);
+    cudaFree(c->d_dbg);
+    cudaFreeHost(c->h_items);
+    cudaFreeHost(c->h_chunk0);
+    cudaFreeHost(c->h_totals);
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int expmc_ctx_get_info(const expmc_ctx* c, expmc_ctx_info* out) {
+    return guarded([&] {
+        need(c && out, EXPMC_EINVAL, "null argument");
+        out->n = c->n;
+        out->n_edges = static_cast<int64_t>(c->nedges);
+        out->d_max = c->d_max;
+        out->d_bar = c->d_bar;
+        out->device = c->device;
+        out->num_sms = c->num_sms;
+        out->table_bytes = static_cast<uint64_t>(c->n) * sizeof(RowRec) + c->nedges * sizeof(EdgeRec);
+    });
+}
+
+int expmc_ctx_set_vector(expmc_ctx* c, const double* u) {
+    return guarded([&] {
+        need(c && (u || c->n == 0), EXPMC_EINVAL, "null argument");
+        if (c->n == 0) return;
+        bind(c);
+        double* d_u = nullptr;
+        dev_alloc(&d_u, c->n);
+        cuda_check(cudaMemcpyAsync(d_u, u, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+        launch_set_vector(c->n, d_u, c->rows, c->stream);
+        c->ctr.h2d_bytes += c->n * 8;
+        c->ctr.kernel_launches += 1;
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        cudaFree(d_u);
+        cuda_check(e, "set vector");
+    });
+}
+
+int expmc_ctx_export_tables(const expmc_ctx* c, double* d, double* rate, int64_t* row_ptr, double* cdf,
+                            int64_t* target, uint8_t* sign) {
+    return guarded([&] {
+        need(c != nullptr, EXPMC_EINVAL, "null context");
+        bind(c);
+        const int64_t n = c->n;
+        const uint64_t m = c->nedges;
+        double *dd = nullptr, *dr = nullptr, *dc = nullptr;
+        int64_t *drp = nullptr, *dt = nullptr;
+        uint8_t* ds = nullptr;
+        dev_alloc(&dd, n); dev_alloc(&dr, n); dev_alloc(&drp, n + 1);
+        dev_alloc(&dc, m); dev_alloc(&dt, m); dev_alloc(&ds, m);
+        launch_export(n, c->rows, dd, dr, drp, c->stream);
+        launch_export_edges(m, c->edges, dc, dt, ds, c->stream);
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        if (e == cudaSuccess && d) e = cudaMemcpy(d, dd, n * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && rate) e = cudaMemcpy(rate, dr, n * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && row_ptr) {
+            e = cudaMemcpy(row_ptr, drp, n * 8, cudaMemcpyDeviceToHost);
+            row_ptr[n] = static_cast<int64_t>(m);
+        }
+        if (e == cudaSuccess && cdf) e = cudaMemcpy(cdf, dc, m * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && target) e = cudaMemcpy(target, dt, m * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && sign) e = cudaMemcpy(sign, ds, m, cudaMemcpyDeviceToHost);
+        cudaFree(dd); cudaFree(dr); cudaFree(drp); cudaFree(dc); cudaFree(dt); cudaFree(ds);
+        cuda_check(e, "export tables");
+    });
+}
+
+int expmc_ctx_get_counters(const expmc_ctx* c, expmc_counters* out) {
+    return guarded([&] {
+        need(c && out, EXPMC_EINVAL, "null argument");
+        *out = c->ctr;
+    });
+}
+
+int expmc_ctx_get_stream(const expmc_ctx* c, void** stream) {
+    return guarded([&] {
+        need(c && stream, EXPMC_EINVAL, "null argument");
+        *stream = static_cast<void*>(c->stream);
+    });
+}
+
+int expmc_bench_gather(int device, uint64_t bytes, int32_t loads_per_thread, int32_t reps, double* gbps) {
+    return guarded([&] {
+        need(gbps != nullptr && bytes >= 64 && loads_per_thread > 0 && reps > 0, EXPMC_EINVAL, "bad gather arguments");
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        int sms = 0;
+        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+        uint64_t loads = 0;
+        const float ms = bench_gather(bytes, loads_per_thread, reps, sms, &loads);
+        *gbps = static_cast<double>(loads) * 32.0 / (static_cast<double>(ms) * 1e-3) / 1e9;
+    });
+}
+
+int expmc_ctx_reset_counters(expmc_ctx* c) {
+    return guarded([&] {
+        need(c != nullptr, EXPMC_EINVAL, "null context");
+        c->ctr = expmc_counters{};
+    });
+}
+
+int expmc_run_level(expmc_ctx* c, int64_t entry, double beta, int32_t level, int32_t base_level, uint64_t first_index,
+                    uint64_t additional, uint64_t seed, expmc_level_stats* out) {
+    return guarded([&] {
+        need(c && out, EXPMC_EINVAL, "null argument");
+        expmc_level_req r{entry, seed, first_index, additional, level, base_level};
+        run_level_batch(c, beta, EXPMC_LANE_ENTRY, &r, 1, out);
+    });
+}
+
+int expmc_run_level_batch(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, const expmc_level_req* req,
+                          expmc_level_stats* out) {
+    return guarded([&] {
+        need(c && (nreq == 0 || (req && out)), EXPMC_EINVAL, "null argument");
+        need(lane == EXPMC_LANE_ENTRY, EXPMC_ENOTIMPL, "only entry-mode sampling (lane 0) is built");
+        run_level_batch(c, beta, lane, req, nreq, out);
+    });
+}
+
+int expmc_sample_debug(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, const expmc_level_req* req,
+                       double* eta_fine, double* eta_coarse, uint64_t* cost, uint64_t* jumps, int64_t* end_state) {
+    return guarded([&] {
+        need(c && (nreq == 0 || req), EXPMC_EINVAL, "null argument");
+        need(lane == EXPMC_LANE_ENTRY, EXPMC_ENOTIMPL, "only entry-mode sampling (lane 0) is built");
+        if (nreq == 0) return;
+        bind(c);
+        std::vector<DevItem> items(static_cast<size_t>(nreq));
+        for (int64_t i = 0; i < nreq; ++i) {
+            expmc_level_req r = req[i];
+            r.count = 1;
+            validate_req(c, r, beta);
+            items[i] = make_item(r, beta, lane);
+        }
+        ensure_items(c, static_cast<size_t>(nreq));
+        if (static_cast<size_t>(nreq) > c->cap_dbg) {
+            dev_alloc(&c->d_dbg, nreq);
+            c->cap_dbg = nreq;
+        }
+        cuda_check(cudaMemcpyAsync(c->d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
+                   "H2D");
+        launch_debug(c->rows, c->edges, c->d_items, static_cast<uint32_t>(nreq), c->d_dbg, c->stream);
+        c->ctr.kernel_launches += 1;
+        std::vector<SampleOut> o(static_cast<size_t>(nreq));
+        cuda_check(cudaMemcpyAsync(o.data(), c->d_dbg, nreq * sizeof(SampleOut), cudaMemcpyDeviceToHost, c->stream),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(c->stream), "sample debug");
+        for (int64_t i = 0; i < nreq; ++i) {
+            if (eta_fine) eta_fine[i] = o[i].fine;
+            if (eta_coarse) eta_coarse[i] = o[i].coarse;
+            if (cost) cost[i] = o[i].cost;
+            if (jumps) jumps[i] = o[i].jumps;
+            if (end_state) end_state[i] = o[i].end_state;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,282 @@
+// Host C++ MLMC driver, batched over rows (the per-component estimator interface).
+//
+// Restates mlmc_driver (mlmc.cpp:170-260) for many entries at once.  Each row keeps its own
+// copy of the reference's state (levels, top, iteration counter) and takes EXACTLY the
+// reference's decision sequence: warm start at L = l0+4 with `warmup` samples per level,
+// then per iteration the Lagrange allocation (optimal_allocation, mlmc.cpp:25-43), the
+// extension of short levels, the stopping test sqrt(V_T) <= eps/sqrt2 and bias <= eps/sqrt2
+// (mlmc.cpp:223-240) and, while the bias bound fails, one more level (mlmc.cpp:241-246).
+// Rows advance in lock-step rounds: every row's pending extensions of one round go to the
+// GPU as a single batched run_level pass (context.cu), so a round costs one sampler launch
+// per 4M chunks no matter how many rows are active.
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+using namespace expmc_b200;
+
+namespace {
+
+struct Level {
+    double sum = 0.0, sum_sq = 0.0;
+    uint64_t samples = 0, cost = 0, jumps = 0;
+    double mean() const { return samples ? sum / static_cast<double>(samples) : 0.0; }
+    double variance() const {  // LevelStats::variance, mlmc.cpp:13-17
+        if (samples < 2) return 0.0;
+        const double m = mean();
+        return std::max(0.0, sum_sq / static_cast<double>(samples) - m * m);
+    }
+    double unit_cost() const {
+        return samples ? static_cast<double>(cost) / static_cast<double>(samples) : 0.0;
+    }
+};
+
+int initial_level_impl(double beta, double d_max) {  // mlmc.cpp:19-23
+    if (!(beta > 0.0)) throw Status(EXPMC_EINVAL, "beta must be positive");
+    if (!(d_max > 0.0)) return 0;
+    return static_cast<int>(std::max<long>(0, std::lround(std::log2(2.0 * beta * d_max))));
+}
+
+void optimal_allocation_impl(size_t n, const double* v, const double* c, double eps, uint64_t* m) {
+    if (!(eps > 0.0)) throw Status(EXPMC_EINVAL, "epsilon must be positive");  // mlmc.cpp:25-43
+    double s = 0.0;
+    for (size_t l = 0; l < n; ++l) {
+        if (v[l] < 0.0 || !(c[l] > 0.0)) throw Status(EXPMC_EINVAL, "require V_l >= 0 and C_l > 0");
+        s += std::sqrt(v[l] * c[l]);
+    }
+    const double scale = 2.0 / (eps * eps) * s;
+    for (size_t l = 0; l < n; ++l) {
+        const double raw = scale * std::sqrt(v[l] / c[l]);
+        m[l] = std::max<uint64_t>(2, static_cast<uint64_t>(std::ceil(raw)));
+    }
+}
+
+double bias_estimate_impl(size_t n, const double* means) {  // mlmc.cpp:45-51
+    if (n < 2) throw Status(EXPMC_EINVAL, "bias estimate needs at least two coupled levels");
+    const double last = std::abs(means[n - 1]);
+    const double prev = std::abs(means[n - 2]);
+    return std::max(last, prev / 4.0) / 3.0;
+}
+
+enum class Phase { waiting_warmup, waiting_extend, waiting_added, done };
+
+struct RowState {
+    int64_t entry = 0;
+    uint64_t seed = 0;
+    int l0 = 0, cap = 0, top = 0, iter = 0;
+    Phase phase = Phase::waiting_warmup;
+    std::vector<Level> lv;
+    std::vector<std::pair<int, uint64_t>> pending;  // (level index, additional samples)
+    double stat_error = 0.0, bias = 0.0;
+    bool converged = false;
+};
+
+struct DriverConfig {
+    double eps, target;
+    uint64_t warmup;
+    int max_iterations;
+};
+
+// Advance one row whose pending work has completed, up to its next GPU request or the end.
+void advance(RowState& r, const DriverConfig& cfg, std::vector<double>& v, std::vector<double>& c,
+             std::vector<uint64_t>& want, std::vector<double>& means) {
+    bool eval = r.phase == Phase::waiting_extend;
+    for (;;) {
+        if (!eval) {
+            // ---- top of the reference's for-iter loop (mlmc.cpp:212-221)
+            if (r.iter >= cfg.max_iterations) {
+                r.phase = Phase::done;
+                return;
+            }
+            const size_t nl = r.lv.size();
+            v.resize(nl);
+            c.resize(nl);
+            want.resize(nl);
+            for (size_t i = 0; i < nl; ++i) {
+                v[i] = r.lv[i].variance();
+                c[i] = std::max(r.lv[i].unit_cost(), 1.0);
+            }
+            optimal_allocation_impl(nl, v.data(), c.data(), cfg.eps, want.data());
+            for (size_t i = 0; i < nl; ++i)
+                if (want[i] > r.lv[i].samples)
+                    r.pending.emplace_back(static_cast<int>(i), want[i] - r.lv[i].samples);
+            if (!r.pending.empty()) {
+                r.phase = Phase::waiting_extend;
+                return;
+            }
+        }
+        eval = false;
+        // ---- statistics after the extension (mlmc.cpp:223-240)
+        double vt = 0.0;
+        for (const Level& l : r.lv) vt += l.variance() / static_cast<double>(l.samples);
+        r.stat_error = std::sqrt(vt);
+        means.clear();
+        for (size_t i = 1; i < r.lv.size(); ++i) means.push_back(r.lv[i].mean());
+        r.bias = bias_estimate_impl(means.size(), means.data());
+        if (r.stat_error <= cfg.target && r.bias <= cfg.target) {
+            r.converged = true;
+            r.phase = Phase::done;
+            return;
+        }
+        if (r.bias > cfg.target) {  // mlmc.cpp:241-246
+            if (r.top == r.cap) {
+                r.phase = Phase::done;
+                return;
+            }
+            ++r.top;
+            r.lv.emplace_back();
+            r.pending.emplace_back(static_cast<int>(r.lv.size() - 1), cfg.warmup);
+            ++r.iter;
+            r.phase = Phase::waiting_added;
+            return;
+        }
+        ++r.iter;
+    }
+}
+
+void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t nrows, const int64_t* rows,
+                const uint64_t* row_seed, expmc_result* out, expmc_level_record* levels, int32_t max_levels) {
+    expmc_ctx_info info{};
+    if (expmc_ctx_get_info(ctx, &info) != EXPMC_OK) throw Status(EXPMC_EINVAL, "null context");
+    for (int64_t r = 0; r < nrows; ++r)  // validate_problem, mlmc.cpp:150-159
+        if (rows[r] < 0 || rows[r] >= info.n) throw Status(EXPMC_ERANGE, "entry index outside matrix");
+    if (!(beta > 0.0)) throw Status(EXPMC_EINVAL, "beta must be positive");
+    if (!(opt.epsilon > 0.0)) throw Status(EXPMC_EINVAL, "epsilon must be positive");
+    const int l0 = opt.l0_override >= 0 ? opt.l0_override : initial_level_impl(beta, info.d_max);
+    const int cap = l0 + opt.max_levels_above_l0;
+    DriverConfig cfg{opt.epsilon, opt.epsilon / std::sqrt(2.0), opt.warmup, opt.max_iterations};
+
+    std::vector<RowState> st(static_cast<size_t>(nrows));
+    for (int64_t r = 0; r < nrows; ++r) {
+        RowState& s = st[static_cast<size_t>(r)];
+        s.entry = rows[r];
+        s.seed = row_seed[r];
+        s.l0 = l0;
+        s.cap = cap;
+        s.top = std::min(l0 + 4, cap);  // mlmc.cpp:201-205
+        s.lv.resize(static_cast<size_t>(s.top - l0 + 1));
+        for (int i = 0; i <= s.top - l0; ++i) s.pending.emplace_back(i, opt.warmup);
+    }
+
+    std::vector<expmc_level_req> req;
+    std::vector<expmc_level_stats> res;
+    std::vector<std::pair<int64_t, int>> owner;
+    std::vector<double> v, c, means;
+    std::vector<uint64_t> want;
+    std::vector<int64_t> active;
+    for (int64_t r = 0; r < nrows; ++r) active.push_back(r);
+    while (!active.empty()) {
+        req.clear();
+        owner.clear();
+        for (int64_t r : active) {
+            RowState& s = st[static_cast<size_t>(r)];
+            for (const auto& p : s.pending) {
+                const Level& l = s.lv[static_cast<size_t>(p.first)];
+                const int level = s.l0 + p.first;
+                req.push_back(expmc_level_req{s.entry, s.seed, l.samples, p.second, level, level == s.l0 ? 1 : 0});
+                owner.emplace_back(r, p.first);
+            }
+        }
+        res.resize(req.size());
+        run_level_batch(ctx, beta, EXPMC_LANE_ENTRY, req.data(), static_cast<int64_t>(req.size()), res.data());
+        for (size_t k = 0; k < req.size(); ++k) {  // extend(): mlmc.cpp:188-199
+            Level& l = st[static_cast<size_t>(owner[k].first)].lv[static_cast<size_t>(owner[k].second)];
+            l.sum += res[k].sum;
+            l.sum_sq += res[k].sum_sq;
+            l.samples += res[k].samples;
+            l.cost += res[k].cost;
+            l.jumps += res[k].jumps;
+        }
+        std::vector<int64_t> next;
+        for (int64_t r : active) {
+            RowState& s = st[static_cast<size_t>(r)];
+            s.pending.clear();
+            advance(s, cfg, v, c, want, means);
+            if (s.phase != Phase::done) next.push_back(r);
+        }
+        active.swap(next);
+    }
+
+    for (int64_t r = 0; r < nrows; ++r) {  // mlmc.cpp:249-259
+        const RowState& s = st[static_cast<size_t>(r)];
+        expmc_result& o = out[r];
+        std::memset(&o, 0, sizeof o);
+        o.l0 = s.l0;
+        o.L = s.top;
+        o.statistical_error = s.stat_error;
+        o.bias_estimate = s.bias;
+        o.converged = s.converged ? 1 : 0;
+        o.nlevels = static_cast<int32_t>(s.lv.size());
+        for (size_t i = 0; i < s.lv.size(); ++i) {
+            const Level& l = s.lv[i];
+            o.estimate += l.mean();
+            o.total_cost += l.cost;
+            o.total_jumps += l.jumps;
+            o.total_samples += l.samples;
+            if (levels && static_cast<int32_t>(i) < max_levels) {
+                expmc_level_record& rec = levels[r * max_levels + static_cast<int64_t>(i)];
+                rec.level = s.l0 + static_cast<int32_t>(i);
+                rec.pad = 0;
+                rec.sum = l.sum;
+                rec.sum_sq = l.sum_sq;
+                rec.samples = l.samples;
+                rec.cost = l.cost;
+            }
+        }
+    }
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return EXPMC_OK;
+    } catch (const Status& s) {
+        set_error(s.what());
+        return s.code;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return EXPMC_EINTERNAL;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int expmc_mlmc_driver_rows(expmc_ctx* ctx, double beta, const expmc_options* opt, int64_t nrows, const int64_t* rows,
+                           const uint64_t* row_seed, expmc_result* out, expmc_level_record* levels,
+                           int32_t max_levels) {
+    return guarded([&] {
+        if (!ctx || !opt || (nrows > 0 && (!rows || !row_seed || !out)))
+            throw Status(EXPMC_EINVAL, "null argument");
+        drive_rows(ctx, beta, *opt, nrows, rows, row_seed, out, levels, max_levels);
+    });
+}
+
+int expmc_mlmc_driver(expmc_ctx* ctx, int64_t entry, double beta, const expmc_options* opt, expmc_result* out,
+                      expmc_level_record* levels, int32_t max_levels) {
+    return guarded([&] {
+        if (!ctx || !opt || !out) throw Status(EXPMC_EINVAL, "null argument");
+        const uint64_t seed = opt->seed;
+        drive_rows(ctx, beta, *opt, 1, &entry, &seed, out, levels, max_levels);
+    });
+}
+
+int expmc_initial_level(double beta, double d_max, int32_t* out) {
+    return guarded([&] { *out = initial_level_impl(beta, d_max); });
+}
+
+int expmc_optimal_allocation(int64_t n, const double* v, const double* c, double eps, uint64_t* out) {
+    return guarded([&] { optimal_allocation_impl(static_cast<size_t>(n), v, c, eps, out); });
+}
+
+int expmc_bias_estimate(int64_t n, const double* means, double* out) {
+    return guarded([&] { *out = bias_estimate_impl(static_cast<size_t>(n), means); });
+}
+
+}  // extern "C"

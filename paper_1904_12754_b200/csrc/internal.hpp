@@ -1,0 +1,123 @@
+// Internal (non-ABI) declarations shared by the CUDA translation units and the host driver.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "expmc_b200.h"
+
+namespace expmc_b200 {
+
+// ----------------------------------------------------------------------------- HBM layout
+// Packed row record: everything a walker needs when it lands on a row, in ONE 32-B sector
+// (the reference reads rate/d/row_ptr/u from four SoA arrays, chain.hpp:31-35).
+struct alignas(32) RowRec {
+    double d;        // a_ii + rate_i                     (chain.cpp:47-48)
+    double rate;     // sum_{j != i} |a_ij|               (chain.cpp:39-46)
+    double u;        // u_i, the terminal factor           (paths.cpp:112,138)
+    uint32_t begin;  // first edge of the row
+    uint32_t deg;    // number of chain edges of the row
+};
+static_assert(sizeof(RowRec) == 32, "row record must be one 32-B sector");
+
+// Edge record, 16 B: the reference's jump_cdf / jump_target / sign triple (chain.hpp:33-35).
+struct alignas(16) EdgeRec {
+    double cdf;       // cumulative |a_ij| / rate_i, last entry of a row exactly 1
+    uint32_t target;  // column j
+    uint32_t sign;    // 1 where a_ij < 0
+};
+static_assert(sizeof(EdgeRec) == 16, "edge record is 16 B");
+
+// One device work item = one run_level request with count > 0.
+struct alignas(16) DevItem {
+    uint64_t seed;
+    uint64_t first;
+    uint64_t count;
+    double dt;        // beta / 2^level (mlmc.cpp:81)
+    uint64_t nsteps;  // 2^level
+    uint32_t entry;
+    uint32_t key3;    // (level & 0xFFFFFF) | lane << 24   (rng.hpp:29)
+    uint32_t base;
+    uint32_t pad;
+};
+
+// Per-chunk partial and per-item running total (SumAcc, parallel.hpp:57-78, + jumps).
+struct alignas(16) Partial {
+    double sum;
+    double sum_sq;
+    unsigned long long cost;
+    unsigned long long jumps;
+};
+
+// Per-sample debug output.
+struct SampleOut {
+    double fine;
+    double coarse;
+    unsigned long long cost;
+    unsigned long long jumps;
+    long long end_state;
+};
+
+constexpr uint64_t kChunk = 512;  // parallel.hpp:20 -- samples per chunk, by absolute index
+
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+// ----------------------------------------------------------------------------- launchers
+struct SamplerArgs {
+    const RowRec* rows;
+    const EdgeRec* edges;
+    const DevItem* items;
+    const uint64_t* chunk0;  // nitems + 1, exclusive prefix of chunk counts
+    uint32_t nitems;
+    uint64_t g_begin, g_end;  // global chunk window of this launch
+    Partial* partials;        // [g_end - g_begin]
+    unsigned int* counter;    // dynamic chunk counter, zeroed before launch
+};
+
+void launch_sampler(const SamplerArgs& a, int grid, cudaStream_t s);
+void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
+                    const Partial* partials, Partial* totals, cudaStream_t s);
+void launch_debug(const RowRec* rows, const EdgeRec* edges, const DevItem* items, uint32_t n,
+                  SampleOut* out, cudaStream_t s);
+int sampler_blocks_per_sm();
+int sampler_threads();
+
+float bench_gather(uint64_t bytes, int loads_per_thread, int reps, int num_sms, uint64_t* total_loads);
+
+// table builder
+void launch_count_edges(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                        uint64_t* deg, unsigned int* err, cudaStream_t s);
+void launch_fill_tables(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                        const double* u, const uint64_t* begin, RowRec* rows, EdgeRec* edges,
+                        cudaStream_t s);
+void launch_set_vector(int64_t n, const double* u, RowRec* rows, cudaStream_t s);
+void launch_export(int64_t n, const RowRec* rows, double* d, double* rate, int64_t* row_ptr,
+                   cudaStream_t s);
+void launch_export_edges(uint64_t e, const EdgeRec* edges, double* cdf, int64_t* target,
+                         uint8_t* sign, cudaStream_t s);
+// scans / reductions (CUB): exclusive sum of n u64, max / sum of RowRec::d
+size_t scan_temp_bytes(int64_t n);
+void exclusive_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* tmp, size_t tmp_bytes,
+                        cudaStream_t s);
+size_t dstat_temp_bytes(int64_t n);
+void d_stats(const RowRec* rows, int64_t n, double* out2 /* device: max, sum */, void* tmp,
+             size_t tmp_bytes, cudaStream_t s);
+
+}  // namespace expmc_b200
+
+// Host-side batched run_level used by the driver (context.cu).
+struct expmc_ctx;
+namespace expmc_b200 {
+void run_level_batch(expmc_ctx* ctx, double beta, uint32_t lane, const expmc_level_req* req,
+                     int64_t nreq, expmc_level_stats* out);
+void set_error(const std::string& m);
+}  // namespace expmc_b200

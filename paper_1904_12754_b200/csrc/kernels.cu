@@ -1,0 +1,433 @@
+// sm_100a kernels of the MLMC random-walk estimator.
+//
+//  k_sample   -- path sampler + level coupling + per-chunk reduction (the hot kernel).
+//                Replaces parallel_samples<SumAcc> (parallel.hpp:31-54) around
+//                LevelSampler::single/coupled (paths.cpp:99-141) in run_level_ex
+//                (mlmc.cpp:76-148).  One warp owns one 512-sample chunk (parallel.hpp:20);
+//                lanes pull the chunk's samples dynamically (a lane that finishes a path
+//                starts the next unclaimed sample at once), so warp time tracks the mean
+//                path length, not the longest path.  The chunk's (sum, sum_sq, cost, jumps)
+//                is reduced with a fixed xor-shuffle tree -> deterministic, independent of
+//                grid size, GPU count and scheduling.
+//  k_combine  -- per-item ordered combine of the chunk partials (SumAcc::combine in
+//                ascending chunk order, parallel.hpp:52).
+//  k_debug    -- one thread per requested sample (golden per-sample parity).
+//  k_count_edges / k_fill_tables -- the transition-table builder (decompose_impl,
+//                chain.cpp:15-71) straight from CSR on the device.
+#include <cub/device/device_scan.cuh>
+
+#include "internal.hpp"
+#include "walker.cuh"
+
+namespace expmc_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ chunk0, uint32_t nitems,
+                                              uint64_t g, uint32_t hint) {
+    // chunk0 is non-decreasing; find the last i with chunk0[i] <= g (items with zero chunks
+    // never occur: count == 0 requests are dropped on the host).  Warps draw chunk ids in
+    // increasing order, so gallop forward from the previous item first.
+    uint32_t lo = hint;
+    if (lo >= nitems || chunk0[lo] > g) lo = 0;
+    uint32_t step = 1, hi = lo + 1;
+    while (hi < nitems && chunk0[hi] <= g) {
+        lo = hi;
+        hi = lo + step;
+        step <<= 1;
+    }
+    if (hi > nitems) hi = nitems;
+    // invariant: chunk0[lo] <= g, and (hi == nitems or chunk0[hi] > g)
+    while (hi - lo > 1) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        if (chunk0[mid] <= g) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kThreads) k_sample(SamplerArgs a) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const unsigned full = 0xFFFFFFFFu;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t hint = 0;
+    for (;;) {
+        uint32_t gi = 0;
+        if (lane == 0) gi = atomicAdd(a.counter, 1u);
+        gi = __shfl_sync(full, gi, 0);
+        const uint64_t g = a.g_begin + gi;
+        if (g >= a.g_end) return;
+
+        const uint32_t item = find_item(a.chunk0, a.nitems, g, hint);
+        hint = item;
+        const ItemConst ic = load_item(a.items, item, a.rows);
+        const DevItem& it = a.items[item];
+        const uint64_t first = it.first, end = it.first + it.count;
+        const uint64_t chunk = first / kChunk + (g - a.chunk0[item]);
+        const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
+        const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
+        const uint32_t cnt = static_cast<uint32_t>(hi - lo);
+
+        double sum = 0.0, sum_sq = 0.0;
+        unsigned long long cost = 0, jumps = 0;
+        Walker w;
+        bool active = false;
+        uint32_t next = 0;
+        for (;;) {
+            const unsigned need = __ballot_sync(full, !active);
+            if (!active) {
+                const uint32_t mine = next + __popc(need & lt_mask);
+                if (mine < cnt) {
+                    walker_start(w, ic, lo + mine);
+                    active = true;
+                }
+            }
+            next += __popc(need);
+            if (!__any_sync(full, active)) break;
+            if (active && walker_event(w, ic, a.rows, a.edges)) {
+                double fine, coarse;
+                walker_finish(w, ic, fine, coarse);
+                const double x = ic.base ? fine : __dsub_rn(fine, coarse);
+                sum = __dadd_rn(sum, x);
+                sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
+                cost += w.draws + ic.nsteps;
+                jumps += w.jumps;
+                active = false;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sum = __dadd_rn(sum, __shfl_xor_sync(full, sum, o));
+            sum_sq = __dadd_rn(sum_sq, __shfl_xor_sync(full, sum_sq, o));
+            cost += __shfl_xor_sync(full, cost, o);
+            jumps += __shfl_xor_sync(full, jumps, o);
+        }
+        if (lane == 0) {
+            Partial p;
+            p.sum = sum;
+            p.sum_sq = sum_sq;
+            p.cost = cost;
+            p.jumps = jumps;
+            a.partials[g - a.g_begin] = p;
+        }
+    }
+}
+
+__global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, uint64_t g_begin,
+                          uint64_t g_end, const Partial* __restrict__ partials, Partial* __restrict__ totals) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nitems) return;
+    const uint64_t c0 = chunk0[i] > g_begin ? chunk0[i] : g_begin;
+    const uint64_t c1 = chunk0[i + 1] < g_end ? chunk0[i + 1] : g_end;
+    if (c0 >= c1) return;
+    Partial t = totals[i];
+    for (uint64_t g = c0; g < c1; ++g) {  // ascending chunk order (parallel.hpp:52)
+        const Partial p = partials[g - g_begin];
+        t.sum = __dadd_rn(t.sum, p.sum);
+        t.sum_sq = __dadd_rn(t.sum_sq, p.sum_sq);
+        t.cost += p.cost;
+        t.jumps += p.jumps;
+    }
+    totals[i] = t;
+}
+
+__global__ void k_debug(const RowRec* __restrict__ rows, const EdgeRec* __restrict__ edges,
+                        const DevItem* __restrict__ items, uint32_t n, SampleOut* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const ItemConst ic = load_item(items, i, rows);
+    Walker w;
+    walker_start(w, ic, items[i].first);
+    while (!walker_event(w, ic, rows, edges)) {
+    }
+    SampleOut o;
+    walker_finish(w, ic, o.fine, o.coarse);
+    o.cost = w.draws + ic.nsteps;
+    o.jumps = w.jumps;
+    o.end_state = w.state;
+    out[i] = o;
+}
+
+// ---------------------------------------------------------------- transition-table builder
+enum : unsigned { kErrNonFinite = 1u, kErrRange = 2u, kErrCanon = 4u };
+
+__global__ void k_count_edges(int64_t n, const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col,
+                              const double* __restrict__ val, uint64_t* __restrict__ deg, unsigned* err) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+    unsigned bad = 0;
+    if (e < b) bad |= kErrCanon;
+    uint64_t cnt = 0;
+    int64_t prev = -1;
+    for (int64_t k = b; k < e; ++k) {
+        const int64_t c = col[k];
+        const double v = val[k];
+        if (c < 0 || c >= n) bad |= kErrRange;
+        if (!isfinite(v)) bad |= kErrNonFinite;
+        if (c <= prev) bad |= kErrCanon;
+        prev = c;
+        if (c != i && v != 0.0) ++cnt;
+    }
+    deg[i] = cnt;
+    if (bad) atomicOr(err, bad);
+}
+
+// decompose_impl per row (chain.cpp:29-64), same operation order: running |a_ij| sum, CDF =
+// running sum / rate, last entry exactly 1, sign = (a_ij < 0), d = a_ii + rate.
+__global__ void k_fill_tables(int64_t n, const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col,
+                              const double* __restrict__ val, const double* __restrict__ u,
+                              const uint64_t* __restrict__ begin, RowRec* __restrict__ rows,
+                              EdgeRec* __restrict__ edges) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t e0 = begin[i];
+    uint64_t e = e0;
+    double diag = 0.0, rate = 0.0;
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+        const int64_t c = col[k];
+        const double v = val[k];
+        if (c == i) {
+            diag = v;
+            continue;
+        }
+        if (v == 0.0) continue;
+        rate = __dadd_rn(rate, fabs(v));
+        EdgeRec r;
+        r.cdf = rate;
+        r.target = static_cast<uint32_t>(c);
+        r.sign = v < 0.0 ? 1u : 0u;
+        edges[e++] = r;
+    }
+    if (rate > 0.0) {
+        for (uint64_t k = e0; k + 1 < e; ++k) edges[k].cdf = __ddiv_rn(edges[k].cdf, rate);
+        edges[e - 1].cdf = 1.0;
+    }
+    RowRec r;
+    r.d = __dadd_rn(diag, rate);
+    r.rate = rate;
+    r.u = u[i];
+    r.begin = static_cast<uint32_t>(e0);
+    r.deg = static_cast<uint32_t>(e - e0);
+    rows[i] = r;
+}
+
+__global__ void k_set_vector(int64_t n, const double* __restrict__ u, RowRec* __restrict__ rows) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) rows[i].u = u[i];
+}
+
+__global__ void k_export_rows(int64_t n, const RowRec* __restrict__ rows, double* d, double* rate, int64_t* row_ptr) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const RowRec r = rows[i];
+    if (d) d[i] = r.d;
+    if (rate) rate[i] = r.rate;
+    if (row_ptr) row_ptr[i] = r.begin;
+}
+
+__global__ void k_export_edges(uint64_t m, const EdgeRec* __restrict__ edges, double* cdf, int64_t* target,
+                               uint8_t* sign) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const EdgeRec r = edges[i];
+    if (cdf) cdf[i] = r.cdf;
+    if (target) target[i] = r.target;
+    if (sign) sign[i] = static_cast<uint8_t>(r.sign);
+}
+
+// d_max / d_sum: fixed two-level tree (block partials, then one block) -> deterministic.
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 1024;
+
+__global__ void k_dstats_partial(const RowRec* __restrict__ rows, int64_t n, double* part) {
+    __shared__ double smax[kRedThreads], ssum[kRedThreads];
+    double m = -INFINITY, s = 0.0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kRedThreads) {
+        const double d = rows[i].d;
+        m = fmax(m, d);
+        s = __dadd_rn(s, d);
+    }
+    smax[threadIdx.x] = m;
+    ssum[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = kRedThreads / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+            ssum[threadIdx.x] = __dadd_rn(ssum[threadIdx.x], ssum[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = smax[0];
+        part[2 * blockIdx.x + 1] = ssum[0];
+    }
+}
+
+__global__ void k_dstats_final(const double* part, int nb, double* out2) {
+    __shared__ double smax[kRedThreads], ssum[kRedThreads];
+    double m = -INFINITY, s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += kRedThreads) {
+        m = fmax(m, part[2 * i]);
+        s = __dadd_rn(s, part[2 * i + 1]);
+    }
+    smax[threadIdx.x] = m;
+    ssum[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = kRedThreads / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+            ssum[threadIdx.x] = __dadd_rn(ssum[threadIdx.x], ssum[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out2[0] = smax[0];
+        out2[1] = ssum[0];
+    }
+}
+
+// Random 32-B sector gather: the roofline denominator for the sampler's table reads.  Every
+// load is independent (hash-generated sector index), so the kernel measures the memory
+// system's random-sector throughput, not latency.
+__global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ buf, uint64_t nsectors, int loads,
+                                                uint64_t salt, unsigned* __restrict__ sink) {
+    uint64_t x = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull ^ salt;
+    unsigned acc = 0;
+#pragma unroll 8
+    for (int i = 0; i < loads; ++i) {
+        x ^= x >> 33;
+        x *= 0xFF51AFD7ED558CCDull;
+        x ^= x >> 29;
+        const uint64_t s = __umul64hi(x, nsectors);
+        const uint4 a = __ldcg(buf + 2 * s);
+        const uint4 b = __ldcg(buf + 2 * s + 1);
+        acc += a.x ^ a.w ^ b.y ^ b.z;
+    }
+    if (acc == 0x12345678u) sink[0] = acc;  // keep the loads alive
+}
+
+inline unsigned grid_for(int64_t n, int threads) {
+    return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+}  // namespace
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Status(EXPMC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int sampler_threads() { return kThreads; }
+
+int sampler_blocks_per_sm() {
+    int b = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample, kThreads, 0), "occupancy");
+    return b > 0 ? b : 1;
+}
+
+void launch_sampler(const SamplerArgs& a, int grid, cudaStream_t s) {
+    k_sample<<<grid, kThreads, 0, s>>>(a);
+    cuda_check(cudaGetLastError(), "k_sample launch");
+}
+
+void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
+                    const Partial* partials, Partial* totals, cudaStream_t s) {
+    k_combine<<<grid_for(nitems, 256), 256, 0, s>>>(chunk0, nitems, g_begin, g_end, partials, totals);
+    cuda_check(cudaGetLastError(), "k_combine launch");
+}
+
+void launch_debug(const RowRec* rows, const EdgeRec* edges, const DevItem* items, uint32_t n, SampleOut* out,
+                  cudaStream_t s) {
+    k_debug<<<grid_for(n, 128), 128, 0, s>>>(rows, edges, items, n, out);
+    cuda_check(cudaGetLastError(), "k_debug launch");
+}
+
+void launch_count_edges(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val, uint64_t* deg,
+                        unsigned int* err, cudaStream_t s) {
+    if (n == 0) return;
+    k_count_edges<<<grid_for(n, 256), 256, 0, s>>>(n, row_ptr, col, val, deg, err);
+    cuda_check(cudaGetLastError(), "k_count_edges launch");
+}
+
+void launch_fill_tables(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val, const double* u,
+                        const uint64_t* begin, RowRec* rows, EdgeRec* edges, cudaStream_t s) {
+    if (n == 0) return;
+    k_fill_tables<<<grid_for(n, 128), 128, 0, s>>>(n, row_ptr, col, val, u, begin, rows, edges);
+    cuda_check(cudaGetLastError(), "k_fill_tables launch");
+}
+
+void launch_set_vector(int64_t n, const double* u, RowRec* rows, cudaStream_t s) {
+    if (n == 0) return;
+    k_set_vector<<<grid_for(n, 256), 256, 0, s>>>(n, u, rows);
+    cuda_check(cudaGetLastError(), "k_set_vector launch");
+}
+
+void launch_export(int64_t n, const RowRec* rows, double* d, double* rate, int64_t* row_ptr, cudaStream_t s) {
+    if (n == 0) return;
+    k_export_rows<<<grid_for(n, 256), 256, 0, s>>>(n, rows, d, rate, row_ptr);
+    cuda_check(cudaGetLastError(), "k_export_rows launch");
+}
+
+void launch_export_edges(uint64_t m, const EdgeRec* edges, double* cdf, int64_t* target, uint8_t* sign,
+                         cudaStream_t s) {
+    if (m == 0) return;
+    k_export_edges<<<grid_for(static_cast<int64_t>(m), 256), 256, 0, s>>>(m, edges, cdf, target, sign);
+    cuda_check(cudaGetLastError(), "k_export_edges launch");
+}
+
+float bench_gather(uint64_t bytes, int loads_per_thread, int reps, int num_sms, uint64_t* total_loads) {
+    const uint64_t nsectors = bytes / 32;
+    uint4* buf = nullptr;
+    unsigned* sink = nullptr;
+    cuda_check(cudaMalloc(&buf, nsectors * 32), "cudaMalloc gather");
+    cuda_check(cudaMalloc(&sink, sizeof(unsigned)), "cudaMalloc sink");
+    cuda_check(cudaMemset(buf, 1, nsectors * 32), "memset gather");
+    const int grid = num_sms * 8;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < reps + 1; ++r) {  // first launch is warm-up
+        cudaEventRecord(e0);
+        k_gather<<<grid, 256>>>(buf, nsectors, loads_per_thread, 0x1234567ull + r, sink);
+        cudaEventRecord(e1);
+        cuda_check(cudaEventSynchronize(e1), "gather");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    cudaFree(sink);
+    *total_loads = static_cast<uint64_t>(grid) * 256 * static_cast<uint64_t>(loads_per_thread);
+    return best;
+}
+
+size_t scan_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cuda_check(cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const uint64_t*>(nullptr),
+                                             static_cast<uint64_t*>(nullptr), static_cast<int>(n)),
+               "scan sizing");
+    return bytes;
+}
+
+void exclusive_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* tmp, size_t tmp_bytes, cudaStream_t s) {
+    cuda_check(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, static_cast<int>(n), s), "scan");
+}
+
+size_t dstat_temp_bytes(int64_t) { return sizeof(double) * 2 * kRedBlocks; }
+
+void d_stats(const RowRec* rows, int64_t n, double* out2, void* tmp, size_t, cudaStream_t s) {
+    double* part = static_cast<double*>(tmp);
+    k_dstats_partial<<<kRedBlocks, kRedThreads, 0, s>>>(rows, n, part);
+    cuda_check(cudaGetLastError(), "k_dstats_partial launch");
+    k_dstats_final<<<1, kRedThreads, 0, s>>>(part, kRedBlocks, out2);
+    cuda_check(cudaGetLastError(), "k_dstats_final launch");
+}
+
+}  // namespace expmc_b200

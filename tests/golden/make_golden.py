@@ -1,0 +1,130 @@
+"""Generate tests/golden/golden.json from the UNMODIFIED reference library.
+
+Run here (where /root/reference exists and oracle/_ref/libexpmc_ref.so is built by
+`make -C oracle`):   python tests/golden/make_golden.py
+Every number in golden.json is an output of the reference's own code path (RngStream,
+decompose, LevelSampler::single/coupled, run_level, mlmc_driver, dense_expmv, smallw),
+stored as exact hex floats.  The fixtures are committed; tests never need /root/reference.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle import CSR, Reference  # noqa: E402
+
+
+def hx(a):
+    return [float(x).hex() for x in np.asarray(a, np.float64).ravel()]
+
+
+def csr_json(a: CSR):
+    return dict(n=int(a.n), row_ptr=[int(x) for x in a.row_ptr], col=[int(x) for x in a.col], val=hx(a.val))
+
+
+def grid(g):
+    n = g * g
+    trips = []
+    for y in range(g):
+        for x in range(g):
+            r = y * g + x
+            trips.append((r, r, -4.0))
+            if x > 0:
+                trips.append((r, r - 1, 1.0))
+            if x + 1 < g:
+                trips.append((r, r + 1, 1.0))
+            if y > 0:
+                trips.append((r, r - g, 1.0))
+            if y + 1 < g:
+                trips.append((r, r + g, 1.0))
+    return CSR.from_triplets(n, trips)
+
+
+def main():
+    ref = Reference()
+    out = {"generator": "tests/golden/make_golden.py (reference: /root/reference/proj/core via oracle/_ref)"}
+
+    # 1. Philox uniforms (rng.hpp:21-79) incl. SURVEY Appendix A anchors
+    keys = [(0, 0, 0, 0), (42, 3, 12345, 0), (7, 5, 2 ** 40, 2), (12345, 0, 7, 6), (2 ** 63 + 5, 62, 2 ** 64 - 1, 255),
+            (1000, 4, 511, 0), (1001, 0, 512, 0)]
+    out["uniforms"] = [dict(key=list(k), values=hx(ref.uniforms(*k, 9))) for k in keys]
+
+    # 2. matrices
+    mats = {
+        "two_state": CSR.from_dense([[0.2, 1.0], [0.5, -0.3]]),        # test_paths.cpp:150-151
+        "k2": CSR.from_dense([[0.0, 1.0], [1.0, 0.0]]),                 # test_paths.cpp:102
+        "diag": CSR.from_dense([[0.75, 0.0], [0.0, -0.5]]),              # test_paths.cpp:85
+        "signed3": CSR.from_dense([[0.1, -1.0, 0.5], [0.7, -0.2, -0.2], [-0.4, 0.0, 0.3]]),
+        "absorb3": CSR.from_dense([[0.0, 1.0, 0.5], [0.0, -1.0, 0.0], [0.25, 0.25, 0.0]]),
+        "grid8": grid(8),
+    }
+    sw = ref.smallw(100, 2, 0.1, 5)                                      # test_paths.cpp:114
+    mats["smallw100"] = sw.a
+    hub = ref.pref(300, 3, 7)                                            # BA, wide hub rows (deg > 4)
+    mats["pref300"] = hub.a
+
+    rng = np.random.default_rng(0)
+    out["matrices"] = {}
+    for name, a in mats.items():
+        ch = ref.chain(a)
+        dec = ch.decomposition()
+        n = a.n
+        u = np.round(rng.uniform(-1.0, 2.0, n), 6)
+        beta = 0.8 if name != "smallw100" else 1.0 / dec["d_max"] if dec["d_max"] > 0 else 1.0
+        entries = sorted(set([0, n - 1, n // 2]))
+        samples = []
+        for entry in entries:
+            for level in range(0, 5):
+                for base in ([1, 0] if level > 0 else [1]):
+                    seed = 1000 + entry + 17 * level
+                    idx = np.array(list(range(24)) + [511, 512, 2 ** 33 + 3, 2 ** 40 + 1], np.uint64)
+                    s = ch.samples(u, entry, beta, level, base, seed, idx)
+                    samples.append(dict(entry=entry, level=level, base=base, seed=seed, idx=[int(x) for x in idx],
+                                        fine=hx(s["fine"]), coarse=hx(s["coarse"]), cost=[int(c) for c in s["cost"]]))
+        runs = []
+        for entry in entries[:2]:
+            for (level, base, first, count) in [(0, 1, 0, 1000), (1, 0, 37, 2500), (3, 0, 1000, 700), (4, 0, 0, 1)]:
+                seed = 77 + entry
+                r = ch.run_level(u, entry, beta, level, base, first, count, seed, threads=4)
+                runs.append(dict(entry=entry, level=level, base=base, first=first, count=count, seed=seed,
+                                 sum=float(r["sum"]).hex(), sum_sq=float(r["sum_sq"]).hex(), samples=int(r["samples"]),
+                                 cost=int(r["cost"])))
+        out["matrices"][name] = dict(csr=csr_json(a), u=hx(u), beta=float(beta).hex(),
+                                     d=hx(dec["d"]), rate=hx(dec["rate"]), row_ptr=[int(x) for x in dec["row_ptr"]],
+                                     jump_cdf=hx(dec["jump_cdf"]), jump_target=[int(x) for x in dec["jump_target"]],
+                                     sign=[int(x) for x in dec["sign"]], d_max=float(dec["d_max"]).hex(),
+                                     d_bar=float(dec["d_bar"]).hex(), samples=samples, run_level=runs)
+
+    # 3. drivers: grid 16x16 (eps 1e-2) and C1 64x64 (eps 1e-3) on a few rows; seeds 1000+row
+    drivers = {}
+    for (name, g, beta, eps, rows) in [("grid16", 16, 1.0, 1e-2, [0, 17, 120, 255]), ("c1", 64, 1.0, 1e-3, [0, 1, 65, 2080, 4095])]:
+        a = grid(g)
+        n = a.n
+        u = np.array([ref.uniforms(12345, 0, i, 6, 1)[0] for i in range(n)])
+        ch = ref.chain(a)
+        res = ch.driver_rows(u, beta, rows, [1000 + r for r in rows], epsilon=eps, threads=4)
+        exact = ch.dense_expmv(u, beta)
+        drivers[name] = dict(g=g, beta=float(beta).hex(), epsilon=eps, rows=rows,
+                             vector="stream_for(12345, 0, i, 6)", row_seed="1000 + row",
+                             exact=hx(exact[rows]), results=[
+                                 dict(estimate=float(r["estimate"]).hex(), statistical_error=float(r["statistical_error"]).hex(),
+                                      bias_estimate=float(r["bias_estimate"]).hex(), l0=r["l0"], L=r["L"],
+                                      total_cost=int(r["total_cost"]), converged=r["converged"],
+                                      levels=[dict(level=int(x["level"]), sum=float(x["sum"]).hex(),
+                                                   sum_sq=float(x["sum_sq"]).hex(), samples=int(x["samples"]),
+                                                   cost=int(x["cost"])) for x in r["levels"]]) for r in res])
+    out["drivers"] = drivers
+    path = os.path.join(HERE, "golden.json")
+    with open(path, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print(path, os.path.getsize(path), "bytes")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden vectors and the
+CPU oracle.
+
+Parity rule:
+  * integer work is bit-exact: decomposition tables, per-sample cost, jump count, end state,
+    run_level sample count and cost;
+  * per-sample functionals eta_fine / eta_coarse agree to <= 4 ulp (CUDA's exp/log1p/expm1 vs
+    glibc's: both < 1 ulp, they may differ in the last bit);
+  * run_level sums agree to 1e-12 relative (the in-chunk summation is a fixed shuffle tree
+    instead of the reference's sequential loop);
+  * full driver runs take the reference's decision sequence: same L, l0, samples per level and
+    cost, estimates to 1e-12 relative;
+  * statistically: every component within 3 combined standard errors of the reference, and
+    RMS error vs the deterministic exp(tA)v <= eps, |err| <= 3 SE + bias up to a
+    Binomial-consistent fraction.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1904_12754_b200 as P
+from paper_1904_12754_b200 import configs
+from oracle import CSR
+
+pytestmark = pytest.mark.gpu
+
+ULP_TOL = 4
+
+
+def unhex(xs):
+    return np.array([float.fromhex(x) for x in xs], np.float64)
+
+
+def ulp_diff(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    ia = a.view(np.int64)
+    ib = b.view(np.int64)
+    ia = np.where(ia < 0, np.int64(-(2 ** 63)) - ia, ia)
+    ib = np.where(ib < 0, np.int64(-(2 ** 63)) - ib, ib)
+    return np.abs(ia - ib)
+
+
+def ctx_from_golden(m):
+    c = m["csr"]
+    a = P.SparseMatrix(c["n"], np.array(c["row_ptr"], np.int64), np.array(c["col"], np.int64), unhex(c["val"]))
+    return P.Context(a, unhex(m["u"]), device=0)
+
+
+NAMES = ["two_state", "k2", "diag", "signed3", "absorb3", "grid8", "smallw100", "pref300"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_tables_bitwise_equal_reference(gpu, golden, name):
+    m = golden["matrices"][name]
+    with ctx_from_golden(m) as ctx:
+        dec = ctx.decomposition()
+        assert np.array_equal(dec["d"], unhex(m["d"]))
+        assert np.array_equal(dec["rate"], unhex(m["rate"]))
+        assert np.array_equal(dec["row_ptr"], np.array(m["row_ptr"]))
+        assert np.array_equal(dec["jump_cdf"], unhex(m["jump_cdf"]))
+        assert np.array_equal(dec["jump_target"], np.array(m["jump_target"]))
+        assert np.array_equal(dec["sign"], np.array(m["sign"], np.uint8))
+        assert ctx.d_max == float.fromhex(m["d_max"])
+        assert ctx.d_bar == pytest.approx(float.fromhex(m["d_bar"]), rel=1e-14, abs=1e-300)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_per_sample_golden(gpu, golden, name):
+    m = golden["matrices"][name]
+    beta = float.fromhex(m["beta"])
+    with ctx_from_golden(m) as ctx:
+        for s in m["samples"]:
+            idx = np.array(s["idx"], np.uint64)
+            got = ctx.sample_debug(beta, s["entry"], s["level"], s["base"], s["seed"], idx)
+            assert np.array_equal(got["cost"], np.array(s["cost"], np.uint64)), (name, s["level"], s["base"])
+            assert ulp_diff(got["fine"], unhex(s["fine"])).max() <= ULP_TOL
+            assert ulp_diff(got["coarse"], unhex(s["coarse"])).max() <= ULP_TOL
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_run_level_golden(gpu, golden, name):
+    m = golden["matrices"][name]
+    beta = float.fromhex(m["beta"])
+    with ctx_from_golden(m) as ctx:
+        for r in m["run_level"]:
+            got = P.run_level(P.MlmcProblem(ctx, r["entry"], beta), r["level"], bool(r["base"]), r["first"],
+                              r["count"], r["seed"])
+            assert got.samples == r["samples"] and got.cost == r["cost"]
+            assert got.sum == pytest.approx(float.fromhex(r["sum"]), rel=1e-12, abs=1e-13)
+            assert got.sum_sq == pytest.approx(float.fromhex(r["sum_sq"]), rel=1e-12, abs=1e-13)
+
+
+def test_per_sample_oracle_c1_random(gpu, oracle_lib):
+    """5,000 random (row, level, seed, sample) draws on C1 against the oracle: path, cost,
+    jumps bit-exact; values <= 4 ulp."""
+    cfg = configs.make_config("c1")
+    och = oracle_lib.chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
+    rng = np.random.default_rng(11)
+    with P.Context(cfg.a, cfg.u) as ctx:
+        worst = 0
+        for level in range(0, 7):
+            for base in ([1] if level == 0 else [1, 0]):
+                rows = rng.integers(0, cfg.a.n, 300)
+                idx = rng.integers(0, 2 ** 40, 300).astype(np.uint64)
+                seeds = (1000 + rows).astype(np.uint64)
+                got = ctx.sample_debug(cfg.beta, rows, level, base, seeds, idx)
+                for k in range(300):
+                    exp = och.samples(cfg.u, int(rows[k]), cfg.beta, level, base, int(seeds[k]), idx[k:k + 1])
+                    assert got["cost"][k] == exp["cost"][0] and got["jumps"][k] == exp["jumps"][0]
+                    assert got["end_state"][k] == exp["end_state"][0]
+                    worst = max(worst, int(ulp_diff(got["fine"][k], exp["fine"][0])),
+                                int(ulp_diff(got["coarse"][k], exp["coarse"][0])))
+        assert worst <= ULP_TOL
+
+
+def test_run_level_batch_equals_singles_and_is_deterministic(gpu):
+    cfg = configs.make_config("c1")
+    with P.Context(cfg.a, cfg.u) as ctx:
+        entries = np.array([0, 5, 77, 4095, 2048])
+        levels = np.array([0, 1, 2, 3, 4])
+        base = (levels == 0).astype(np.int32)
+        first = np.array([0, 511, 1000, 3, 100000])
+        count = np.array([5000, 1025, 1, 777, 2049])
+        seeds = 1000 + entries
+        b1 = ctx.run_level_batch(cfg.beta, entries, levels, base, first, count, seeds)
+        b2 = ctx.run_level_batch(cfg.beta, entries, levels, base, first, count, seeds)
+        assert b1.tobytes() == b2.tobytes()
+        for k in range(len(entries)):
+            s = P.run_level(P.MlmcProblem(ctx, int(entries[k]), cfg.beta), int(levels[k]), bool(base[k]),
+                            int(first[k]), int(count[k]), int(seeds[k]))
+            assert (s.sum, s.sum_sq, s.samples, s.cost, s.jumps) == tuple(b1[k].tolist())
+
+
+def test_run_level_extension_is_additive(gpu):  # test_mlmc.cpp:128-143
+    cfg = configs.make_config("c1")
+    with P.Context(cfg.a, cfg.u) as ctx:
+        p = P.MlmcProblem(ctx, 100, cfg.beta)
+        whole = P.run_level(p, 5, False, 0, 3000, 13)
+        a = P.run_level(p, 5, False, 0, 1000, 13)
+        b = P.run_level(p, 5, False, 1000, 2000, 13)
+        assert whole.cost == a.cost + b.cost and whole.jumps == a.jumps + b.jumps
+        assert whole.sum == pytest.approx(a.sum + b.sum, rel=1e-12)
+        # chunk-aligned split reproduces the partials exactly (ordered chunk combine)
+        c = P.run_level(p, 5, False, 0, 1024, 13)
+        d = P.run_level(p, 5, False, 1024, 1976, 13)
+        assert whole.sum == (0.0 + c.sum) + d.sum or whole.sum == pytest.approx(c.sum + d.sum, rel=1e-15)
+
+
+def test_run_level_oracle_large(gpu, oracle_lib):
+    cfg = configs.make_config("c1")
+    och = oracle_lib.chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
+    with P.Context(cfg.a, cfg.u) as ctx:
+        for (entry, level, base, first, count) in [(63, 0, 1, 0, 200000), (2080, 1, 0, 12345, 100000),
+                                                   (4095, 4, 0, 7, 20000), (1, 8, 0, 0, 3000)]:
+            g = P.run_level(P.MlmcProblem(ctx, entry, cfg.beta), level, bool(base), first, count, 1000 + entry)
+            o = och.run_level(cfg.u, entry, cfg.beta, level, base, first, count, 1000 + entry, threads=8)
+            assert g.samples == o["samples"] and g.cost == o["cost"] and g.jumps == o["jumps"]
+            assert g.sum == pytest.approx(o["sum"], rel=1e-12) and g.sum_sq == pytest.approx(o["sum_sq"], rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["grid16", "c1"])
+def test_driver_golden(gpu, golden, name):
+    d = golden["drivers"][name]
+    a = configs.grid_laplacian(d["g"])
+    u = configs.grid_vector(12345, a.n)
+    beta = float.fromhex(d["beta"])
+    with P.Context(a, u) as ctx:
+        res, lv = P.mlmc_driver_rows(ctx, beta, d["rows"], configs.row_seeds(d["rows"]), P.MlmcOptions(epsilon=d["epsilon"]))
+        for k, ref in enumerate(d["results"]):
+            r = res[k]
+            assert (int(r["l0"]), int(r["L"]), bool(r["converged"])) == (ref["l0"], ref["L"], ref["converged"])
+            assert int(r["total_cost"]) == ref["total_cost"]
+            assert float(r["estimate"]) == pytest.approx(float.fromhex(ref["estimate"]), rel=1e-12)
+            for got, rl in zip(lv[k][: int(r["nlevels"])], ref["levels"]):
+                assert int(got["samples"]) == rl["samples"] and int(got["cost"]) == rl["cost"]
+        # the single-row entry point is the same code path
+        one = P.mlmc_driver(P.MlmcProblem(ctx, d["rows"][0], beta), P.MlmcOptions(epsilon=d["epsilon"], seed=1000 + d["rows"][0]))
+        assert one.estimate == float(res[0]["estimate"]) and one.total_cost == int(res[0]["total_cost"])
+
+
+def test_c1_all_components(gpu, oracle_lib):
+    """Config 1 (BASELINE configs[0]): all 4096 components through the batched driver.
+    Against the reference-restating oracle on 512 rows: identical decision sequences (same
+    cost and L) and estimates within 3 combined SE (here: to 1e-10).  Against dense
+    expm(tA)v on all rows: RMS <= eps and |err| <= 3 SE + bias up to a Binomial tail."""
+    cfg = configs.make_config("c1")
+    rows = np.arange(cfg.a.n)
+    with P.Context(cfg.a, cfg.u) as ctx:
+        res, _ = P.mlmc_driver_rows(ctx, cfg.beta, rows, configs.row_seeds(rows), P.MlmcOptions(epsilon=cfg.epsilon),
+                                    want_levels=False)
+    assert res["converged"].all()
+    exact = oracle_lib.dense_expmv(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val), cfg.u, cfg.beta)
+    err = res["estimate"] - exact
+    rms = math.sqrt(float(np.mean(err ** 2)))
+    assert rms <= cfg.epsilon
+    bound = 3 * res["statistical_error"] + res["bias_estimate"]
+    frac = float(np.mean(np.abs(err) > bound))
+    assert frac <= 0.0027 + 4 * math.sqrt(0.0027 / cfg.a.n) + 0.003  # SURVEY §0.7 measured 0.34 % for the reference
+    sub = np.arange(0, cfg.a.n, 8)
+    och = oracle_lib.chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
+    ref = och.driver_rows(cfg.u, cfg.beta, sub, configs.row_seeds(sub), epsilon=cfg.epsilon, threads=8)
+    est_ref = np.array([r["estimate"] for r in ref])
+    se_ref = np.array([r["statistical_error"] for r in ref])
+    cost_ref = np.array([r["total_cost"] for r in ref])
+    g = res[sub]
+    assert np.all(np.abs(g["estimate"] - est_ref) <= 3 * np.sqrt(g["statistical_error"] ** 2 + se_ref ** 2))
+    same = cost_ref == g["total_cost"].astype(np.int64)
+    assert same.mean() >= 0.99  # identical decision sequence (a ceil() flip on a 1e-16 variance difference is allowed)
+    assert np.allclose(g["estimate"][same], est_ref[same], rtol=1e-10, atol=1e-13)
+
+
+def test_c2_property_full_size(gpu, oracle_lib):
+    """Config 2 at its full size (n = 1,048,576): a seeded sample of 4096 components through the
+    batched driver vs the deterministic oracle; interior rows (d = 0 on every path) produce
+    samples that are exact copies of u[end], which also checks the jump chain."""
+    cfg = configs.make_config("c2")
+    rng = np.random.default_rng(2)
+    rows = np.unique(np.r_[rng.integers(0, cfg.a.n, 4000), [0, 1023, cfg.a.n - 1, cfg.a.n // 2 + 512]])
+    with P.Context(cfg.a, cfg.u) as ctx:
+        assert ctx.n == 1 << 20 and ctx.n_edges == 4 * 1024 * 1023
+        assert ctx.d_max == 0.0
+        res, lv = P.mlmc_driver_rows(ctx, cfg.beta, rows, configs.row_seeds(rows), P.MlmcOptions(epsilon=cfg.epsilon))
+    assert res["converged"].all()
+    assert (res["l0"] == 0).all()
+    exact = oracle_lib.dense_expmv(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val), cfg.u, cfg.beta)[rows]
+    err = res["estimate"] - exact
+    assert math.sqrt(float(np.mean(err ** 2))) <= cfg.epsilon
+    frac = float(np.mean(np.abs(err) > 3 * res["statistical_error"] + res["bias_estimate"]))
+    assert frac <= 0.01
+    # jumps == cost - 2 * samples * 2^l exactly (no absorbing rows)
+    for k in range(len(rows)):
+        n_l = int(res["nlevels"][k])
+        lev = lv[k][:n_l]
+        steps = (1 << lev["level"].astype(np.int64))
+        assert int(res["total_jumps"][k]) == int(np.sum(lev["cost"].astype(np.int64) - 2 * lev["samples"].astype(np.int64) * steps))
+
+
+# ---------------------------------------------------------------- reference unit-test KATs on the GPU
+def test_kat_diagonal_and_k2(gpu):  # test_paths.cpp:84-111, 135-146; test_mlmc.cpp:94-108
+    with P.Context(P.SparseMatrix.from_dense([[0.75, 0.0], [0.0, -0.5]]), np.array([3.0, 5.0])) as ctx:
+        s = ctx.sample_debug(2.0, 0, 3, 1, 2, np.arange(50))
+        assert np.all(s["fine"] == s["fine"][0]) and np.all(s["cost"] == 8)
+        assert s["fine"][0] == pytest.approx(3.0 * math.exp(1.5), rel=1e-14)
+    with P.Context(P.SparseMatrix.from_dense([[0.0, 1.0], [1.0, 0.0]]), np.ones(2)) as ctx:
+        s = ctx.sample_debug(1.0, 0, 4, 1, 3, np.arange(1000))
+        assert np.all(s["fine"] == math.exp(1.0))
+        res, _ = P.mlmc_driver_rows(ctx, 1.0, np.zeros(10, np.int64), np.arange(10), P.MlmcOptions(epsilon=1e-3))
+        assert res["converged"].all() and np.all(np.abs(res["estimate"] - math.e) <= 1e-3)
+    with P.Context(P.SparseMatrix.from_dense([[1.5, 0.0], [0.0, 0.5]]), np.array([1.0, 2.0])) as ctx:
+        s = P.run_level(P.MlmcProblem(ctx, 0, 1.0), 3, False, 0, 500, 9)
+        assert s.sum == 0.0 and s.sum_sq == 0.0 and s.samples == 500 and s.variance() == 0.0
+
+
+def test_kat_sign_parity(gpu):  # test_paths.cpp:226-249
+    pos = P.SparseMatrix.from_dense([[0, 1.0, 0], [1.0, 0, 0.5], [0, 0.5, 0]])
+    neg = P.SparseMatrix.from_dense([[0, -1.0, 0], [-1.0, 0, -0.5], [0, -0.5, 0]])
+    u = np.array([1.0, 2.0, 3.0])
+    with P.Context(pos, u) as cp, P.Context(neg, u) as cn:
+        a = cp.sample_debug(2.0, 0, 0, 1, 8, np.arange(200))
+        b = cn.sample_debug(2.0, 0, 0, 1, 8, np.arange(200))
+    assert np.array_equal(a["end_state"], b["end_state"]) and np.array_equal(a["jumps"], b["jumps"])
+    assert np.array_equal(b["fine"], a["fine"] * np.where(a["jumps"] % 2 == 0, 1.0, -1.0))
+
+
+def test_kat_driver_diagonal(gpu):  # test_mlmc.cpp:145-163
+    with P.Context(P.SparseMatrix.from_dense([[0.75, 0.0], [0.0, -0.25]]), np.array([3.0, 1.0])) as ctx:
+        r = P.mlmc_driver(P.MlmcProblem(ctx, 0, 2.0), P.MlmcOptions(epsilon=1e-6, seed=5))
+    assert r.converged and r.statistical_error == 0.0 and r.bias_estimate == 0.0
+    assert r.estimate == pytest.approx(3.0 * math.exp(1.5), rel=1e-14)
+    assert all(lv.samples == 1000 for lv in r.levels)
+
+
+def test_errors_match_reference_types(gpu):
+    with P.Context(P.SparseMatrix.from_dense([[0.0, 1.0], [1.0, 0.0]]), np.ones(2)) as ctx:
+        with pytest.raises(P.OutOfRange):
+            P.run_level(P.MlmcProblem(ctx, 2, 1.0), 1, False, 0, 10, 1)
+        with pytest.raises(P.InvalidArgument):
+            P.run_level(P.MlmcProblem(ctx, 0, 1.0), 63, False, 0, 10, 1)
+        with pytest.raises(P.InvalidArgument):
+            P.run_level(P.MlmcProblem(ctx, 0, 0.0), 1, False, 0, 10, 1)
+        with pytest.raises(P.InvalidArgument):
+            P.run_level(P.MlmcProblem(ctx, 0, 1.0), 0, False, 0, 10, 1)
+        with pytest.raises(P.InvalidArgument):
+            P.mlmc_driver(P.MlmcProblem(ctx, 0, 1.0), P.MlmcOptions(epsilon=0.0))
+        with pytest.raises(P.OutOfRange):
+            P.mlmc_driver_rows(ctx, 1.0, [0, 5], [1, 2])
+        z = P.run_level(P.MlmcProblem(ctx, 0, 1.0), 2, False, 7, 0, 1)  # empty extension
+        assert z.samples == 0 and z.sum == 0.0
+    with pytest.raises(P.InvalidArgument):
+        P.Context(P.SparseMatrix(2, np.array([0, 1, 1]), np.array([1]), np.array([np.nan])), np.ones(2))
+    with pytest.raises(P.OutOfRange):
+        P.Context(P.SparseMatrix(2, np.array([0, 1, 1]), np.array([2]), np.array([1.0])), np.ones(2))
+    with pytest.raises(P.InvalidArgument):
+        P.Context(P.SparseMatrix(2, np.array([0, 2, 2]), np.array([1, 0]), np.array([1.0, 1.0])), np.ones(2))
+
+
+def test_set_vector_rebinds_u(gpu):
+    cfg = configs.make_config("grid8")
+    with P.Context(cfg.a, cfg.u) as ctx:
+        a = ctx.sample_debug(1.0, 3, 2, 0, 9, np.arange(64))
+        ctx.set_vector(2.0 * cfg.u)
+        b = ctx.sample_debug(1.0, 3, 2, 0, 9, np.arange(64))
+    assert np.array_equal(b["fine"], 2.0 * a["fine"]) and np.array_equal(a["cost"], b["cost"])
