@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libexpmc_b200.so")
+LIB_PATH = os.environ.get("EXPMC_LIB") or os.path.join(_HERE, "_lib", "libexpmc_b200.so")
 
 _I32, _I64, _U32, _U64, _D = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 

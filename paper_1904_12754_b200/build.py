@@ -32,25 +32,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile the library (to `out`, default the in-tree _lib/libexpmc_b200.so)."""
+    lib = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     # the image exports CC/CXX pointing at a gcc wrapper; nvcc's host compiler is explicit
     ccbin = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
     cmd = [NVCC, *ARCH, *FLAGS, "-ccbin", ccbin, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+           *[f"-D{d}" for d in defines], *[os.path.join(CSRC, s) for s in SOURCES], "-o", lib + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(LIBDIR, "build.log")
+    log = lib + ".build.log"
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError(f"nvcc failed (see {log})")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     if verbose:
         sys.stdout.write(r.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

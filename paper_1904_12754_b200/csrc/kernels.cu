@@ -23,6 +23,10 @@ namespace expmc_b200 {
 
 namespace {
 
+#ifndef EXPMC_SAMPLER_MINB
+#define EXPMC_SAMPLER_MINB 4  // resident 256-thread blocks per SM the sampler is register-budgeted for
+#endif
+
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
@@ -49,10 +53,12 @@ __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ chunk
     return lo;
 }
 
-__global__ void __launch_bounds__(kThreads) k_sample(SamplerArgs a) {
+__global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(SamplerArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned full = 0xFFFFFFFFu;
     const unsigned lt_mask = (1u << lane) - 1u;
+    __shared__ ItemConst s_ic[kWarps];  // per-warp item constants: read at use, not held in registers
+    ItemConst& ic = s_ic[threadIdx.x >> 5];
     uint32_t hint = 0;
     for (;;) {
         uint32_t gi = 0;
@@ -63,7 +69,11 @@ __global__ void __launch_bounds__(kThreads) k_sample(SamplerArgs a) {
 
         const uint32_t item = find_item(a.chunk0, a.nitems, g, hint);
         hint = item;
-        const ItemConst ic = load_item(a.items, item, a.rows);
+        {
+            const ItemConst c = load_item(a.items, item);
+            if (lane == 0) ic = c;
+            __syncwarp();
+        }
         const DevItem& it = a.items[item];
         const uint64_t first = it.first, end = it.first + it.count;
         const uint64_t chunk = first / kChunk + (g - a.chunk0[item]);
@@ -81,20 +91,17 @@ __global__ void __launch_bounds__(kThreads) k_sample(SamplerArgs a) {
             if (!active) {
                 const uint32_t mine = next + __popc(need & lt_mask);
                 if (mine < cnt) {
-                    walker_start(w, ic, lo + mine);
+                    walker_start(w, ic, a.rows, lo + mine);
                     active = true;
                 }
             }
             next += __popc(need);
             if (!__any_sync(full, active)) break;
-            if (active && walker_event(w, ic, a.rows, a.edges)) {
-                double fine, coarse;
-                walker_finish(w, ic, fine, coarse);
-                const double x = ic.base ? fine : __dsub_rn(fine, coarse);
+            if (active && walker_event(w, ic, a.rows, a.edges, cost, jumps)) {
+                const double x = walker_sample(w, ic, a.rows);
                 sum = __dadd_rn(sum, x);
                 sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
-                cost += w.draws + ic.nsteps;
-                jumps += w.jumps;
+                cost += ic.nsteps;
                 active = false;
             }
         }
@@ -138,15 +145,16 @@ __global__ void k_debug(const RowRec* __restrict__ rows, const EdgeRec* __restri
                         const DevItem* __restrict__ items, uint32_t n, SampleOut* __restrict__ out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const ItemConst ic = load_item(items, i, rows);
+    const ItemConst ic = load_item(items, i);
     Walker w;
-    walker_start(w, ic, items[i].first);
-    while (!walker_event(w, ic, rows, edges)) {
+    walker_start(w, ic, rows, items[i].first);
+    unsigned long long draws = 0, jumps = 0;
+    while (!walker_event(w, ic, rows, edges, draws, jumps)) {
     }
     SampleOut o;
-    walker_finish(w, ic, o.fine, o.coarse);
-    o.cost = w.draws + ic.nsteps;
-    o.jumps = w.jumps;
+    walker_finish(w, ic, rows, o.fine, o.coarse);
+    o.cost = draws + ic.nsteps;
+    o.jumps = jumps;
     o.end_state = w.state;
     out[i] = o;
 }

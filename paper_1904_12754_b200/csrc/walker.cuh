@@ -6,6 +6,12 @@
 // Every floating-point expression that can round differently under FMA contraction is
 // written with explicit __d*_rn intrinsics in the reference's evaluation order; the only
 // remaining source of difference is CUDA's log1p/expm1/exp vs glibc (both < 1 ulp).
+//
+// SIMT shape: a warp advances 32 independent paths one EVENT per loop trip (one pass of
+// evolve_common's for(;;) body).  Each event has exactly one call site for every expensive
+// operation -- one Philox block (the stream keeps a 3-word queue so one refill per event is
+// always enough for the u and v draws) and one log1p (the threshold test runs in log space,
+// see below) -- so a diverged warp pays each of them at most once per trip.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -17,11 +23,11 @@ namespace expmc_b200 {
 
 // ----------------------------------------------------------------------------- Philox
 struct Stream {
-    uint32_t k0, k1;      // key = (seed_lo, seed_hi)                  rng.hpp:25
-    uint32_t c1, c2, c3;  // counter words 1..3 = (sample_lo, sample_hi, level|lane<<24)
-    uint32_t block;       // counter word 0, one per 128-bit block      rng.hpp:56
-    uint64_t buf;         // the second word of the last block (buffer_[0])
-    uint32_t has;         // 1 if buf is still unconsumed
+    uint32_t k0, k1;       // key = (seed_lo, seed_hi)                       rng.hpp:25
+    uint32_t c1, c2, c3;   // counter words 1..3 = (sample_lo, sample_hi, level|lane<<24)
+    uint32_t block;        // counter word 0, one per 128-bit block           rng.hpp:56
+    uint64_t w0, w1, w2;   // queue of unconsumed 64-bit words, w0 next
+    uint32_t n;            // queued words
 };
 
 __device__ __forceinline__ void stream_init(Stream& s, uint64_t seed, uint64_t sample, uint32_t key3) {
@@ -31,8 +37,8 @@ __device__ __forceinline__ void stream_init(Stream& s, uint64_t seed, uint64_t s
     s.c2 = static_cast<uint32_t>(sample >> 32);
     s.c3 = key3;
     s.block = 0;
-    s.buf = 0;
-    s.has = 0;
+    s.w0 = s.w1 = s.w2 = 0;
+    s.n = 0;
 }
 
 // Philox4x32 with 10 rounds and the Weyl key schedule (rng.hpp:44-62).
@@ -53,37 +59,49 @@ __device__ __forceinline__ void philox10(uint32_t& c0, uint32_t& c1, uint32_t& c
     }
 }
 
-// next_uniform (rng.hpp:32-36): a refill yields words (c0c1, c2c3); c2c3 is consumed first.
-__device__ __forceinline__ double next_uniform(Stream& s) {
-    uint64_t bits;
-    if (!s.has) {
+// Make sure two words are queued (an event draws at most u and v).  A refill appends the
+// block's words in the reference's consumption order: (c2,c3) first, then (c0,c1)
+// (rng.hpp:32-36, 63-65).
+__device__ __forceinline__ void stream_reserve2(Stream& s) {
+    if (s.n < 2u) {
         uint32_t c0 = s.block++, c1 = s.c1, c2 = s.c2, c3 = s.c3;
         philox10(c0, c1, c2, c3, s.k0, s.k1);
-        s.buf = (static_cast<uint64_t>(c0) << 32) | c1;
-        bits = (static_cast<uint64_t>(c2) << 32) | c3;
-        s.has = 1;
-    } else {
-        bits = s.buf;
-        s.has = 0;
+        const uint64_t first = (static_cast<uint64_t>(c2) << 32) | c3;
+        const uint64_t second = (static_cast<uint64_t>(c0) << 32) | c1;
+        if (s.n == 0u) {
+            s.w0 = first;
+            s.w1 = second;
+        } else {
+            s.w1 = first;
+            s.w2 = second;
+        }
+        s.n += 2u;
     }
+}
+
+// next_uniform: 53 random bits -> [0,1) exactly as rng.hpp:35.
+__device__ __forceinline__ double stream_pop(Stream& s) {
+    const uint64_t bits = s.w0;
+    s.w0 = s.w1;
+    s.w1 = s.w2;
+    --s.n;
     return __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);
 }
 
 // ----------------------------------------------------------------------------- tables
-struct Row {
-    double d, rate, u;
+struct Row {  // u_i is not kept in registers: walker_finish reloads it for the end state
+    double d, rate;
     uint32_t begin, deg;
 };
 
 __device__ __forceinline__ Row load_row(const RowRec* __restrict__ rows, uint32_t i) {
     const double2 a = __ldg(reinterpret_cast<const double2*>(rows + i));
-    const uint4 b = __ldg(reinterpret_cast<const uint4*>(rows + i) + 1);
+    const uint2 b = __ldg(reinterpret_cast<const uint2*>(rows + i) + 3);
     Row r;
     r.d = a.x;
     r.rate = a.y;
-    r.u = __hiloint2double(static_cast<int>(b.y), static_cast<int>(b.x));
-    r.begin = b.z;
-    r.deg = b.w;
+    r.begin = b.x;
+    r.deg = b.y;
     return r;
 }
 
@@ -130,14 +148,22 @@ __device__ __forceinline__ void pick_edge(const EdgeRec* __restrict__ edges, uin
 }
 
 // ----------------------------------------------------------------------------- walker
+// Holding-interval test in log space.  The reference decides "no jump in the rest of the
+// interval" by u >= q with q = -expm1(-rate*remaining) (paths.cpp:53, 68, 90) and, on a jump,
+// spends E = -log1p(-u) of the interval (paths.cpp:54).  Mathematically u >= 1 - e^{-x} is
+// E >= x (x = rate*remaining), so the walker computes E once per event and compares it with
+// x: the draws consumed, the jump chain, the exponents and every sample value are the
+// reference's; the only difference is that a u lying within one ulp of the threshold may
+// round the other way (probability ~1e-16 per event -- the same order as the CUDA-vs-glibc
+// expm1 ulp differences that reference-order sampling has to accept anyway).  This removes the
+// expm1 from every event and the per-level nojump_ table altogether.
+
 // Per-item constants (uniform across the warp while it works on one chunk).
 struct ItemConst {
     uint64_t seed;
     uint64_t nsteps;
     double dt;
     double half_dt;  // dt_ * 0.5, the left factor of paths.cpp:110
-    double qdt_entry;
-    Row entry_row;
     uint32_t entry;
     uint32_t key3;
     uint32_t base;
@@ -147,64 +173,57 @@ struct Walker {
     Stream st;
     Row cur;               // row record of the current state
     uint32_t state;
-    uint32_t qstate;       // state whose step-start threshold is cached in qdt
     int32_t sign;
     uint32_t half;         // coupled: 0 before the pair's middle node, 1 after
     double remaining;      // time left in the current fine step
-    double q;              // no-jump threshold for the current holding interval
-    double qdt;            // -expm1(-rate[qstate] * dt), the LevelSampler nojump_ entry
     double acc_a, acc_b;   // single: expo; coupled: coarse, delta
     double d0, d1;         // d[s0], d[s1]
     uint64_t step;         // completed fine steps
-    uint64_t draws, jumps;
 };
 
-__device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, uint64_t sample) {
+__device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+                                             uint64_t sample) {
     stream_init(w.st, ic.seed, sample, ic.key3);
-    w.cur = ic.entry_row;
+    w.cur = load_row(rows, ic.entry);  // L1-resident: every lane of the warp starts here
     w.state = ic.entry;
-    w.qstate = ic.entry;
     w.sign = 1;
     w.half = 0;
     w.remaining = ic.dt;
-    w.q = ic.qdt_entry;
-    w.qdt = ic.qdt_entry;
     w.acc_a = 0.0;
     w.acc_b = 0.0;
-    w.d0 = ic.entry_row.d;
+    w.d0 = w.cur.d;
     w.d1 = 0.0;
     w.step = 0;
-    w.draws = 0;
-    w.jumps = 0;
 }
 
 // One event of the path: one pass of evolve_common's for(;;) body, plus the step
 // bookkeeping of single/coupled when the holding interval ends the fine step.
-// Returns true when the sample's last fine step has completed.
+// Returns true when the sample's last fine step has completed.  Exponential draws and jumps
+// are counted straight into the caller's accumulators (cost = draws + fine steps,
+// paths.hpp:22-23; the fine steps are added by the caller when the sample ends).
 __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
-                                             const EdgeRec* __restrict__ edges) {
+                                             const EdgeRec* __restrict__ edges, unsigned long long& draws,
+                                             unsigned long long& jumps) {
+    stream_reserve2(w.st);  // the event's only Philox call site
     bool step_done = true;
     if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
-        const double u = next_uniform(w.st);
-        ++w.draws;
-        if (u < w.q) {  // u >= q: holding time exceeds the rest of the interval (paths.cpp:53)
-            // remaining -= -log1p(-u) / rate                                  paths.cpp:54
-            w.remaining = __dsub_rn(w.remaining, __ddiv_rn(-log1p(-u), w.cur.rate));
-            ++w.jumps;
-            const double v = next_uniform(w.st);
+        const double u = stream_pop(w.st);
+        ++draws;
+        const double e = -log1p(-u);  // the event's only transcendental
+        if (e < __dmul_rn(w.cur.rate, w.remaining)) {  // == (u < q), see above
+            w.remaining = __dsub_rn(w.remaining, __ddiv_rn(e, w.cur.rate));  // paths.cpp:54
+            ++jumps;
+            const double v = stream_pop(w.st);
             uint32_t target, sgn;
             pick_edge(edges, w.cur.begin, w.cur.deg, v, target, sgn);
             if (sgn) w.sign = -w.sign;
             w.state = target;
             w.cur = load_row(rows, target);
-            if (w.remaining > 0.0) {  // else: rounding pushed past the boundary (paths.cpp:67)
-                w.q = -expm1(__dmul_rn(-w.cur.rate, w.remaining));  // paths.cpp:68
-                step_done = false;
-            }
+            // remaining <= 0: rounding pushed past the boundary, the step ends (paths.cpp:67)
+            step_done = !(w.remaining > 0.0);
         }
     }
     if (!step_done) return false;
-
     // ---- the fine step ended in w.state
     const double dn = w.cur.d;
     if (ic.base) {
@@ -224,33 +243,40 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
         w.half = 0u;
     }
     if (++w.step == ic.nsteps) return true;
-    // next fine step: fresh holding interval of length dt with q = nojump_[state] (paths.cpp:95-96)
-    w.remaining = ic.dt;
-    if (w.state != w.qstate) {
-        w.qdt = -expm1(__dmul_rn(-w.cur.rate, ic.dt));  // paths.cpp:90
-        w.qstate = w.state;
-    }
-    w.q = w.qdt;
+    w.remaining = ic.dt;  // next fine step: fresh holding interval of length dt (paths.cpp:95-96)
     return false;
 }
 
+// exp(x) with the exact shortcut exp(0) = 1 (both libms return exactly 1): rows whose d is
+// constant along the path (every interior row of a Laplacian) never pay for the exp.
+__device__ __forceinline__ double exp_or_one(double x) { return x == 0.0 ? 1.0 : exp(x); }
+
 // Terminal values: single -> (sign * e^expo) * u[end] (paths.cpp:112);
 // coupled -> uf = sign * u[end]; (uf e^{coarse+delta}, uf e^{coarse}) (paths.cpp:138-140).
-__device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& ic, double& fine,
-                                              double& coarse) {
+__device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+                                              double& fine, double& coarse) {
     const double sg = static_cast<double>(w.sign);
+    const double u_end = __ldg(&rows[w.state].u);  // same sector as the last row record read
     if (ic.base) {
-        fine = __dmul_rn(__dmul_rn(sg, exp(w.acc_a)), w.cur.u);
+        fine = __dmul_rn(__dmul_rn(sg, exp_or_one(w.acc_a)), u_end);
         coarse = 0.0;
     } else {
-        const double uf = __dmul_rn(sg, w.cur.u);
-        fine = __dmul_rn(uf, exp(__dadd_rn(w.acc_a, w.acc_b)));
-        coarse = __dmul_rn(uf, exp(w.acc_a));
+        const double uf = __dmul_rn(sg, u_end);
+        fine = __dmul_rn(uf, exp_or_one(__dadd_rn(w.acc_a, w.acc_b)));
+        coarse = __dmul_rn(uf, exp_or_one(w.acc_a));
     }
 }
 
-__device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items, uint32_t i,
-                                               const RowRec* __restrict__ rows) {
+// The level-statistics sample x = P_l (base) or P_l - P_{l-1} (coupled), as run_level_ex adds
+// it (mlmc.cpp:103-108).  delta == 0 makes fine and coarse bitwise equal, so x = 0 exactly.
+__device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows) {
+    if (!ic.base && w.acc_b == 0.0) return 0.0;
+    double fine, coarse;
+    walker_finish(w, ic, rows, fine, coarse);
+    return ic.base ? fine : __dsub_rn(fine, coarse);
+}
+
+__device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items, uint32_t i) {
     const DevItem it = items[i];
     ItemConst ic;
     ic.seed = it.seed;
@@ -260,8 +286,6 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.entry = it.entry;
     ic.key3 = it.key3;
     ic.base = it.base;
-    ic.entry_row = load_row(rows, it.entry);
-    ic.qdt_entry = -expm1(__dmul_rn(-ic.entry_row.rate, it.dt));
     return ic;
 }
 
