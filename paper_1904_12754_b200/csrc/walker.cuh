@@ -17,9 +17,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "fastmath.cuh"
 #include "internal.hpp"
 
 namespace expmc_b200 {
+
+// log1p polynomial of fast_log in constant memory: DFMA reads it as a c[] operand directly.
+__constant__ double c_log_poly[7] = EXPMC_LOG_POLY;
+__device__ const LogEntry g_log_table[128] = {
+#include "log_table.inc"
+};
+
+// Copy the log table to shared memory (call from every thread, then __syncthreads()).
+__device__ __forceinline__ void load_log_table(LogEntry* s_log) {
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) s_log[i] = g_log_table[i];
+}
 
 // ----------------------------------------------------------------------------- Philox
 struct Stream {
@@ -202,16 +214,18 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
 // are counted straight into the caller's accumulators (cost = draws + fine steps,
 // paths.hpp:22-23; the fine steps are added by the caller when the sample ends).
 __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
-                                             const EdgeRec* __restrict__ edges, unsigned long long& draws,
-                                             unsigned long long& jumps) {
+                                             const EdgeRec* __restrict__ edges, const LogEntry* s_log,
+                                             unsigned long long& draws, unsigned long long& jumps) {
     stream_reserve2(w.st);  // the event's only Philox call site
     bool step_done = true;
     if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
         const double u = stream_pop(w.st);
         ++draws;
-        const double e = -log1p(-u);  // the event's only transcendental
+        // E = -log1p(-u), the event's only transcendental.  u = k 2^-53, so 1 - u is exact in
+        // fp64 and log(1 - u) is the same real number as log1p(-u) (fastmath.cuh: <= 1 ulp).
+        const double e = -fast_log(__dsub_rn(1.0, u), s_log, c_log_poly);
         if (e < __dmul_rn(w.cur.rate, w.remaining)) {  // == (u < q), see above
-            w.remaining = __dsub_rn(w.remaining, __ddiv_rn(e, w.cur.rate));  // paths.cpp:54
+            w.remaining = __dsub_rn(w.remaining, fast_div(e, w.cur.rate));  // paths.cpp:54
             ++jumps;
             const double v = stream_pop(w.st);
             uint32_t target, sgn;
