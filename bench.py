@@ -6,10 +6,11 @@
 Workload (BASELINE.json configs[1]): 2-D 5-point Laplacian on a 1024x1024 grid
 (n = 1,048,576, 5.2M nnz, fp64), t = 0.5, v uniform [0,1) from the reference's Philox stream,
 every component estimated to eps = 1e-3 by the reference's MLMC driver (Algorithm 1, one
-decision sequence per component, row seed 1000 + row).  A STEP is one complete driver solve
-of a batch of R components; batches walk a seeded permutation of all 2^20 rows, so steps
-cover C2 without repeating.  Each rank solves its own R-row batch (weak scaling: rows shard
-across ranks with no data-path collective; only the timings are reduced).
+decision sequence per component, row seed 1000 + row).  A STEP is the whole C2 job: every one of
+the 2^20 components solved to eps; with N ranks the components are dealt round-robin over a
+fixed permutation (strong scaling, no data-path collective -- components are independent MLMC
+problems; only timings are reduced).  `--rows-per-step R` instead gives every rank R
+components per step (weak scaling).
 
 Timed region (`value`): tables already resident in HBM; K steps bracketed by barrier +
 torch.cuda.synchronize(), CUDA events recorded on the library's own stream; max over ranks.
@@ -67,14 +68,30 @@ def dist_env():
 _PERM = {}
 
 
-def batch_rows(n, step, rank, world, r):
-    """Rows of (step, rank): consecutive slices of a fixed permutation of all rows."""
+def perm_rows(n):
     if n not in _PERM:
-        _PERM[n] = np.random.default_rng(20190429).permutation(n)
-    perm = _PERM[n]
+        _PERM[n] = np.random.default_rng(20190429).permutation(n).astype(np.int64)
+    return _PERM[n]
+
+
+def batch_rows(n, step, rank, world, r):
+    """Rows rank `rank` solves in `step`.  r == 0: the whole job -- every component, dealt
+    round-robin over a fixed permutation to the ranks (strong scaling).  r > 0: r components
+    per rank per step, consecutive slices of the permutation (weak scaling)."""
+    perm = perm_rows(n)
+    if r == 0:
+        return np.sort(perm[rank::world])
     k = (step * world + rank) * r
     idx = (np.arange(k, k + r) % n)
-    return np.sort(perm[idx]).astype(np.int64)
+    return np.sort(perm[idx])
+
+
+def sample_rows(n, step, r):
+    """Unsorted rows for the bounded CPU sample (a random subset of the step's batch)."""
+    perm = perm_rows(n)
+    if r == 0:
+        return np.roll(perm, -step * 1024)
+    return perm[(np.arange(step * r, step * r + r) % n)]
 
 
 class Clocks:
@@ -170,11 +187,11 @@ def run_reference(args, cfg, rank, world, r):
     ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
     per_step = max(1.0, args.ref_seconds / max(1, args.steps))
     for w in range(args.warmup):
-        reference_rows(ref, cfg, batch_rows(cfg.a.n, w, 0, 1, r), min(per_step, 2.0), threads, 4)
+        reference_rows(ref, cfg, sample_rows(cfg.a.n, w, r), min(per_step, 2.0), threads, 4)
     tj = ts = tr = 0
     tt = 0.0
     for s in range(args.steps):
-        j, smp, done, dt = reference_rows(ref, cfg, batch_rows(cfg.a.n, args.warmup + s, 0, 1, r), per_step, threads, r)
+        j, smp, done, dt = reference_rows(ref, cfg, sample_rows(cfg.a.n, args.warmup + s, r), per_step, threads, 1 << 30)
         tj += j
         ts += smp
         tr += done
@@ -183,7 +200,8 @@ def run_reference(args, cfg, rank, world, r):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "scaling": "strong" if r == 0 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
         "config": {"workload": cfg.description, "sample": f"{tr} components (as-shipped mlmc_driver per row)",
                    "parallelism": f"OpenMP {threads} threads, rank 0 only"},
         "rows_per_s": tr / tt, "samples_per_s": ts / tt,
@@ -202,7 +220,7 @@ def main():
     from paper_1904_12754_b200 import configs
 
     cfg = configs.make_config(args.config)
-    r = args.rows_per_step or (1 << 16)
+    r = args.rows_per_step  # 0: the whole C2 job per step
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world, r)
 
@@ -304,8 +322,9 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         jumps_e = 0
         h2d = d2h = 0
+        e2e_steps = min(args.steps, 3)  # bounded: each e2e step is a full solve plus the table build
         e0.record()
-        for s in range(args.steps):
+        for s in range(e2e_steps):
             with P.Context(cfg.a, cfg.u, device=local) as c2:
                 rows = batches[args.warmup + s]
                 P.mlmc_driver_rows(c2, cfg.beta, rows, seeds[args.warmup + s], opts, want_levels=False)
@@ -318,8 +337,8 @@ def main():
         barrier()
         ms_e = max_over_ranks(e0.elapsed_time(e1))
         e2e = {"value": sum_over_ranks(jumps_e) / (ms_e * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
-               "ms_per_step": ms_e / args.steps,
+               "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(d2h / e2e_steps),
+               "ms_per_step": ms_e / e2e_steps, "steps": e2e_steps,
                "includes": "table build from host CSR+u (H2D), driver solve, per-round H2D/D2H, results to host"}
 
     cpu = None
@@ -330,10 +349,10 @@ def main():
             if have_reference():
                 threads = os.cpu_count() or 1
                 ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
-                j, smp, done, dt = reference_rows(ref, cfg, batch_rows(cfg.a.n, args.warmup, 0, 1, r),
-                                                  args.ref_seconds, threads, r)
+                j, smp, done, dt = reference_rows(ref, cfg, sample_rows(cfg.a.n, args.warmup, r),
+                                                  args.ref_seconds, threads, 1 << 30)
                 cpu = {"value": j / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-                       "sample": f"{done} C2 components of the first timed batch through the as-shipped reference "
+                       "sample": f"{done} randomly chosen C2 components through the as-shipped reference "
                                  f"mlmc_driver (OpenMP, {dt:.1f} s)", "rows_per_s": done / dt}
         except Exception as exc:  # baseline failure must not hide the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
@@ -341,11 +360,13 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if r == 0 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2 (BASELINE configs[1]): {cfg.description}; one step = full MLMC driver "
-                                   f"solve of {r} components per rank",
-                       "rows_per_rank_per_step": r, "epsilon": cfg.epsilon, "t": cfg.beta,
+            "config": {"workload": f"C2 (BASELINE configs[1]): {cfg.description}; one step = "
+                                   + (f"the whole job (all {cfg.a.n} components) split over the ranks" if r == 0 else
+                                      f"MLMC driver solve of {r} components per rank"),
+                       "components_per_step": int(rows_done / args.steps), "epsilon": cfg.epsilon, "t": cfg.beta,
                        "l2": "flushed (256 MB write) before every step; C2 tables (~100 MB) are L2-sized",
                        "parallelism": f"rows sharded over {world} rank(s), no data-path collective"},
             "rows_per_s": rows_done / (ms * 1e-3), "samples_per_s": samples / (ms * 1e-3),

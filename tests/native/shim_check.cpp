@@ -1,0 +1,123 @@
+// The C++ shim (include/expmc_b200.hpp) exercised the way the reference's own doctest suite
+// exercises expmc::run_level / mlmc_driver (test_mlmc.cpp): same call shapes, same exception
+// types.  `shim_check host` runs the host-only checks (no GPU); `shim_check gpu` adds the GPU
+// cases.  Exit code 0 = all checks passed; failures are printed.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "expmc_b200.hpp"
+
+using namespace expmc::b200;
+
+static int failures = 0;
+#define CHECK(c)                                                          \
+    do {                                                                  \
+        if (!(c)) {                                                       \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);      \
+            ++failures;                                                   \
+        }                                                                 \
+    } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static CsrView dense(int64_t n, const std::vector<double>& d) {
+    CsrView a;
+    a.n = n;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t j = 0; j < n; ++j)
+            if (d[i * n + j] != 0.0) {
+                a.col.push_back(j);
+                a.val.push_back(d[i * n + j]);
+            }
+        a.row_ptr.push_back(static_cast<int64_t>(a.col.size()));
+    }
+    return a;
+}
+
+static void host_checks() {
+    // test_mlmc.cpp:17-23
+    CHECK(initial_level(0.25, 4.0) == 1);
+    CHECK(initial_level(1.0, 7.0) == 4);
+    CHECK(initial_level(1.0, 0.25) == 0);
+    CHECK(initial_level(1.0, 0.0) == 0);
+    CHECK(initial_level(1.0, -3.0) == 0);
+    // test_mlmc.cpp:25-34
+    CHECK(optimal_allocation({1.0}, {1.0}, 0.1) == std::vector<std::uint64_t>{200});
+    const auto m = optimal_allocation({1.0, 0.25}, {1.0, 4.0}, 0.1);
+    CHECK(std::abs(static_cast<double>(m[0]) / static_cast<double>(m[1]) - 4.0) < 1e-12);
+    // test_mlmc.cpp:79-88
+    CHECK(bias_estimate({0.0, 0.0}) == 0.0);
+    CHECK(throws<std::invalid_argument>([] { bias_estimate({1.0}); }));
+    CHECK(throws<std::invalid_argument>([] { initial_level(0.0, 1.0); }));
+    CHECK(throws<std::invalid_argument>([] { optimal_allocation({1.0}, {0.0}, 0.1); }));
+}
+
+static void gpu_checks() {
+    // test_mlmc.cpp:94-108: diagonal A gives exactly zero coupled differences
+    {
+        Context ctx(dense(2, {1.5, 0.0, 0.0, 0.5}), {1.0, 2.0});
+        MlmcProblem p{&ctx, 0, 1.0};
+        const LevelStats s = run_level(p, 3, false, 0, 500, 9);
+        CHECK(s.sum == 0.0 && s.sum_sq == 0.0 && s.variance() == 0.0 && s.samples == 500);
+    }
+    // test_mlmc.cpp:165-182: K2 hits e within eps for seeds 0..9
+    {
+        Context ctx(dense(2, {0.0, 1.0, 1.0, 0.0}), {1.0, 1.0});
+        MlmcProblem p{&ctx, 0, 1.0};
+        for (std::uint64_t seed = 0; seed < 10; ++seed) {
+            MlmcOptions o;
+            o.epsilon = 1e-3;
+            o.seed = seed;
+            const MlmcResult r = mlmc_driver(p, o);
+            CHECK(r.converged);
+            CHECK(std::abs(r.estimate - std::exp(1.0)) <= 1e-3);
+        }
+        // the batched form takes the same decision sequence
+        MlmcOptions o;
+        const auto rows = mlmc_driver_rows(ctx, 1.0, {0, 1}, {3, 3}, o);
+        o.seed = 3;
+        const MlmcResult one = mlmc_driver(p, o);
+        CHECK(rows[0].estimate == one.estimate && rows[0].total_cost == one.total_cost);
+        // errors: the reference's exception types
+        CHECK(throws<std::out_of_range>([&] { run_level(MlmcProblem{&ctx, 2, 1.0}, 1, false, 0, 10, 1); }));
+        CHECK(throws<std::invalid_argument>([&] { run_level(MlmcProblem{&ctx, 0, 1.0}, 63, false, 0, 10, 1); }));
+        CHECK(throws<std::invalid_argument>([&] { run_level(MlmcProblem{&ctx, 0, -1.0}, 1, false, 0, 10, 1); }));
+        CHECK(throws<std::invalid_argument>([&] {
+            MlmcOptions bad;
+            bad.epsilon = 0.0;
+            mlmc_driver(p, bad);
+        }));
+    }
+    // test_mlmc.cpp:145-163: diagonal driver converges at warm-up
+    {
+        Context ctx(dense(2, {0.75, 0.0, 0.0, -0.25}), {3.0, 1.0});
+        MlmcOptions o;
+        o.epsilon = 1e-6;
+        o.seed = 5;
+        const MlmcResult r = mlmc_driver(MlmcProblem{&ctx, 0, 2.0}, o);
+        CHECK(r.converged && r.statistical_error == 0.0 && r.bias_estimate == 0.0);
+        CHECK(std::abs(r.estimate - 3.0 * std::exp(1.5)) <= 1e-13 * r.estimate);
+        for (const LevelStats& l : r.levels) CHECK(l.samples == 1000);
+    }
+    CHECK(throws<std::invalid_argument>([] { Context bad(dense(2, {0.0, NAN, 0.0, 0.0}), {1.0, 1.0}); }));
+}
+
+int main(int argc, char** argv) {
+    host_checks();
+    if (argc > 1 && std::strcmp(argv[1], "gpu") == 0) gpu_checks();
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "ok", failures);
+    return failures ? 1 : 0;
+}
