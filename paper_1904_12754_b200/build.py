@@ -19,7 +19,7 @@ HEADERS = ["internal.hpp", "walker.cuh", "fastmath.cuh", "log_table.inc"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-fopenmp", "-Xptxas", "-v", "-lgomp",
          "--expt-relaxed-constexpr"]
 
 

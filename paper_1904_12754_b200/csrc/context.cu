@@ -140,26 +140,40 @@ void set_error(const std::string& m) { g_err = m; }
 void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
                      expmc_level_stats* out) {
     bind(c);
-    std::vector<int64_t> slot;  // request index of each item
-    slot.reserve(static_cast<size_t>(nreq));
+    // validate (first failing request wins, as a sequential loop would report it)
+    int64_t bad = nreq;
+#pragma omp parallel for schedule(static) reduction(min : bad)
     for (int64_t i = 0; i < nreq; ++i) {
-        validate_req(c, req[i], beta);
         out[i] = expmc_level_stats{0.0, 0.0, 0, 0, 0};
-        if (req[i].count > 0) slot.push_back(i);
+        try {
+            validate_req(c, req[i], beta);
+        } catch (const Status&) {
+            bad = std::min(bad, i);
+        }
     }
+    if (bad < nreq) validate_req(c, req[bad], beta);  // rethrows with the right code
+    std::vector<int64_t> slot;  // request index of each item (count > 0)
+    slot.reserve(static_cast<size_t>(nreq));
+    for (int64_t i = 0; i < nreq; ++i)
+        if (req[i].count > 0) slot.push_back(i);
     const size_t nitems = slot.size();
     if (nitems == 0) return;
     c->ctr.rounds += 1;
     need(nitems < (size_t{1} << 31), EXPMC_EINVAL, "too many run_level requests in one batch");
     ensure_items(c, nitems);
-    uint64_t total = 0;
+#pragma omp parallel for schedule(static)
     for (size_t k = 0; k < nitems; ++k) {
         const expmc_level_req& r = req[slot[k]];
         c->h_items[k] = make_item(r, beta, lane);
-        c->h_chunk0[k] = total;
         const uint64_t first_chunk = r.first_index / kChunk;
         const uint64_t last_chunk = (r.first_index + r.count - 1) / kChunk;  // parallel.hpp:36-38
-        total += last_chunk - first_chunk + 1;
+        c->h_chunk0[k] = last_chunk - first_chunk + 1;
+    }
+    uint64_t total = 0;
+    for (size_t k = 0; k < nitems; ++k) {  // exclusive prefix of the chunk counts
+        const uint64_t n = c->h_chunk0[k];
+        c->h_chunk0[k] = total;
+        total += n;
     }
     c->h_chunk0[nitems] = total;
     cuda_check(cudaMemcpyAsync(c->d_items, c->h_items, nitems * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
@@ -213,6 +227,8 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         cuda_check(cudaEventElapsedTime(&ms, c->ev[2 * k], c->ev[2 * k + 1]), "event time");
         c->ctr.sampler_ms += ms;
     }
+    uint64_t samples = 0, jumps = 0, steps = 0;
+#pragma omp parallel for schedule(static) reduction(+ : samples, jumps, steps)
     for (size_t k = 0; k < nitems; ++k) {
         const expmc_level_req& r = req[slot[k]];
         expmc_level_stats& o = out[slot[k]];
@@ -221,10 +237,13 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         o.samples = r.count;
         o.cost = c->h_totals[k].cost;
         o.jumps = c->h_totals[k].jumps;
-        c->ctr.samples += r.count;
-        c->ctr.jumps += o.jumps;
-        c->ctr.fine_steps += r.count << r.level;
+        samples += r.count;
+        jumps += o.jumps;
+        steps += r.count << r.level;
     }
+    c->ctr.samples += samples;
+    c->ctr.jumps += jumps;
+    c->ctr.fine_steps += steps;
 }
 
 }  // namespace expmc_b200

@@ -154,6 +154,7 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
     DriverConfig cfg{opt.epsilon, opt.epsilon / std::sqrt(2.0), opt.warmup, opt.max_iterations};
 
     std::vector<RowState> st(static_cast<size_t>(nrows));
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < nrows; ++r) {
         RowState& s = st[static_cast<size_t>(r)];
         s.entry = rows[r];
@@ -165,61 +166,89 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
         for (int i = 0; i <= s.top - l0; ++i) s.pending.emplace_back(i, opt.warmup);
     }
 
+    // Per round: (1) every active row's pending extensions become one contiguous slice of the
+    // batch, (2) one batched GPU pass, (3) each row applies its slice (extend(), mlmc.cpp:188-199)
+    // and advances its state machine.  Rows are independent, so (1) and (3) run in parallel.
     std::vector<expmc_level_req> req;
     std::vector<expmc_level_stats> res;
-    std::vector<std::pair<int64_t, int>> owner;
-    std::vector<double> v, c, means;
-    std::vector<uint64_t> want;
-    std::vector<int64_t> active;
-    for (int64_t r = 0; r < nrows; ++r) active.push_back(r);
+    std::vector<size_t> off;
+    std::vector<unsigned char> keep;
+    std::vector<int64_t> active(static_cast<size_t>(nrows));
+    for (int64_t r = 0; r < nrows; ++r) active[static_cast<size_t>(r)] = r;
     const bool trace = std::getenv("EXPMC_TRACE") != nullptr;  // per-round timeline on stderr
     using clk = std::chrono::steady_clock;
     int round = 0;
     while (!active.empty()) {
         const auto t0 = clk::now();
-        req.clear();
-        owner.clear();
-        for (int64_t r : active) {
-            RowState& s = st[static_cast<size_t>(r)];
+        const size_t na = active.size();
+        off.assign(na + 1, 0);
+        for (size_t i = 0; i < na; ++i) off[i + 1] = off[i] + st[static_cast<size_t>(active[i])].pending.size();
+        req.resize(off[na]);
+        res.resize(off[na]);
+#pragma omp parallel for schedule(static)
+        for (size_t i = 0; i < na; ++i) {
+            const RowState& s = st[static_cast<size_t>(active[i])];
+            size_t k = off[i];
             for (const auto& p : s.pending) {
                 const Level& l = s.lv[static_cast<size_t>(p.first)];
                 const int level = s.l0 + p.first;
-                req.push_back(expmc_level_req{s.entry, s.seed, l.samples, p.second, level, level == s.l0 ? 1 : 0});
-                owner.emplace_back(r, p.first);
+                req[k++] = expmc_level_req{s.entry, s.seed, l.samples, p.second, level, level == s.l0 ? 1 : 0};
             }
         }
-        res.resize(req.size());
         const auto t1 = clk::now();
         run_level_batch(ctx, beta, EXPMC_LANE_ENTRY, req.data(), static_cast<int64_t>(req.size()), res.data());
         const auto t2 = clk::now();
-        for (size_t k = 0; k < req.size(); ++k) {  // extend(): mlmc.cpp:188-199
-            Level& l = st[static_cast<size_t>(owner[k].first)].lv[static_cast<size_t>(owner[k].second)];
-            l.sum += res[k].sum;
-            l.sum_sq += res[k].sum_sq;
-            l.samples += res[k].samples;
-            l.cost += res[k].cost;
-            l.jumps += res[k].jumps;
+        keep.assign(na, 0);
+        int err_code = 0;
+        std::string err_msg;
+#pragma omp parallel
+        {
+            std::vector<double> v, c, means;
+            std::vector<uint64_t> want;
+#pragma omp for schedule(dynamic, 256)
+            for (size_t i = 0; i < na; ++i) {
+                RowState& s = st[static_cast<size_t>(active[i])];
+                for (size_t j = 0; j < s.pending.size(); ++j) {  // extend(): mlmc.cpp:188-199
+                    const expmc_level_stats& d = res[off[i] + j];
+                    Level& l = s.lv[static_cast<size_t>(s.pending[j].first)];
+                    l.sum += d.sum;
+                    l.sum_sq += d.sum_sq;
+                    l.samples += d.samples;
+                    l.cost += d.cost;
+                    l.jumps += d.jumps;
+                }
+                s.pending.clear();
+                try {
+                    advance(s, cfg, v, c, want, means);
+                } catch (const Status& e) {
+#pragma omp critical(expmc_driver_error)
+                    if (err_code == 0) {
+                        err_code = e.code;
+                        err_msg = e.what();
+                    }
+                    s.phase = Phase::done;
+                }
+                keep[i] = s.phase != Phase::done;
+            }
         }
-        std::vector<int64_t> next;
-        for (int64_t r : active) {
-            RowState& s = st[static_cast<size_t>(r)];
-            s.pending.clear();
-            advance(s, cfg, v, c, want, means);
-            if (s.phase != Phase::done) next.push_back(r);
-        }
+        if (err_code) throw Status(err_code, err_msg);
+        size_t m = 0;
+        for (size_t i = 0; i < na; ++i)
+            if (keep[i]) active[m++] = active[i];
         if (trace) {
             uint64_t smp = 0;
             for (const auto& q : req) smp += q.count;
             const auto t3 = clk::now();
             auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
             std::fprintf(stderr, "[expmc] round %d rows %zu reqs %zu samples %llu | build %.2f ms gpu %.2f ms advance %.2f ms\n",
-                         round, active.size(), req.size(), static_cast<unsigned long long>(smp), ms(t0, t1), ms(t1, t2),
+                         round, na, req.size(), static_cast<unsigned long long>(smp), ms(t0, t1), ms(t1, t2),
                          ms(t2, t3));
         }
         ++round;
-        active.swap(next);
+        active.resize(m);
     }
 
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < nrows; ++r) {  // mlmc.cpp:249-259
         const RowState& s = st[static_cast<size_t>(r)];
         expmc_result& o = out[r];
