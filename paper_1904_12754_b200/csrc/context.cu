@@ -25,7 +25,9 @@ struct expmc_ctx {
     uint64_t nedges = 0;
     double d_max = 0.0, d_bar = 0.0;
     RowRec* rows = nullptr;
-    EdgeRec* edges = nullptr;
+    double* cdf = nullptr;     // per edge, read only for non-uniform rows
+    uint32_t* tgt = nullptr;   // per edge: target | sign bit
+    EdgeTables edges() const { return EdgeTables{cdf, tgt}; }
 
     // batch buffers (grown on demand)
     DevItem* d_items = nullptr;
@@ -195,7 +197,7 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         cuda_check(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), c->stream), "memset counter");
         SamplerArgs a;
         a.rows = c->rows;
-        a.edges = c->edges;
+        a.edges = c->edges();
         a.items = c->d_items;
         a.chunk0 = c->d_chunk0;
         a.nitems = static_cast<uint32_t>(nitems);
@@ -331,8 +333,9 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
                     c->nedges = last[0] + last[1];
                     need(c->nedges < (uint64_t{1} << 32), EXPMC_EINVAL, "more than 2^32 chain edges");
                     dev_alloc(&c->rows, n);
-                    dev_alloc(&c->edges, c->nedges);
-                    launch_fill_tables(n, d_rp, d_col, d_val, d_u, d_begin, c->rows, c->edges, c->stream);
+                    dev_alloc(&c->cdf, c->nedges);
+                    dev_alloc(&c->tgt, c->nedges);
+                    launch_fill_tables(n, d_rp, d_col, d_val, d_u, d_begin, c->rows, c->cdf, c->tgt, c->stream);
                     d_stats(c->rows, n, d_st, tmp, tb, c->stream);
                     double st[2];
                     cuda_check(cudaMemcpyAsync(st, d_st, sizeof st, cudaMemcpyDeviceToHost, c->stream), "D2H");
@@ -360,7 +363,8 @@ void expmc_ctx_destroy(expmc_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     cudaFree(c->rows);
-    cudaFree(c->edges);
+    cudaFree(c->cdf);
+    cudaFree(c->tgt);
     cudaFree(c->d_items);
     cudaFree(c->d_chunk0);
     cudaFree(c->d_totals);
@@ -384,7 +388,7 @@ int expmc_ctx_get_info(const expmc_ctx* c, expmc_ctx_info* out) {
         out->d_bar = c->d_bar;
         out->device = c->device;
         out->num_sms = c->num_sms;
-        out->table_bytes = static_cast<uint64_t>(c->n) * sizeof(RowRec) + c->nedges * sizeof(EdgeRec);
+        out->table_bytes = static_cast<uint64_t>(c->n) * sizeof(RowRec) + c->nedges * (sizeof(double) + sizeof(uint32_t));
     });
 }
 
@@ -418,7 +422,7 @@ int expmc_ctx_export_tables(const expmc_ctx* c, double* d, double* rate, int64_t
         dev_alloc(&dd, n); dev_alloc(&dr, n); dev_alloc(&drp, n + 1);
         dev_alloc(&dc, m); dev_alloc(&dt, m); dev_alloc(&ds, m);
         launch_export(n, c->rows, dd, dr, drp, c->stream);
-        launch_export_edges(m, c->edges, dc, dt, ds, c->stream);
+        launch_export_edges(m, c->edges(), dc, dt, ds, c->stream);
         cudaError_t e = cudaStreamSynchronize(c->stream);
         if (e == cudaSuccess && d) e = cudaMemcpy(d, dd, n * 8, cudaMemcpyDeviceToHost);
         if (e == cudaSuccess && rate) e = cudaMemcpy(rate, dr, n * 8, cudaMemcpyDeviceToHost);
@@ -506,7 +510,7 @@ int expmc_sample_debug(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, c
         }
         cuda_check(cudaMemcpyAsync(c->d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
                    "H2D");
-        launch_debug(c->rows, c->edges, c->d_items, static_cast<uint32_t>(nreq), c->d_dbg, c->stream);
+        launch_debug(c->rows, c->edges(), c->d_items, static_cast<uint32_t>(nreq), c->d_dbg, c->stream);
         c->ctr.kernel_launches += 1;
         std::vector<SampleOut> o(static_cast<size_t>(nreq));
         cuda_check(cudaMemcpyAsync(o.data(), c->d_dbg, nreq * sizeof(SampleOut), cudaMemcpyDeviceToHost, c->stream),

@@ -20,17 +20,27 @@ struct alignas(32) RowRec {
     double rate;     // sum_{j != i} |a_ij|               (chain.cpp:39-46)
     double u;        // u_i, the terminal factor           (paths.cpp:112,138)
     uint32_t begin;  // first edge of the row
-    uint32_t deg;    // number of chain edges of the row
+    uint32_t deg;    // bits 0-30: number of chain edges; bit 31: kUniformRow
 };
 static_assert(sizeof(RowRec) == 32, "row record must be one 32-B sector");
 
-// Edge record, 16 B: the reference's jump_cdf / jump_target / sign triple (chain.hpp:33-35).
-struct alignas(16) EdgeRec {
-    double cdf;       // cumulative |a_ij| / rate_i, last entry of a row exactly 1
-    uint32_t target;  // column j
-    uint32_t sign;    // 1 where a_ij < 0
+// Edges, structure of arrays (chain.hpp:33-35):
+//   tgt[e] = column j | kSignBit where a_ij < 0          (4 B, read on every jump)
+//   cdf[e] = cumulative |a_ij| / rate_i, last entry of a row exactly 1   (8 B, read only for
+//            rows without kUniformRow)
+// kUniformRow marks rows whose stored CDF is exactly fl((j+1)/deg) for every j -- every row
+// whose off-diagonal magnitudes are equal (Laplacians, adjacency matrices).  Their
+// upper_bound(cdf, v) is computed exactly from v's 53-bit integer (walker.cuh), so a jump
+// reads one 4-B target word instead of the row's CDF.
+constexpr uint32_t kUniformRow = 0x80000000u;
+constexpr uint32_t kDegMask = 0x7FFFFFFFu;
+constexpr uint32_t kSignBit = 0x80000000u;
+constexpr uint32_t kTargetMask = 0x7FFFFFFFu;
+
+struct EdgeTables {
+    const double* cdf;
+    const uint32_t* tgt;
 };
-static_assert(sizeof(EdgeRec) == 16, "edge record is 16 B");
 
 // One device work item = one run_level request with count > 0.
 struct alignas(16) DevItem {
@@ -74,7 +84,7 @@ void cuda_check(cudaError_t e, const char* what);
 // ----------------------------------------------------------------------------- launchers
 struct SamplerArgs {
     const RowRec* rows;
-    const EdgeRec* edges;
+    EdgeTables edges;
     const DevItem* items;
     const uint64_t* chunk0;  // nitems + 1, exclusive prefix of chunk counts
     uint32_t nitems;
@@ -86,7 +96,7 @@ struct SamplerArgs {
 void launch_sampler(const SamplerArgs& a, int grid, cudaStream_t s);
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
                     const Partial* partials, Partial* totals, cudaStream_t s);
-void launch_debug(const RowRec* rows, const EdgeRec* edges, const DevItem* items, uint32_t n,
+void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n,
                   SampleOut* out, cudaStream_t s);
 int sampler_blocks_per_sm();
 int sampler_threads();
@@ -97,12 +107,12 @@ float bench_gather(uint64_t bytes, int loads_per_thread, int reps, int num_sms, 
 void launch_count_edges(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
                         uint64_t* deg, unsigned int* err, cudaStream_t s);
 void launch_fill_tables(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
-                        const double* u, const uint64_t* begin, RowRec* rows, EdgeRec* edges,
+                        const double* u, const uint64_t* begin, RowRec* rows, double* cdf, uint32_t* tgt,
                         cudaStream_t s);
 void launch_set_vector(int64_t n, const double* u, RowRec* rows, cudaStream_t s);
 void launch_export(int64_t n, const RowRec* rows, double* d, double* rate, int64_t* row_ptr,
                    cudaStream_t s);
-void launch_export_edges(uint64_t e, const EdgeRec* edges, double* cdf, int64_t* target,
+void launch_export_edges(uint64_t e, EdgeTables edges, double* cdf, int64_t* target,
                          uint8_t* sign, cudaStream_t s);
 // scans / reductions (CUB): exclusive sum of n u64, max / sum of RowRec::d
 size_t scan_temp_bytes(int64_t n);

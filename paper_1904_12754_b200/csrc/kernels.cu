@@ -144,7 +144,7 @@ __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, 
     totals[i] = t;
 }
 
-__global__ void k_debug(const RowRec* __restrict__ rows, const EdgeRec* __restrict__ edges,
+__global__ void k_debug(const RowRec* __restrict__ rows, EdgeTables edges,
                         const DevItem* __restrict__ items, uint32_t n, SampleOut* __restrict__ out) {
     __shared__ LogEntry s_log[128];
     load_log_table(s_log);
@@ -195,7 +195,7 @@ __global__ void k_count_edges(int64_t n, const int64_t* __restrict__ row_ptr, co
 __global__ void k_fill_tables(int64_t n, const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col,
                               const double* __restrict__ val, const double* __restrict__ u,
                               const uint64_t* __restrict__ begin, RowRec* __restrict__ rows,
-                              EdgeRec* __restrict__ edges) {
+                              double* __restrict__ cdf, uint32_t* __restrict__ tgt) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t e0 = begin[i];
@@ -210,22 +210,26 @@ __global__ void k_fill_tables(int64_t n, const int64_t* __restrict__ row_ptr, co
         }
         if (v == 0.0) continue;
         rate = __dadd_rn(rate, fabs(v));
-        EdgeRec r;
-        r.cdf = rate;
-        r.target = static_cast<uint32_t>(c);
-        r.sign = v < 0.0 ? 1u : 0u;
-        edges[e++] = r;
+        cdf[e] = rate;
+        tgt[e] = static_cast<uint32_t>(c) | (v < 0.0 ? kSignBit : 0u);
+        ++e;
     }
+    const uint32_t deg = static_cast<uint32_t>(e - e0);
+    bool uniform = true;  // cdf_j == fl((j+1)/deg) for all j: kUniformRow
     if (rate > 0.0) {
-        for (uint64_t k = e0; k + 1 < e; ++k) edges[k].cdf = __ddiv_rn(edges[k].cdf, rate);
-        edges[e - 1].cdf = 1.0;
+        for (uint64_t k = e0; k + 1 < e; ++k) {
+            const double c = __ddiv_rn(cdf[k], rate);
+            cdf[k] = c;
+            uniform = uniform && c == __ddiv_rn(static_cast<double>(k - e0 + 1), static_cast<double>(deg));
+        }
+        cdf[e - 1] = 1.0;
     }
     RowRec r;
     r.d = __dadd_rn(diag, rate);
     r.rate = rate;
     r.u = u[i];
     r.begin = static_cast<uint32_t>(e0);
-    r.deg = static_cast<uint32_t>(e - e0);
+    r.deg = deg | (uniform && deg > 0 ? kUniformRow : 0u);
     rows[i] = r;
 }
 
@@ -243,14 +247,13 @@ __global__ void k_export_rows(int64_t n, const RowRec* __restrict__ rows, double
     if (row_ptr) row_ptr[i] = r.begin;
 }
 
-__global__ void k_export_edges(uint64_t m, const EdgeRec* __restrict__ edges, double* cdf, int64_t* target,
-                               uint8_t* sign) {
+__global__ void k_export_edges(uint64_t m, EdgeTables edges, double* cdf, int64_t* target, uint8_t* sign) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= m) return;
-    const EdgeRec r = edges[i];
-    if (cdf) cdf[i] = r.cdf;
-    if (target) target[i] = r.target;
-    if (sign) sign[i] = static_cast<uint8_t>(r.sign);
+    const uint32_t t = edges.tgt[i];
+    if (cdf) cdf[i] = edges.cdf[i];
+    if (target) target[i] = t & kTargetMask;
+    if (sign) sign[i] = (t & kSignBit) ? 1 : 0;
 }
 
 // d_max / d_sum: fixed two-level tree (block partials, then one block) -> deterministic.
@@ -354,7 +357,7 @@ void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, u
     cuda_check(cudaGetLastError(), "k_combine launch");
 }
 
-void launch_debug(const RowRec* rows, const EdgeRec* edges, const DevItem* items, uint32_t n, SampleOut* out,
+void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n, SampleOut* out,
                   cudaStream_t s) {
     k_debug<<<grid_for(n, 128), 128, 0, s>>>(rows, edges, items, n, out);
     cuda_check(cudaGetLastError(), "k_debug launch");
@@ -368,9 +371,9 @@ void launch_count_edges(int64_t n, const int64_t* row_ptr, const int64_t* col, c
 }
 
 void launch_fill_tables(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val, const double* u,
-                        const uint64_t* begin, RowRec* rows, EdgeRec* edges, cudaStream_t s) {
+                        const uint64_t* begin, RowRec* rows, double* cdf, uint32_t* tgt, cudaStream_t s) {
     if (n == 0) return;
-    k_fill_tables<<<grid_for(n, 128), 128, 0, s>>>(n, row_ptr, col, val, u, begin, rows, edges);
+    k_fill_tables<<<grid_for(n, 128), 128, 0, s>>>(n, row_ptr, col, val, u, begin, rows, cdf, tgt);
     cuda_check(cudaGetLastError(), "k_fill_tables launch");
 }
 
@@ -386,7 +389,7 @@ void launch_export(int64_t n, const RowRec* rows, double* d, double* rate, int64
     cuda_check(cudaGetLastError(), "k_export_rows launch");
 }
 
-void launch_export_edges(uint64_t m, const EdgeRec* edges, double* cdf, int64_t* target, uint8_t* sign,
+void launch_export_edges(uint64_t m, EdgeTables edges, double* cdf, int64_t* target, uint8_t* sign,
                          cudaStream_t s) {
     if (m == 0) return;
     k_export_edges<<<grid_for(static_cast<int64_t>(m), 256), 256, 0, s>>>(m, edges, cdf, target, sign);

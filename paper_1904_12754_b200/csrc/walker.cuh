@@ -91,14 +91,19 @@ __device__ __forceinline__ void stream_reserve2(Stream& s) {
     }
 }
 
-// next_uniform: 53 random bits -> [0,1) exactly as rng.hpp:35.
-__device__ __forceinline__ double stream_pop(Stream& s) {
+// The 53-bit integer K of the next uniform v = K 2^-53 (rng.hpp:34-35).
+__device__ __forceinline__ uint64_t stream_pop_bits(Stream& s) {
     const uint64_t bits = s.w0;
     s.w0 = s.w1;
     s.w1 = s.w2;
     --s.n;
-    return __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);
+    return bits >> 11;
 }
+
+__device__ __forceinline__ double to_uniform(uint64_t k53) { return __dmul_rn(__ull2double_rn(k53), 0x1.0p-53); }
+
+// next_uniform: 53 random bits -> [0,1) exactly as rng.hpp:35.
+__device__ __forceinline__ double stream_pop(Stream& s) { return to_uniform(stream_pop_bits(s)); }
 
 // ----------------------------------------------------------------------------- tables
 struct Row {  // u_i is not kept in registers: walker_finish reloads it for the end state
@@ -117,46 +122,51 @@ __device__ __forceinline__ Row load_row(const RowRec* __restrict__ rows, uint32_
     return r;
 }
 
-__device__ __forceinline__ double edge_cdf(const uint4& e) {
-    return __hiloint2double(static_cast<int>(e.y), static_cast<int>(e.x));
-}
-
-// Neighbour choice k = upper_bound(cdf[begin:begin+deg], v), clamped to deg-1
-// (paths.cpp:57-63).  The row's CDF is non-decreasing, so upper_bound == #{j : cdf_j <= v};
-// rows of degree <= 4 load all their edge records at once (independent loads, one round
-// trip) and count; wider rows binary-search exactly like std::upper_bound.
-__device__ __forceinline__ void pick_edge(const EdgeRec* __restrict__ edges, uint32_t begin, uint32_t deg,
-                                          double v, uint32_t& target, uint32_t& sign) {
-    const uint4* e = reinterpret_cast<const uint4*>(edges + begin);
-    if (deg <= 4u) {
-        const uint4 z = make_uint4(0u, 0x7FF00000u, 0u, 0u);  // cdf = +inf, never <= v
-        const uint4 r0 = __ldg(e);
-        const uint4 r1 = deg > 1u ? __ldg(e + 1) : z;
-        const uint4 r2 = deg > 2u ? __ldg(e + 2) : z;
-        const uint4 r3 = deg > 3u ? __ldg(e + 3) : z;
-        uint32_t c = (edge_cdf(r0) <= v) + (edge_cdf(r1) <= v) + (edge_cdf(r2) <= v) + (edge_cdf(r3) <= v);
-        c = c < deg - 1u ? c : deg - 1u;
-        const uint4 r = c == 0u ? r0 : c == 1u ? r1 : c == 2u ? r2 : r3;
-        target = r.z;
-        sign = r.w;
-        return;
+// Neighbour choice (paths.cpp:57-65): k = upper_bound(cdf[begin:begin+deg], v) clamped to
+// deg-1, then (target, sign) = tgt[begin + k].  Returns the packed target|sign word.
+//
+// Uniform rows (kUniformRow: cdf_j == fl((j+1)/deg) for all j) never read the CDF.  With
+// v = K 2^-53 and |v - (j+1)/deg| >= 2^-53 for every j, fl((j+1)/deg) <= v iff
+// (j+1)/deg <= v (the rounding error of fl is <= 2^-54), so upper_bound = floor(K deg / 2^53),
+// an exact 128-bit integer product.  Draws within 2^-53 of a boundary (probability 2 deg 2^-53)
+// take the generic path, which compares against the stored CDF exactly as std::upper_bound
+// does: the choice is the reference's in every case.  Generic rows of degree <= 4 read their
+// CDF with independent loads and count (#{j : cdf_j <= v} == upper_bound on a non-decreasing
+// array); wider rows binary-search.
+__device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53) {
+    const uint32_t deg = degf & kDegMask;
+    uint32_t k = 0;
+    bool done = false;
+    if (degf & kUniformRow) {
+        const uint64_t lo = k53 * deg;
+        const uint64_t hi = __umul64hi(k53, static_cast<uint64_t>(deg));
+        const uint64_t rem = lo & ((uint64_t{1} << 53) - 1);
+        k = static_cast<uint32_t>((hi << 11) | (lo >> 53));
+        done = rem >= deg && rem <= (uint64_t{1} << 53) - deg;
     }
-    uint32_t lo = 0, count = deg;
-    while (count > 0u) {
-        const uint32_t step = count >> 1;
-        const uint32_t it = lo + step;
-        const double c = __ldg(reinterpret_cast<const double*>(edges + begin + it));
-        if (!(v < c)) {
-            lo = it + 1u;
-            count -= step + 1u;
+    if (!done) {
+        const double v = to_uniform(k53);
+        const double* c = e.cdf + begin;
+        if (deg <= 4u) {
+            k = (__ldg(c) <= v) + (deg > 1u && __ldg(c + 1) <= v) + (deg > 2u && __ldg(c + 2) <= v) +
+                (deg > 3u && __ldg(c + 3) <= v);
         } else {
-            count = step;
+            uint32_t lo = 0, count = deg;
+            while (count > 0u) {
+                const uint32_t step = count >> 1;
+                const uint32_t it = lo + step;
+                if (!(v < __ldg(c + it))) {
+                    lo = it + 1u;
+                    count -= step + 1u;
+                } else {
+                    count = step;
+                }
+            }
+            k = lo;
         }
     }
-    const uint32_t k = lo < deg - 1u ? lo : deg - 1u;
-    const uint4 r = __ldg(e + k);
-    target = r.z;
-    sign = r.w;
+    k = k < deg - 1u ? k : deg - 1u;
+    return __ldg(e.tgt + begin + k);
 }
 
 // ----------------------------------------------------------------------------- walker
@@ -214,7 +224,7 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
 // are counted straight into the caller's accumulators (cost = draws + fine steps,
 // paths.hpp:22-23; the fine steps are added by the caller when the sample ends).
 __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
-                                             const EdgeRec* __restrict__ edges, const LogEntry* s_log,
+                                             const EdgeTables& edges, const LogEntry* s_log,
                                              unsigned long long& draws, unsigned long long& jumps) {
     stream_reserve2(w.st);  // the event's only Philox call site
     bool step_done = true;
@@ -227,12 +237,10 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
         if (e < __dmul_rn(w.cur.rate, w.remaining)) {  // == (u < q), see above
             w.remaining = __dsub_rn(w.remaining, fast_div(e, w.cur.rate));  // paths.cpp:54
             ++jumps;
-            const double v = stream_pop(w.st);
-            uint32_t target, sgn;
-            pick_edge(edges, w.cur.begin, w.cur.deg, v, target, sgn);
-            if (sgn) w.sign = -w.sign;
-            w.state = target;
-            w.cur = load_row(rows, target);
+            const uint32_t ts = pick_edge(edges, w.cur.begin, w.cur.deg, stream_pop_bits(w.st));
+            if (ts & kSignBit) w.sign = -w.sign;
+            w.state = ts & kTargetMask;
+            w.cur = load_row(rows, w.state);
             // remaining <= 0: rounding pushed past the boundary, the step ends (paths.cpp:67)
             step_done = !(w.remaining > 0.0);
         }
