@@ -32,6 +32,13 @@ extern "C" {
 #define EXPMC_ENOTIMPL 5  /* mode not built yet (forward / fem sampling)   */
 #define EXPMC_EINTERNAL 9
 
+/* Path samplers.  REFERENCE: draw-for-draw the reference's evolve_common / single / coupled
+ * (paths.cpp:44-141) -- same jump chain, same values, exact parity (default).  EVENT: one
+ * exponential clock per jump, fine-step boundaries crossed in closed form: the same path law
+ * at O(jumps) instead of O(2^level) events per path; statistical parity. */
+#define EXPMC_SAMPLER_REFERENCE 0
+#define EXPMC_SAMPLER_EVENT 1
+
 /* Sampling lanes of the reference's Philox key (mlmc.cpp:94-96). */
 #define EXPMC_LANE_ENTRY 0u
 
@@ -146,6 +153,9 @@ int expmc_ctx_set_vector(expmc_ctx* ctx, const double* u);
 int expmc_ctx_export_tables(const expmc_ctx* ctx, double* d, double* rate, int64_t* row_ptr,
                             double* jump_cdf, int64_t* jump_target, uint8_t* sign);
 int expmc_ctx_get_counters(const expmc_ctx* ctx, expmc_counters* out);
+/* Select the path sampler (EXPMC_SAMPLER_REFERENCE / EXPMC_SAMPLER_EVENT) for all later calls. */
+int expmc_ctx_set_sampler(expmc_ctx* ctx, int32_t mode);
+int expmc_ctx_get_sampler(const expmc_ctx* ctx, int32_t* mode);
 /* The context's CUDA stream (cudaStream_t as void*), for timing with events on the stream
  * the sampler kernels are launched on. */
 int expmc_ctx_get_stream(const expmc_ctx* ctx, void** stream);

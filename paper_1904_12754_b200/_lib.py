@@ -14,6 +14,7 @@ _I32, _I64, _U32, _U64, _D = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_d
 
 EXPMC_OK, EXPMC_EINVAL, EXPMC_ERANGE, EXPMC_EDOMAIN, EXPMC_ECUDA, EXPMC_ENOTIMPL, EXPMC_EINTERNAL = 0, 1, 2, 3, 4, 5, 9
 LANE_ENTRY = 0
+SAMPLER_REFERENCE, SAMPLER_EVENT = 0, 1
 
 
 class Csr(C.Structure):
@@ -68,6 +69,8 @@ SYMBOLS = [
     ("expmc_ctx_get_counters", C.c_int, [_P, C.POINTER(CountersC)]),
     ("expmc_ctx_reset_counters", C.c_int, [_P]),
     ("expmc_ctx_get_stream", C.c_int, [_P, C.POINTER(_P)]),
+    ("expmc_ctx_set_sampler", C.c_int, [_P, _I32]),
+    ("expmc_ctx_get_sampler", C.c_int, [_P, C.POINTER(_I32)]),
     ("expmc_bench_gather", C.c_int, [C.c_int, _U64, _I32, _I32, C.POINTER(_D)]),
     ("expmc_run_level", C.c_int, [_P, _I64, _D, _I32, _I32, _U64, _U64, _U64, C.POINTER(LevelStatsC)]),
     ("expmc_run_level_batch", C.c_int, [_P, _D, _U32, _I64, _P, _P]),

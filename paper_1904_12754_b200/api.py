@@ -207,7 +207,9 @@ class Context:
     """Device-resident sampling tables of A plus the bound vector u on one GPU
     (decompose + LevelSampler tables + MlmcProblem::u)."""
 
-    def __init__(self, a: SparseMatrix, u, device: int = 0):
+    SAMPLERS = {"reference": L.SAMPLER_REFERENCE, "event": L.SAMPLER_EVENT}
+
+    def __init__(self, a: SparseMatrix, u, device: int = 0, sampler: str = "reference"):
         self._h = C.c_void_p()
         u = np.ascontiguousarray(u, np.float64)
         if u.shape != (a.n,):
@@ -226,6 +228,15 @@ class Context:
         self.device = info.device
         self.num_sms = info.num_sms
         self.table_bytes = info.table_bytes
+        self.set_sampler(sampler)
+
+    def set_sampler(self, sampler: str):
+        """'reference' (draw-for-draw the reference's sampler, exact parity) or 'event'
+        (one exponential clock per jump; same law, O(jumps) per path)."""
+        if sampler not in self.SAMPLERS:
+            raise InvalidArgument(f"unknown sampler {sampler!r}")
+        _check(L.lib.expmc_ctx_set_sampler(self._h, self.SAMPLERS[sampler]))
+        self.sampler = sampler
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:

@@ -19,7 +19,10 @@ using namespace expmc_b200;
 struct expmc_ctx {
     int device = 0;
     int num_sms = 0;
-    int sampler_grid = 0;
+    int sampler_grid = 0;       // persistent grid of the active sampler
+    int sampler_grid_ref = 0;
+    int sampler_grid_ed = 0;
+    int sampler = EXPMC_SAMPLER_REFERENCE;
     cudaStream_t stream = nullptr;
     int64_t n = 0;
     uint64_t nedges = 0;
@@ -213,7 +216,7 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
             c->ev.push_back(e);
         }
         cuda_check(cudaEventRecord(c->ev[2 * nev], c->stream), "event");
-        launch_sampler(a, grid, c->stream);
+        launch_sampler(a, grid, c->sampler, c->stream);
         cuda_check(cudaEventRecord(c->ev[2 * nev + 1], c->stream), "event");
         ++nev;
         launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, c->d_partials, c->d_totals, c->stream);
@@ -286,7 +289,9 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
             bind(c);
             cuda_check(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
             cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
-            c->sampler_grid = c->num_sms * sampler_blocks_per_sm();
+            c->sampler_grid_ref = c->num_sms * sampler_blocks_per_sm(EXPMC_SAMPLER_REFERENCE);
+            c->sampler_grid_ed = c->num_sms * sampler_blocks_per_sm(EXPMC_SAMPLER_EVENT);
+            c->sampler_grid = c->sampler_grid_ref;
             c->n = n;
             if (n > 0) {
                 const int64_t nnz = A->nnz;
@@ -445,6 +450,22 @@ int expmc_ctx_get_counters(const expmc_ctx* c, expmc_counters* out) {
     });
 }
 
+int expmc_ctx_set_sampler(expmc_ctx* c, int32_t mode) {
+    return guarded([&] {
+        need(c != nullptr, EXPMC_EINVAL, "null context");
+        need(mode == EXPMC_SAMPLER_REFERENCE || mode == EXPMC_SAMPLER_EVENT, EXPMC_EINVAL, "unknown sampler mode");
+        c->sampler = mode;
+        c->sampler_grid = mode == EXPMC_SAMPLER_EVENT ? c->sampler_grid_ed : c->sampler_grid_ref;
+    });
+}
+
+int expmc_ctx_get_sampler(const expmc_ctx* c, int32_t* mode) {
+    return guarded([&] {
+        need(c && mode, EXPMC_EINVAL, "null argument");
+        *mode = c->sampler;
+    });
+}
+
 int expmc_ctx_get_stream(const expmc_ctx* c, void** stream) {
     return guarded([&] {
         need(c && stream, EXPMC_EINVAL, "null argument");
@@ -510,7 +531,7 @@ int expmc_sample_debug(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, c
         }
         cuda_check(cudaMemcpyAsync(c->d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
                    "H2D");
-        launch_debug(c->rows, c->edges(), c->d_items, static_cast<uint32_t>(nreq), c->d_dbg, c->stream);
+        launch_debug(c->rows, c->edges(), c->d_items, static_cast<uint32_t>(nreq), c->d_dbg, c->sampler, c->stream);
         c->ctr.kernel_launches += 1;
         std::vector<SampleOut> o(static_cast<size_t>(nreq));
         cuda_check(cudaMemcpyAsync(o.data(), c->d_dbg, nreq * sizeof(SampleOut), cudaMemcpyDeviceToHost, c->stream),

@@ -1,0 +1,168 @@
+// Event-driven walker: the statistically equivalent fast sampler.
+//
+// The reference redraws a fresh holding time at every fine-step boundary (paths.cpp:95-96):
+// one uniform per step even when nothing happens, 2^l of them per path.  The CTMC is
+// memoryless, so the same law follows from one exponential clock per jump: hold in state s
+// for E/rate(s), jump, repeat until the clock passes beta.  The fine-step boundaries
+// k*dt (k = 0..N, N = 2^l) that fall inside a holding interval all see state s, so their
+// Strang weights are added in closed form:
+//   single  (paths.cpp:110):      expo  = dt * sum_k w_k d(s_k),  w = 1/2 at k = 0, N, else 1
+//   coupled (paths.cpp:134-136):  coarse = dt * sum_k c_k d(s_k), c = 2 at interior even k,
+//                                                                 1 at k = 0, N, 0 at odd k
+//                                 delta  = dt * sum_k e_k d(s_k), e = +1 odd, -1 interior even,
+//                                                                 -1/2 at k = 0, N
+// (doubled integer weights below keep the per-segment sums exact).  A path now costs
+// O(jumps) instead of O(2^l) events; the random numbers differ from the reference's, so
+// parity is statistical (tests/test_gpu_ed.py).  The cost counter is the reference's model
+// for the path this walker drew -- draws = jumps + #{k in 1..N : rate(s_k) > 0} (each
+// non-absorbing step ends with one rejected draw, paths.cpp:50-53), cost = draws + N -- so the
+// driver's allocation (mlmc.cpp:216) sees the same unit costs in expectation.
+#pragma once
+
+#include "walker.cuh"
+
+namespace expmc_b200 {
+
+struct EdWalker {
+    Stream st;
+    Row cur;
+    uint32_t state;
+    int32_t sign;
+    uint32_t dconst;   // every visited state has the entry's d (=> coupled difference is 0)
+    uint64_t kcur;     // first fine-step boundary not yet assigned a state
+    double t;          // start time of the current holding interval
+    double acc_a;      // doubled-weight sum of d: expo (single) or coarse (coupled)
+    double acc_b;      // doubled-weight sum of d: delta (coupled)
+    double dfirst;
+};
+
+__device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+                                         uint64_t sample) {
+    stream_init(w.st, ic.seed, sample, ic.key3);
+    w.cur = load_row(rows, ic.entry);
+    w.state = ic.entry;
+    w.sign = 1;
+    w.dconst = 1u;
+    w.kcur = 0;
+    w.t = 0.0;
+    w.acc_a = 0.0;
+    w.acc_b = 0.0;
+    w.dfirst = w.cur.d;
+}
+
+// Boundaries [ka, kb] (ka <= kb <= N) all see the current state.
+__device__ __forceinline__ void ed_segment(EdWalker& w, const ItemConst& ic, uint64_t ka, uint64_t kb,
+                                           unsigned long long& draws) {
+    const uint64_t n = kb - ka + 1;
+    const int64_t ends = static_cast<int64_t>(ka == 0) + static_cast<int64_t>(kb == ic.nsteps);
+    if (w.cur.rate != 0.0) draws += n - (ka == 0 ? 1u : 0u);  // one rejected draw per non-absorbing step end
+    const double d = w.cur.d;
+    if (ic.base) {
+        const int64_t w2 = 2 * static_cast<int64_t>(n) - ends;
+        w.acc_a = __dadd_rn(w.acc_a, __dmul_rn(d, static_cast<double>(w2)));
+    } else {
+        const int64_t ev = static_cast<int64_t>(kb >> 1) - static_cast<int64_t>((ka + 1) >> 1) + 1;
+        const int64_t od = static_cast<int64_t>(n) - ev;
+        const int64_t c2 = 4 * ev - 2 * ends;
+        const int64_t e2 = 2 * od - 2 * ev + ends;
+        w.acc_a = __dadd_rn(w.acc_a, __dmul_rn(d, static_cast<double>(c2)));
+        w.acc_b = __dadd_rn(w.acc_b, __dmul_rn(d, static_cast<double>(e2)));
+    }
+}
+
+// One holding interval: draw its length, assign the boundaries it covers, jump (or finish).
+__device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+                                         const EdgeTables& edges, const LogEntry* s_log, unsigned long long& draws,
+                                         unsigned long long& jumps) {
+    stream_reserve2(w.st);
+    double tjump = INFINITY;
+    if (w.cur.rate != 0.0) {
+        const double e = -fast_log(__dsub_rn(1.0, stream_pop(w.st)), s_log, c_log_poly);
+        tjump = __dadd_rn(w.t, fast_div(e, w.cur.rate));
+    }
+    if (!(tjump < ic.tend)) {  // holds to the end of the interval [0, beta]
+        if (w.kcur <= ic.nsteps) ed_segment(w, ic, w.kcur, ic.nsteps, draws);
+        return true;
+    }
+    // boundaries k with k*dt < tjump: k <= ceil(tjump/dt) - 1
+    const double q = __dmul_rn(tjump, ic.inv_dt);
+    const uint64_t kq = static_cast<uint64_t>(ceil(q));
+    const uint64_t kend = kq == 0 ? 0 : kq - 1;  // kq >= 1 unless tjump == 0
+    if (kq >= 1 && kend >= w.kcur) {
+        ed_segment(w, ic, w.kcur, kend, draws);
+        w.kcur = kend + 1;
+    }
+    w.t = tjump;
+    ++jumps;
+    ++draws;  // the accepted holding-time draw of the jump (paths.cpp:51-54)
+    const uint32_t ts = pick_edge(edges, w.cur.begin, w.cur.deg, stream_pop_bits(w.st));
+    if (ts & kSignBit) w.sign = -w.sign;
+    w.state = ts & kTargetMask;
+    w.cur = load_row(rows, w.state);
+    if (w.cur.d != w.dfirst) w.dconst = 0u;
+    return false;
+}
+
+__device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+                                          double& fine, double& coarse) {
+    const double sg = static_cast<double>(w.sign);
+    const double u_end = __ldg(&rows[w.state].u);
+    const double h = __dmul_rn(0.5, ic.dt);
+    if (ic.base) {
+        const double expo = __dmul_rn(h, w.acc_a);
+        fine = __dmul_rn(__dmul_rn(sg, expo == 0.0 ? 1.0 : exp(expo)), u_end);
+        coarse = 0.0;
+    } else {
+        const double uf = __dmul_rn(sg, u_end);
+        const double c = __dmul_rn(h, w.acc_a);
+        const double ec = c == 0.0 ? 1.0 : exp(c);
+        coarse = __dmul_rn(uf, ec);
+        fine = w.dconst ? coarse : __dmul_rn(uf, exp(__dadd_rn(c, __dmul_rn(h, w.acc_b))));
+    }
+}
+
+__device__ __forceinline__ double ed_sample(const EdWalker& w, const ItemConst& ic, const RowRec* __restrict__ rows) {
+    if (!ic.base && w.dconst) return 0.0;
+    double fine, coarse;
+    ed_finish(w, ic, rows, fine, coarse);
+    return ic.base ? fine : __dsub_rn(fine, coarse);
+}
+
+// ---- policies the chunk kernel is templated on
+struct RefPolicy {
+    using W = Walker;
+    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const RowRec* rows, uint64_t s) {
+        walker_start(w, ic, rows, s);
+    }
+    static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const RowRec* rows, const EdgeTables& e,
+                                                 const LogEntry* lg, unsigned long long& dr, unsigned long long& j) {
+        return walker_event(w, ic, rows, e, lg, dr, j);
+    }
+    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const RowRec* rows) {
+        return walker_sample(w, ic, rows);
+    }
+    static __device__ __forceinline__ void finish(const W& w, const ItemConst& ic, const RowRec* rows, double& f,
+                                                  double& c) {
+        walker_finish(w, ic, rows, f, c);
+    }
+};
+
+struct EdPolicy {
+    using W = EdWalker;
+    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const RowRec* rows, uint64_t s) {
+        ed_start(w, ic, rows, s);
+    }
+    static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const RowRec* rows, const EdgeTables& e,
+                                                 const LogEntry* lg, unsigned long long& dr, unsigned long long& j) {
+        return ed_event(w, ic, rows, e, lg, dr, j);
+    }
+    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const RowRec* rows) {
+        return ed_sample(w, ic, rows);
+    }
+    static __device__ __forceinline__ void finish(const W& w, const ItemConst& ic, const RowRec* rows, double& f,
+                                                  double& c) {
+        ed_finish(w, ic, rows, f, c);
+    }
+};
+
+}  // namespace expmc_b200

@@ -93,12 +93,12 @@ struct SamplerArgs {
     unsigned int* counter;    // dynamic chunk counter, zeroed before launch
 };
 
-void launch_sampler(const SamplerArgs& a, int grid, cudaStream_t s);
+void launch_sampler(const SamplerArgs& a, int grid, int mode, cudaStream_t s);
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
                     const Partial* partials, Partial* totals, cudaStream_t s);
 void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n,
-                  SampleOut* out, cudaStream_t s);
-int sampler_blocks_per_sm();
+                  SampleOut* out, int mode, cudaStream_t s);
+int sampler_blocks_per_sm(int mode);
 int sampler_threads();
 
 float bench_gather(uint64_t bytes, int loads_per_thread, int reps, int num_sms, uint64_t* total_loads);

@@ -17,6 +17,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "internal.hpp"
+#include "ed_walker.cuh"
 #include "walker.cuh"
 
 namespace expmc_b200 {
@@ -53,6 +54,7 @@ __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ chunk
     return lo;
 }
 
+template <class P>
 __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(SamplerArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned full = 0xFFFFFFFFu;
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
 
         double sum = 0.0, sum_sq = 0.0;
         unsigned long long cost = 0, jumps = 0;
-        Walker w;
+        typename P::W w;
         bool active = false;
         uint32_t next = 0;
         for (;;) {
@@ -94,14 +96,14 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
             if (!active) {
                 const uint32_t mine = next + __popc(need & lt_mask);
                 if (mine < cnt) {
-                    walker_start(w, ic, a.rows, lo + mine);
+                    P::start(w, ic, a.rows, lo + mine);
                     active = true;
                 }
             }
             next += __popc(need);
             if (!__any_sync(full, active)) break;
-            if (active && walker_event(w, ic, a.rows, a.edges, s_log, cost, jumps)) {
-                const double x = walker_sample(w, ic, a.rows);
+            if (active && P::event(w, ic, a.rows, a.edges, s_log, cost, jumps)) {
+                const double x = P::sample(w, ic, a.rows);
                 sum = __dadd_rn(sum, x);
                 sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
                 cost += ic.nsteps;
@@ -144,6 +146,7 @@ __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, 
     totals[i] = t;
 }
 
+template <class P>
 __global__ void k_debug(const RowRec* __restrict__ rows, EdgeTables edges,
                         const DevItem* __restrict__ items, uint32_t n, SampleOut* __restrict__ out) {
     __shared__ LogEntry s_log[128];
@@ -152,13 +155,13 @@ __global__ void k_debug(const RowRec* __restrict__ rows, EdgeTables edges,
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const ItemConst ic = load_item(items, i);
-    Walker w;
-    walker_start(w, ic, rows, items[i].first);
+    typename P::W w;
+    P::start(w, ic, rows, items[i].first);
     unsigned long long draws = 0, jumps = 0;
-    while (!walker_event(w, ic, rows, edges, s_log, draws, jumps)) {
+    while (!P::event(w, ic, rows, edges, s_log, draws, jumps)) {
     }
     SampleOut o;
-    walker_finish(w, ic, rows, o.fine, o.coarse);
+    P::finish(w, ic, rows, o.fine, o.coarse);
     o.cost = draws + ic.nsteps;
     o.jumps = jumps;
     o.end_state = w.state;
@@ -340,14 +343,18 @@ void cuda_check(cudaError_t e, const char* what) {
 
 int sampler_threads() { return kThreads; }
 
-int sampler_blocks_per_sm() {
+int sampler_blocks_per_sm(int mode) {
     int b = 0;
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample, kThreads, 0), "occupancy");
+    if (mode == EXPMC_SAMPLER_EVENT)
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<EdPolicy>, kThreads, 0), "occupancy");
+    else
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<RefPolicy>, kThreads, 0), "occupancy");
     return b > 0 ? b : 1;
 }
 
-void launch_sampler(const SamplerArgs& a, int grid, cudaStream_t s) {
-    k_sample<<<grid, kThreads, 0, s>>>(a);
+void launch_sampler(const SamplerArgs& a, int grid, int mode, cudaStream_t s) {
+    if (mode == EXPMC_SAMPLER_EVENT) k_sample<EdPolicy><<<grid, kThreads, 0, s>>>(a);
+    else k_sample<RefPolicy><<<grid, kThreads, 0, s>>>(a);
     cuda_check(cudaGetLastError(), "k_sample launch");
 }
 
@@ -357,9 +364,10 @@ void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, u
     cuda_check(cudaGetLastError(), "k_combine launch");
 }
 
-void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n, SampleOut* out,
+void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n, SampleOut* out, int mode,
                   cudaStream_t s) {
-    k_debug<<<grid_for(n, 128), 128, 0, s>>>(rows, edges, items, n, out);
+    if (mode == EXPMC_SAMPLER_EVENT) k_debug<EdPolicy><<<grid_for(n, 128), 128, 0, s>>>(rows, edges, items, n, out);
+    else k_debug<RefPolicy><<<grid_for(n, 128), 128, 0, s>>>(rows, edges, items, n, out);
     cuda_check(cudaGetLastError(), "k_debug launch");
 }
 

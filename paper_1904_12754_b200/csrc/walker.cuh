@@ -186,6 +186,8 @@ struct ItemConst {
     uint64_t nsteps;
     double dt;
     double half_dt;  // dt_ * 0.5, the left factor of paths.cpp:110
+    double tend;     // N * dt (= beta), event-driven walker
+    double inv_dt;   // 1 / dt, event-driven walker
     uint32_t entry;
     uint32_t key3;
     uint32_t base;
@@ -305,6 +307,8 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.nsteps = it.nsteps;
     ic.dt = it.dt;
     ic.half_dt = __dmul_rn(it.dt, 0.5);
+    ic.tend = __dmul_rn(it.dt, static_cast<double>(it.nsteps));
+    ic.inv_dt = __ddiv_rn(1.0, it.dt);
     ic.entry = it.entry;
     ic.key3 = it.key3;
     ic.base = it.base;

@@ -1,0 +1,91 @@
+"""GPU: the event-driven sampler (csrc/ed_walker.cuh) -- same path law, different draws.
+
+Exact checks where the law leaves no randomness (the reference unit tests' known answers:
+diagonal, K2 = e, coupled difference 0 on constant d, sign parity), the cost identity
+(cost = jumps + #non-absorbing boundaries + 2^l), and statistical agreement with the
+reference-order sampler (which is bit-for-bit the reference) at 4 standard errors.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1904_12754_b200 as P
+from paper_1904_12754_b200 import configs
+from oracle import CSR
+
+pytestmark = pytest.mark.gpu
+
+
+def test_ed_known_answers(gpu):
+    # diagonal: never moves, cost = steps (absorbing rows draw nothing), value exact (test_paths.cpp:84-99)
+    with P.Context(P.SparseMatrix.from_dense([[0.75, 0.0], [0.0, -0.5]]), np.array([3.0, 5.0]), sampler="event") as c:
+        s = c.sample_debug(2.0, 0, 3, 1, 2, np.arange(50))
+        assert np.all(s["cost"] == 8) and np.all(s["jumps"] == 0)
+        assert np.all(s["fine"] == s["fine"][0])
+        assert s["fine"][0] == pytest.approx(3.0 * math.exp(1.5), rel=1e-14)
+        s = c.sample_debug(2.0, 0, 3, 0, 4, np.arange(50))  # coupled on constant d: difference exactly 0
+        assert np.all(s["fine"] - s["coarse"] == 0.0)
+    # K2: d constant = 1 -> every path is exactly e (test_paths.cpp:101-111)
+    with P.Context(P.SparseMatrix.from_dense([[0.0, 1.0], [1.0, 0.0]]), np.ones(2), sampler="event") as c:
+        s = c.sample_debug(1.0, 0, 4, 1, 3, np.arange(1000))
+        assert np.all(s["fine"] == math.exp(1.0))
+        assert np.all(s["cost"] == s["jumps"] + 2 * 16)  # no absorbing rows: cost = jumps + 2 N
+        r = c.run_level_batch(1.0, 0, 4, 0, 0, 5000, 7)
+        assert r["sum"][0] == 0.0 and r["sum_sq"][0] == 0.0
+
+
+def test_ed_sign_parity(gpu):  # test_paths.cpp:226-249
+    pos = P.SparseMatrix.from_dense([[0, 1.0, 0], [1.0, 0, 0.5], [0, 0.5, 0]])
+    neg = P.SparseMatrix.from_dense([[0, -1.0, 0], [-1.0, 0, -0.5], [0, -0.5, 0]])
+    u = np.array([1.0, 2.0, 3.0])
+    with P.Context(pos, u, sampler="event") as cp, P.Context(neg, u, sampler="event") as cn:
+        a = cp.sample_debug(2.0, 0, 2, 1, 8, np.arange(300))
+        b = cn.sample_debug(2.0, 0, 2, 1, 8, np.arange(300))
+    assert np.array_equal(a["end_state"], b["end_state"]) and np.array_equal(a["jumps"], b["jumps"])
+    assert np.array_equal(b["fine"], a["fine"] * np.where(a["jumps"] % 2 == 0, 1.0, -1.0))
+
+
+def test_ed_absorbing_cost_identity(gpu):
+    # row 1 absorbing: cost = jumps + #{k >= 1 : rate(s_k) > 0} + N; check the bound and the mean
+    a = P.SparseMatrix.from_dense([[0.0, 1.0, 0.5], [0.0, -1.0, 0.0], [0.25, 0.25, 0.0]])
+    u = np.array([1.0, 2.0, 3.0])
+    with P.Context(a, u, sampler="event") as ce, P.Context(a, u) as cr:
+        e = ce.sample_debug(1.3, 0, 3, 0, 11, np.arange(20000))
+        r = cr.sample_debug(1.3, 0, 3, 0, 11, np.arange(20000))
+    n = 8
+    assert np.all(e["cost"] <= e["jumps"] + 2 * n) and np.all(e["cost"] >= e["jumps"] + n)
+    for key in ("cost", "jumps"):
+        me, mr = e[key].mean(), r[key].mean()
+        se = math.sqrt(e[key].var() / len(e[key]) + r[key].var() / len(r[key]))
+        assert abs(me - mr) < 4 * se + 1e-12, key
+
+
+@pytest.mark.parametrize("level,base", [(0, 1), (2, 1), (1, 0), (3, 0), (5, 0)])
+def test_ed_matches_reference_order_statistically(gpu, level, base):
+    cfg = configs.make_config("c1")
+    rows = np.array([0, 63, 130, 2080, 4095])
+    n = 400_000
+    with P.Context(cfg.a, cfg.u) as cr, P.Context(cfg.a, cfg.u, sampler="event") as ce:
+        r = cr.run_level_batch(cfg.beta, rows, level, base, 0, n, 1000 + rows)
+        e = ce.run_level_batch(cfg.beta, rows, level, base, 0, n, 77 + rows)
+    for k in range(len(rows)):
+        mr, me = r["sum"][k] / n, e["sum"][k] / n
+        vr = max(r["sum_sq"][k] / n - mr * mr, 0.0)
+        ve = max(e["sum_sq"][k] / n - me * me, 0.0)
+        se = math.sqrt((vr + ve) / n)
+        assert abs(mr - me) <= 4 * se + 1e-15, (level, base, rows[k], mr, me, se)
+        cr_, ce_ = r["cost"][k] / n, e["cost"][k] / n  # same unit cost in expectation
+        assert abs(cr_ - ce_) <= 0.02 * cr_ + 0.05, (cr_, ce_)
+
+
+def test_ed_driver_c1_rows_vs_exact(gpu, oracle_lib):
+    cfg = configs.make_config("c1")
+    rows = np.arange(0, cfg.a.n, 16)
+    with P.Context(cfg.a, cfg.u, sampler="event") as c:
+        res, _ = P.mlmc_driver_rows(c, cfg.beta, rows, configs.row_seeds(rows), P.MlmcOptions(epsilon=cfg.epsilon))
+    exact = oracle_lib.dense_expmv(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val), cfg.u, cfg.beta)[rows]
+    err = res["estimate"] - exact
+    assert res["converged"].all()
+    assert math.sqrt(float(np.mean(err ** 2))) <= cfg.epsilon
+    assert float(np.mean(np.abs(err) > 3 * res["statistical_error"] + res["bias_estimate"])) <= 0.02
