@@ -196,6 +196,22 @@ int expmc_mlmc_driver_rows(expmc_ctx* ctx, double beta, const expmc_options* opt
  * best of `reps` launches.  Writes achieved GB/s (32 B per load / kernel time). */
 int expmc_bench_gather(int device, uint64_t bytes, int32_t loads_per_thread, int32_t reps, double* gbps);
 
+/* Host input generators for the BASELINE configs (no GPU needed; csrc/gen.cpp).
+ * Results are canonical CSR matrices owned by the library until expmc_matrix_destroy. */
+typedef struct expmc_matrix expmc_matrix;
+/* Barabasi-Albert, the reference's pref(n, d, seed) algorithm (netgen.cpp:61-107). */
+int expmc_gen_ba(int64_t n, int64_t d, uint64_t seed, expmc_matrix** out);
+/* R-MAT: 2^scale nodes, edge_factor * 2^scale directed draws, symmetrised, unit weights. */
+int expmc_gen_rmat(int32_t scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
+                   expmc_matrix** out);
+/* 3-D 7-point convection-diffusion on g^3 nodes, cell Peclet `peclet` along `axis` (0=x). */
+int expmc_gen_convdiff3d(int64_t g, double peclet, int32_t axis, expmc_matrix** out);
+int expmc_matrix_info(const expmc_matrix* m, int64_t* n, int64_t* nnz);
+int expmc_matrix_copy(const expmc_matrix* m, int64_t* row_ptr, int64_t* col, double* val);
+void expmc_matrix_destroy(expmc_matrix* m);
+/* lambda_max estimate by `iters` power iterations from the all-ones vector. */
+int expmc_power_iteration(const expmc_csr* A, int32_t iters, double* lambda);
+
 /* Host-side driver helpers, identical to the reference (no GPU needed). */
 int expmc_initial_level(double beta, double d_max, int32_t* out);             /* mlmc.cpp:19-23 */
 int expmc_optimal_allocation(int64_t nlevels, const double* variances,        /* mlmc.cpp:25-43 */

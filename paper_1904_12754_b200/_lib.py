@@ -77,6 +77,13 @@ SYMBOLS = [
     ("expmc_sample_debug", C.c_int, [_P, _D, _U32, _I64, _P, _P, _P, _P, _P, _P]),
     ("expmc_mlmc_driver", C.c_int, [_P, _I64, _D, C.POINTER(OptionsC), C.POINTER(ResultC), _P, _I32]),
     ("expmc_mlmc_driver_rows", C.c_int, [_P, _D, C.POINTER(OptionsC), _I64, _P, _P, _P, _P, _I32]),
+    ("expmc_gen_ba", C.c_int, [_I64, _I64, _U64, C.POINTER(_P)]),
+    ("expmc_gen_rmat", C.c_int, [_I32, _I64, _D, _D, _D, _U64, C.POINTER(_P)]),
+    ("expmc_gen_convdiff3d", C.c_int, [_I64, _D, _I32, C.POINTER(_P)]),
+    ("expmc_matrix_info", C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("expmc_matrix_copy", C.c_int, [_P, _P, _P, _P]),
+    ("expmc_matrix_destroy", None, [_P]),
+    ("expmc_power_iteration", C.c_int, [C.POINTER(Csr), _I32, C.POINTER(_D)]),
     ("expmc_initial_level", C.c_int, [_D, _D, C.POINTER(_I32)]),
     ("expmc_optimal_allocation", C.c_int, [_I64, _P, _P, _D, _P]),
     ("expmc_bias_estimate", C.c_int, [_I64, _P, C.POINTER(_D)]),

@@ -9,11 +9,13 @@ There is no public dataset behind these configs: everything is generated from se
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+import ctypes as C
+from dataclasses import dataclass, field
 
 import numpy as np
 
-from .api import SparseMatrix
+from . import _lib as L
+from .api import SparseMatrix, _check, _ptr
 
 _M0, _M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
 _W0, _W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
@@ -71,17 +73,83 @@ class Config:
     beta: float
     epsilon: float
     description: str
+    sampler: str = "reference"         # the path sampler the config is run with
+    rows: np.ndarray | None = None     # components to estimate (None: all)
+    max_levels_above_l0: int = 30      # MlmcOptions.max_levels_above_l0
+    extra: dict = field(default_factory=dict)
 
 
 VECTOR_SEED = 12345  # v = stream_for(12345, 0, i, 6), as in the survey probes
+GRAPH_SEED = 1       # BA / R-MAT seed (SURVEY §8d probes used seed 1 for C3)
+
+
+# ---------------------------------------------------------------- native generators (csrc/gen.cpp)
+def _take(h) -> SparseMatrix:
+    n, nnz = C.c_int64(), C.c_int64()
+    _check(L.lib.expmc_matrix_info(h, C.byref(n), C.byref(nnz)))
+    rp = np.empty(n.value + 1, np.int64)
+    col = np.empty(nnz.value, np.int64)
+    val = np.empty(nnz.value, np.float64)
+    _check(L.lib.expmc_matrix_copy(h, _ptr(rp), _ptr(col), _ptr(val)))
+    L.lib.expmc_matrix_destroy(h)
+    return SparseMatrix(n.value, rp, col, val)
+
+
+def gen_ba(n: int, d: int, seed: int) -> SparseMatrix:
+    """Barabasi-Albert adjacency, the reference's pref(n, d, seed) (netgen.cpp:61-107)."""
+    h = C.c_void_p()
+    _check(L.lib.expmc_gen_ba(n, d, seed, C.byref(h)))
+    return _take(h)
+
+
+def gen_rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19, c: float = 0.19,
+             seed: int = GRAPH_SEED) -> SparseMatrix:
+    """Symmetrised unit-weight R-MAT graph on 2^scale nodes (BASELINE config 4)."""
+    h = C.c_void_p()
+    _check(L.lib.expmc_gen_rmat(scale, edge_factor, a, b, c, seed, C.byref(h)))
+    return _take(h)
+
+
+def gen_convdiff3d(g: int, peclet: float = 10.0, axis: int = 0) -> SparseMatrix:
+    """3-D 7-point convection-diffusion on g^3 nodes (BASELINE config 5): diag -6, off 1,
+    upwind/downwind 1 +/- Pe/2 along `axis` (x by default: Pe = 10 gives +6 / -4)."""
+    h = C.c_void_p()
+    _check(L.lib.expmc_gen_convdiff3d(g, peclet, axis, C.byref(h)))
+    return _take(h)
+
+
+def power_iteration(a: SparseMatrix, iters: int = 50) -> float:
+    rp = np.ascontiguousarray(a.row_ptr, np.int64)
+    col = np.ascontiguousarray(a.col, np.int64)
+    val = np.ascontiguousarray(a.val, np.float64)
+    csr = L.Csr(a.n, int(rp[-1]), _ptr(rp), _ptr(col), _ptr(val))
+    lam = C.c_double()
+    _check(L.lib.expmc_power_iteration(C.byref(csr), iters, C.byref(lam)))
+    return lam.value
+
+
+def seeded_rows(n: int, k: int, seed: int = 4242) -> np.ndarray:
+    """k distinct seed-chosen components, sorted."""
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n, size=min(k, n), replace=False)).astype(np.int64)
+
+
+def _graph_config(name, a, desc, rows=None) -> Config:
+    # e^{A / lambda} 1 = e^{beta A} 1 with beta = 1 / lambda: the unscaled 0/1 adjacency keeps every
+    # row's CDF exactly uniform (kUniformRow); both arms are run on the same (A, beta).
+    lam = power_iteration(a, 50)
+    return Config(name, a, np.ones(a.n), 1.0 / lam, 1e-3, desc + f"; lambda_max~{lam:.4g} (50 power iterations), "
+                  "beta = 1/lambda, v = 1 (total communicability)", sampler="event", rows=rows,
+                  extra={"lambda": lam})
 
 
 def make_config(name: str) -> Config:
-    if name in ("c1", "C1"):
+    name = name.lower()
+    if name == "c1":
         a = grid_laplacian(64)
         return Config("c1", a, grid_vector(VECTOR_SEED, a.n), 1.0, 1e-3,
                       "2D 5-point Laplacian 64x64 (n=4096), t=1, eps=1e-3, all components")
-    if name in ("c2", "C2"):
+    if name == "c2":
         a = grid_laplacian(1024)
         return Config("c2", a, grid_vector(VECTOR_SEED, a.n), 0.5, 1e-3,
                       "2D 5-point Laplacian 1024x1024 (n=1,048,576), t=0.5, eps=1e-3, all components")
@@ -89,4 +157,20 @@ def make_config(name: str) -> Config:
         g = int(name[4:])
         a = grid_laplacian(g)
         return Config(name, a, grid_vector(VECTOR_SEED, a.n), 1.0, 1e-3, f"2D 5-point Laplacian {g}x{g}")
+    if name == "c3" or name.startswith("c3-"):
+        n = int(name[3:]) if "-" in name else 1_000_000
+        return _graph_config(name, gen_ba(n, 5, GRAPH_SEED),
+                             f"Barabasi-Albert n={n}, m=5 (reference pref algorithm, seed {GRAPH_SEED})")
+    if name == "c4" or name.startswith("c4-"):
+        scale = int(name[3:]) if "-" in name else 24
+        a = gen_rmat(scale, 16)
+        return _graph_config(name, a, f"R-MAT scale {scale} (a=0.57, b=c=0.19, d=0.05), 16*2^{scale} edges, "
+                             "symmetrised, unit weights", rows=seeded_rows(a.n, min(a.n, 1 << 20)))
+    if name == "c5" or name.startswith("c5-"):
+        g = int(name[3:]) if "-" in name else 256
+        a = gen_convdiff3d(g, 10.0, 0)
+        u = 2.0 * philox_first_uniform(VECTOR_SEED, 0, np.arange(a.n, dtype=np.uint64), 6) - 1.0
+        return Config(name, a, u, 0.1, 1e-4,
+                      f"3D 7-point convection-diffusion {g}^3 (cell Peclet 10 along x: off-diagonals +6/-4/1), "
+                      "t=0.1, v uniform [-1,1), eps=1e-4, 5 MLMC levels", max_levels_above_l0=4)
     raise ValueError(f"unknown config {name!r}")
