@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--config", default="c2")
     p.add_argument("--rows-per-step", type=int, default=0, help="components per rank per step (0: default)")
     p.add_argument("--ref-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    p.add_argument("--max-cost", type=float, default=None,
+                   help="per-component model-unit budget (driver extension; default off for C1/C2, 1e10 for C3-C5)")
+    p.add_argument("--sampler", default=None, choices=["reference", "event"], help="override the config's sampler")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -92,6 +95,17 @@ def sample_rows(n, step, r):
     if r == 0:
         return np.roll(perm, -step * 1024)
     return perm[(np.arange(step * r, step * r + r) % n)]
+
+
+def cpu_rows(cfg, step, r):
+    """Components for the CPU reference sample.  Graph/3-D configs: light rows only (degree <= 32)
+    -- the reference has no cost budget and one hub row can run for hours."""
+    universe = cfg.rows if cfg.rows is not None else np.arange(cfg.a.n, dtype=np.int64)
+    rows = universe[sample_rows(len(universe), step, r)]
+    if cfg.name.startswith(("c3", "c4", "c5")):
+        deg = np.diff(cfg.a.row_ptr)
+        rows = rows[deg[rows] <= 32]
+    return rows
 
 
 class Clocks:
@@ -166,7 +180,8 @@ def reference_rows(ref_chain, cfg, rows, seconds, threads, max_rows):
     jumps = samples = done = 0
     t0 = time.perf_counter()
     for r in rows[:max_rows]:
-        (res,) = ref_chain.driver_rows(cfg.u, cfg.beta, [int(r)], [1000 + int(r)], epsilon=cfg.epsilon, threads=threads)
+        (res,) = ref_chain.driver_rows(cfg.u, cfg.beta, [int(r)], [1000 + int(r)], epsilon=cfg.epsilon, threads=threads,
+                                       max_levels_above_l0=cfg.max_levels_above_l0)
         jumps += res["total_jumps"]
         samples += res["total_samples"]
         done += 1
@@ -187,11 +202,11 @@ def run_reference(args, cfg, rank, world, r):
     ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
     per_step = max(1.0, args.ref_seconds / max(1, args.steps))
     for w in range(args.warmup):
-        reference_rows(ref, cfg, sample_rows(cfg.a.n, w, r), min(per_step, 2.0), threads, 4)
+        reference_rows(ref, cfg, cpu_rows(cfg, w, r), min(per_step, 2.0), threads, 4)
     tj = ts = tr = 0
     tt = 0.0
     for s in range(args.steps):
-        j, smp, done, dt = reference_rows(ref, cfg, sample_rows(cfg.a.n, args.warmup + s, r), per_step, threads, 1 << 30)
+        j, smp, done, dt = reference_rows(ref, cfg, cpu_rows(cfg, args.warmup + s, r), per_step, threads, 1 << 30)
         tj += j
         ts += smp
         tr += done
@@ -220,7 +235,13 @@ def main():
     from paper_1904_12754_b200 import configs
 
     cfg = configs.make_config(args.config)
-    r = args.rows_per_step  # 0: the whole C2 job per step
+    graph_like = cfg.name.startswith(("c3", "c4", "c5"))
+    # C1/C2: the whole job per step.  C3-C5 (10^6-10^7 components, hub rows infeasible at the
+    # stated eps): a seeded sample of components per step and a per-component budget.
+    r = args.rows_per_step if args.rows_per_step or not graph_like else 65536
+    max_cost = args.max_cost if args.max_cost is not None else (1e10 if graph_like else 0.0)
+    sampler = args.sampler or cfg.sampler
+    universe = cfg.rows if cfg.rows is not None else np.arange(cfg.a.n, dtype=np.int64)
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world, r)
 
@@ -253,13 +274,13 @@ def main():
         dist.all_reduce(t)
         return float(t.item())
 
-    opts = P.MlmcOptions(epsilon=cfg.epsilon)
+    opts = P.MlmcOptions(epsilon=cfg.epsilon, max_levels_above_l0=cfg.max_levels_above_l0, max_cost=max_cost)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    ctx = P.Context(cfg.a, cfg.u, device=local)
+    ctx = P.Context(cfg.a, cfg.u, device=local, sampler=sampler)
     ext = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local))
 
     # the batches of every step are built before any timing starts
-    batches = [batch_rows(cfg.a.n, s, rank, world, r) for s in range(args.warmup + args.steps)]
+    batches = [universe[batch_rows(len(universe), s, rank, world, r)] for s in range(args.warmup + args.steps)]
     seeds = [configs.row_seeds(b) for b in batches]
 
     def solve(step):
@@ -296,6 +317,8 @@ def main():
     samples = sum_over_ranks(ctr["samples"])
     rows_done = sum_over_ranks(len(res))
     conv = sum_over_ranks(int(res["converged"].sum()))
+    over = sum_over_ranks(int(res["over_budget"].sum()))
+    proj_over = float(res["projected_cost"][res["over_budget"] != 0].max()) if (res["over_budget"] != 0).any() else 0.0
     value = jumps / (ms * 1e-3)
 
     # roofline of the dominant kernel (k_sample): algorithmic bytes / summed launch time
@@ -349,7 +372,7 @@ def main():
             if have_reference():
                 threads = os.cpu_count() or 1
                 ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
-                j, smp, done, dt = reference_rows(ref, cfg, sample_rows(cfg.a.n, args.warmup, r),
+                j, smp, done, dt = reference_rows(ref, cfg, cpu_rows(cfg, args.warmup, r),
                                                   args.ref_seconds, threads, 1 << 30)
                 cpu = {"value": j / dt, "unit": UNIT, "cores": threads, "kind": "reference",
                        "sample": f"{done} randomly chosen C2 components through the as-shipped reference "
@@ -363,14 +386,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if r == 0 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2 (BASELINE configs[1]): {cfg.description}; one step = "
+            "config": {"workload": f"{cfg.name.upper()}: {cfg.description}; one step = "
                                    + (f"the whole job (all {cfg.a.n} components) split over the ranks" if r == 0 else
-                                      f"MLMC driver solve of {r} components per rank"),
+                                      f"MLMC driver solve of {r} seeded components per rank"),
                        "components_per_step": int(rows_done / args.steps), "epsilon": cfg.epsilon, "t": cfg.beta,
-                       "l2": "flushed (256 MB write) before every step; C2 tables (~100 MB) are L2-sized",
+                       "l2": f"flushed (256 MB write) before every step; tables {ctx.table_bytes / 1e6:.0f} MB",
                        "parallelism": f"rows sharded over {world} rank(s), no data-path collective"},
             "rows_per_s": rows_done / (ms * 1e-3), "samples_per_s": samples / (ms * 1e-3),
-            "converged_rows": int(conv), "rows": int(rows_done),
+            "converged_rows": int(conv), "rows": int(rows_done), "sampler": sampler,
+            "over_budget_rows": int(over), "max_cost": max_cost, "max_projected_cost_over_budget": proj_over,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k_sample", "sampler_launches": ctr["sampler_launches"],

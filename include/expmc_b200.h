@@ -95,6 +95,10 @@ typedef struct {
     uint64_t warmup;
     int32_t max_levels_above_l0;
     int32_t max_iterations;
+    /* Extension (0 = off = the reference's behaviour): stop a component, unconverged, as soon
+     * as the Lagrange allocation projects more than max_cost model units for it (hub rows of
+     * C3/C4 need ~1e17 at eps = 1e-3); its projection is reported. */
+    double max_cost;
 } expmc_options;
 
 /* MlmcResult (mlmc.hpp:33-43) without the per-level vector (returned separately). */
@@ -109,6 +113,9 @@ typedef struct {
     int32_t nlevels;
     uint64_t total_jumps;
     uint64_t total_samples;
+    double projected_cost; /* model units the last allocation asked for (sum_l M_l C_l) */
+    int32_t over_budget;   /* 1: stopped by max_cost */
+    int32_t pad;
 } expmc_result;
 
 /* One entry of MlmcResult::levels (LevelStats, mlmc.hpp:18-24). */

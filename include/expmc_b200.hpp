@@ -70,8 +70,9 @@ struct MlmcOptions {
     std::uint64_t warmup = 1000;
     int max_levels_above_l0 = 30;
     int max_iterations = 200;
+    double max_cost = 0.0;  // extension (0 = off): per-component budget in model units
     expmc_options c() const {
-        return expmc_options{epsilon, seed, threads, l0_override, warmup, max_levels_above_l0, max_iterations};
+        return expmc_options{epsilon, seed, threads, l0_override, warmup, max_levels_above_l0, max_iterations, max_cost};
     }
 };
 

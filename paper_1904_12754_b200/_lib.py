@@ -37,13 +37,13 @@ class LevelStatsC(C.Structure):
 
 class OptionsC(C.Structure):
     _fields_ = [("epsilon", _D), ("seed", _U64), ("threads", _I32), ("l0_override", _I32), ("warmup", _U64),
-                ("max_levels_above_l0", _I32), ("max_iterations", _I32)]
+                ("max_levels_above_l0", _I32), ("max_iterations", _I32), ("max_cost", _D)]
 
 
 class ResultC(C.Structure):
     _fields_ = [("estimate", _D), ("statistical_error", _D), ("bias_estimate", _D), ("l0", _I32), ("L", _I32),
                 ("total_cost", _U64), ("converged", _I32), ("nlevels", _I32), ("total_jumps", _U64),
-                ("total_samples", _U64)]
+                ("total_samples", _U64), ("projected_cost", _D), ("over_budget", _I32), ("pad", _I32)]
 
 
 class LevelRecordC(C.Structure):

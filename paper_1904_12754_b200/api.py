@@ -179,10 +179,11 @@ class MlmcOptions:
     warmup: int = 1000
     max_levels_above_l0: int = 30
     max_iterations: int = 200
+    max_cost: float = 0.0  # extension: per-component model-unit budget (0 = off, the reference)
 
     def _c(self) -> L.OptionsC:
         return L.OptionsC(self.epsilon, self.seed, self.threads, self.l0_override, self.warmup,
-                          self.max_levels_above_l0, self.max_iterations)
+                          self.max_levels_above_l0, self.max_iterations, self.max_cost)
 
 
 @dataclass
@@ -200,6 +201,8 @@ class MlmcResult:
     converged: bool = False
     total_jumps: int = 0
     total_samples: int = 0
+    projected_cost: float = 0.0
+    over_budget: bool = False
 
 
 # --------------------------------------------------------------------------------- context
@@ -325,7 +328,8 @@ _STATS_DT = np.dtype([("sum", np.float64), ("sum_sq", np.float64), ("samples", n
                       ("jumps", np.uint64)])
 _RESULT_DT = np.dtype([("estimate", np.float64), ("statistical_error", np.float64), ("bias_estimate", np.float64),
                        ("l0", np.int32), ("L", np.int32), ("total_cost", np.uint64), ("converged", np.int32),
-                       ("nlevels", np.int32), ("total_jumps", np.uint64), ("total_samples", np.uint64)])
+                       ("nlevels", np.int32), ("total_jumps", np.uint64), ("total_samples", np.uint64),
+                       ("projected_cost", np.float64), ("over_budget", np.int32), ("pad", np.int32)])
 LEVEL_RECORD_DT = np.dtype([("level", np.int32), ("pad", np.int32), ("sum", np.float64), ("sum_sq", np.float64),
                             ("samples", np.uint64), ("cost", np.uint64)])
 assert _REQ_DT.itemsize == C.sizeof(L.LevelReq)
@@ -357,7 +361,7 @@ def _result(r, levels) -> MlmcResult:
           for x in levels]
     return MlmcResult(float(r["estimate"]), float(r["statistical_error"]), float(r["bias_estimate"]), 0.0, lv,
                       int(r["l0"]), int(r["L"]), int(r["total_cost"]), bool(r["converged"]), int(r["total_jumps"]),
-                      int(r["total_samples"]))
+                      int(r["total_samples"]), float(r["projected_cost"]), bool(r["over_budget"]))
 
 
 def mlmc_driver(problem: MlmcProblem, options: MlmcOptions = MlmcOptions(), max_levels: int = 64) -> MlmcResult:

@@ -75,13 +75,16 @@ struct RowState {
     std::vector<Level> lv;
     std::vector<std::pair<int, uint64_t>> pending;  // (level index, additional samples)
     double stat_error = 0.0, bias = 0.0;
+    double projected = 0.0;
     bool converged = false;
+    bool over_budget = false;
 };
 
 struct DriverConfig {
     double eps, target;
     uint64_t warmup;
     int max_iterations;
+    double max_cost;
 };
 
 // Advance one row whose pending work has completed, up to its next GPU request or the end.
@@ -104,6 +107,15 @@ void advance(RowState& r, const DriverConfig& cfg, std::vector<double>& v, std::
                 c[i] = std::max(r.lv[i].unit_cost(), 1.0);
             }
             optimal_allocation_impl(nl, v.data(), c.data(), cfg.eps, want.data());
+            double proj = 0.0;
+            for (size_t i = 0; i < nl; ++i)
+                proj += static_cast<double>(std::max(want[i], r.lv[i].samples)) * c[i];
+            r.projected = proj;
+            if (cfg.max_cost > 0.0 && proj > cfg.max_cost) {  // extension: infeasible component
+                r.over_budget = true;
+                r.phase = Phase::done;
+                return;
+            }
             for (size_t i = 0; i < nl; ++i)
                 if (want[i] > r.lv[i].samples)
                     r.pending.emplace_back(static_cast<int>(i), want[i] - r.lv[i].samples);
@@ -151,7 +163,7 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
     if (!(opt.epsilon > 0.0)) throw Status(EXPMC_EINVAL, "epsilon must be positive");
     const int l0 = opt.l0_override >= 0 ? opt.l0_override : initial_level_impl(beta, info.d_max);
     const int cap = l0 + opt.max_levels_above_l0;
-    DriverConfig cfg{opt.epsilon, opt.epsilon / std::sqrt(2.0), opt.warmup, opt.max_iterations};
+    DriverConfig cfg{opt.epsilon, opt.epsilon / std::sqrt(2.0), opt.warmup, opt.max_iterations, opt.max_cost};
 
     std::vector<RowState> st(static_cast<size_t>(nrows));
 #pragma omp parallel for schedule(static)
@@ -258,6 +270,8 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
         o.statistical_error = s.stat_error;
         o.bias_estimate = s.bias;
         o.converged = s.converged ? 1 : 0;
+        o.projected_cost = s.projected;
+        o.over_budget = s.over_budget ? 1 : 0;
         o.nlevels = static_cast<int32_t>(s.lv.size());
         for (size_t i = 0; i < s.lv.size(); ++i) {
             const Level& l = s.lv[i];
