@@ -176,18 +176,34 @@ def load_traffic():
 
 # ------------------------------------------------------------------------------ reference arm
 def reference_rows(ref_chain, cfg, rows, seconds, threads, max_rows):
-    """Reference mlmc_driver on rows one at a time until the budget runs out."""
-    jumps = samples = done = 0
+    """Reference mlmc_driver on rows one at a time, in a worker thread, for at most `seconds`.
+
+    A single reference run cannot be interrupted and some components never finish in practice
+    (the bias test can escalate to 2^(l0+30) steps per path), so the worker is
+    abandoned at the deadline (it dies with the process) and only completed components count:
+    throughput = their transitions / the time the last of them finished."""
+    deg = np.diff(cfg.a.row_ptr)
+    done_rows = []
     t0 = time.perf_counter()
-    for r in rows[:max_rows]:
-        (res,) = ref_chain.driver_rows(cfg.u, cfg.beta, [int(r)], [1000 + int(r)], epsilon=cfg.epsilon, threads=threads,
-                                       max_levels_above_l0=cfg.max_levels_above_l0)
-        jumps += res["total_jumps"]
-        samples += res["total_samples"]
-        done += 1
-        if time.perf_counter() - t0 >= seconds:
-            break
-    return jumps, samples, done, time.perf_counter() - t0
+
+    def work():
+        for r in rows[:max_rows]:
+            (res,) = ref_chain.driver_rows(cfg.u, cfg.beta, [int(r)], [1000 + int(r)], epsilon=cfg.epsilon,
+                                           threads=threads, max_levels_above_l0=cfg.max_levels_above_l0)
+            # transitions = cost - 2 M 2^l per level (BASELINE.md §3.5); an isolated row (rate 0,
+            # absorbing) draws nothing and never jumps
+            jumps = 0 if deg[int(r)] == 0 else res["total_jumps"]
+            done_rows.append((time.perf_counter(), jumps, res["total_samples"]))
+            if time.perf_counter() - t0 >= seconds:
+                return
+
+    th = threading.Thread(target=work, daemon=True)
+    th.start()
+    th.join(timeout=seconds + 1.0)
+    got = list(done_rows)
+    if not got:
+        return 0, 0, 0, time.perf_counter() - t0
+    return sum(g[1] for g in got), sum(g[2] for g in got), len(got), got[-1][0] - t0
 
 
 def run_reference(args, cfg, rank, world, r):
@@ -200,18 +216,12 @@ def run_reference(args, cfg, rank, world, r):
         return 0
     threads = os.cpu_count() or 1
     ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
-    per_step = max(1.0, args.ref_seconds / max(1, args.steps))
-    for w in range(args.warmup):
-        reference_rows(ref, cfg, cpu_rows(cfg, w, r), min(per_step, 2.0), threads, 4)
-    tj = ts = tr = 0
-    tt = 0.0
-    for s in range(args.steps):
-        j, smp, done, dt = reference_rows(ref, cfg, cpu_rows(cfg, args.warmup + s, r), per_step, threads, 1 << 30)
-        tj += j
-        ts += smp
-        tr += done
-        tt += dt
-    value = tj / tt
+    # warm-up: one small component (pages the matrix in, spins up the OpenMP pool); then the
+    # whole timed sample as ONE bounded worker run (an abandoned worker must not overlap a
+    # later timing window), reported per step as its K-th part
+    reference_rows(ref, cfg, cpu_rows(cfg, 0, r), 2.0, threads, 1)
+    tj, ts, tr, tt = reference_rows(ref, cfg, cpu_rows(cfg, args.warmup, r), args.ref_seconds, threads, 1 << 30)
+    value = tj / tt if tr else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
@@ -219,9 +229,9 @@ def run_reference(args, cfg, rank, world, r):
         "impl": "reference",
         "config": {"workload": cfg.description, "sample": f"{tr} components (as-shipped mlmc_driver per row)",
                    "parallelism": f"OpenMP {threads} threads, rank 0 only"},
-        "rows_per_s": tr / tt, "samples_per_s": ts / tt,
+        "rows_per_s": tr / tt if tr else None, "samples_per_s": ts / tt if tr else None,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{tr} C2 components, as-shipped reference mlmc_driver, {tt:.1f} s"},
+                         "sample": f"{tr} {cfg.name.upper()} components, as-shipped reference mlmc_driver, {tt:.1f} s"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -374,9 +384,9 @@ def main():
                 ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
                 j, smp, done, dt = reference_rows(ref, cfg, cpu_rows(cfg, args.warmup, r),
                                                   args.ref_seconds, threads, 1 << 30)
-                cpu = {"value": j / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-                       "sample": f"{done} randomly chosen C2 components through the as-shipped reference "
-                                 f"mlmc_driver (OpenMP, {dt:.1f} s)", "rows_per_s": done / dt}
+                cpu = {"value": j / dt if done else None, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"{done} randomly chosen {cfg.name.upper()} components through the as-shipped reference "
+                                 f"mlmc_driver (OpenMP, {dt:.1f} s)", "rows_per_s": done / dt if done else None}
         except Exception as exc:  # baseline failure must not hide the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
 
