@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--max-cost", type=float, default=None,
                    help="per-component model-unit budget (driver extension; default off for C1/C2, 1e10 for C3-C5)")
     p.add_argument("--sampler", default=None, choices=["reference", "event"], help="override the config's sampler")
+    p.add_argument("--multi", default="rows", choices=["rows", "samples"],
+                   help="N>1: shard components over ranks (no collective) or shard every component's "
+                        "samples with an exact NCCL all-reduce of the chunk partials")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -83,7 +86,9 @@ def batch_rows(n, step, rank, world, r):
     per rank per step, consecutive slices of the permutation (weak scaling)."""
     perm = perm_rows(n)
     if r == 0:
-        return np.sort(perm[rank::world])
+        from paper_1904_12754_b200.shard import row_shard
+
+        return row_shard(n, rank, world)  # == np.sort(perm[rank::world])
     k = (step * world + rank) * r
     idx = (np.arange(k, k + r) % n)
     return np.sort(perm[idx])
@@ -287,10 +292,16 @@ def main():
     opts = P.MlmcOptions(epsilon=cfg.epsilon, max_levels_above_l0=cfg.max_levels_above_l0, max_cost=max_cost)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ctx = P.Context(cfg.a, cfg.u, device=local, sampler=sampler)
+    sample_shard = args.multi == "samples" and world > 1
+    if sample_shard:  # every rank runs the same components; chunk g is sampled on rank g % world
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.shard_samples(obj[0], rank, world)
+    rank_b, world_b = (0, 1) if sample_shard else (rank, world)
     ext = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device("cuda", local))
 
     # the batches of every step are built before any timing starts
-    batches = [universe[batch_rows(len(universe), s, rank, world, r)] for s in range(args.warmup + args.steps)]
+    batches = [universe[batch_rows(len(universe), s, rank_b, world_b, r)] for s in range(args.warmup + args.steps)]
     seeds = [configs.row_seeds(b) for b in batches]
 
     def solve(step):
@@ -323,11 +334,13 @@ def main():
     ms = max_over_ranks(ms_local)
     ctr = ctx.counters()
     res = np.concatenate(results)
-    jumps = sum_over_ranks(ctr["jumps"])
-    samples = sum_over_ranks(ctr["samples"])
-    rows_done = sum_over_ranks(len(res))
-    conv = sum_over_ranks(int(res["converged"].sum()))
-    over = sum_over_ranks(int(res["over_budget"].sum()))
+    # sample sharding: every rank holds the combined (all-reduced) totals of the same components
+    agg = (lambda x: x) if sample_shard else sum_over_ranks
+    jumps = agg(ctr["jumps"])
+    samples = agg(ctr["samples"])
+    rows_done = agg(len(res))
+    conv = agg(int(res["converged"].sum()))
+    over = agg(int(res["over_budget"].sum()))
     proj_over = float(res["projected_cost"][res["over_budget"] != 0].max()) if (res["over_budget"] != 0).any() else 0.0
     value = jumps / (ms * 1e-3)
 
@@ -356,9 +369,15 @@ def main():
         jumps_e = 0
         h2d = d2h = 0
         e2e_steps = min(args.steps, 3)  # bounded: each e2e step is a full solve plus the table build
+        ids = [None] * e2e_steps
+        if sample_shard:
+            ids = [P.nccl_unique_id() if rank == 0 else None for _ in range(e2e_steps)]
+            dist.broadcast_object_list(ids, src=0)
         e0.record()
         for s in range(e2e_steps):
-            with P.Context(cfg.a, cfg.u, device=local) as c2:
+            with P.Context(cfg.a, cfg.u, device=local, sampler=sampler) as c2:
+                if sample_shard:
+                    c2.shard_samples(ids[s], rank, world)
                 rows = batches[args.warmup + s]
                 P.mlmc_driver_rows(c2, cfg.beta, rows, seeds[args.warmup + s], opts, want_levels=False)
                 k = c2.counters()
@@ -369,7 +388,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ms_e = max_over_ranks(e0.elapsed_time(e1))
-        e2e = {"value": sum_over_ranks(jumps_e) / (ms_e * 1e-3), "unit": UNIT,
+        e2e = {"value": agg(jumps_e) / (ms_e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d / e2e_steps), "d2h_bytes_per_step": int(d2h / e2e_steps),
                "ms_per_step": ms_e / e2e_steps, "steps": e2e_steps,
                "includes": "table build from host CSR+u (H2D), driver solve, per-round H2D/D2H, results to host"}
@@ -401,7 +420,9 @@ def main():
                                       f"MLMC driver solve of {r} seeded components per rank"),
                        "components_per_step": int(rows_done / args.steps), "epsilon": cfg.epsilon, "t": cfg.beta,
                        "l2": f"flushed (256 MB write) before every step; tables {ctx.table_bytes / 1e6:.0f} MB",
-                       "parallelism": f"rows sharded over {world} rank(s), no data-path collective"},
+                       "parallelism": (f"samples sharded over {world} ranks, exact NCCL all-reduce of chunk partials"
+                                       if sample_shard else
+                                       f"rows sharded over {world} rank(s), no data-path collective")},
             "rows_per_s": rows_done / (ms * 1e-3), "samples_per_s": samples / (ms * 1e-3),
             "converged_rows": int(conv), "rows": int(rows_done), "sampler": sampler,
             "over_budget_rows": int(over), "max_cost": max_cost, "max_projected_cost_over_budget": proj_over,

@@ -139,6 +139,7 @@ typedef struct {
     uint64_t jumps;
     uint64_t fine_steps;
     uint64_t rounds;           /* batched driver rounds (kernel batches) */
+    uint64_t nccl_bytes;       /* chunk-partial bytes all-reduced (sample-sharded mode) */
 } expmc_counters;
 
 const char* expmc_last_error(void);
@@ -167,6 +168,22 @@ int expmc_ctx_get_sampler(const expmc_ctx* ctx, int32_t* mode);
  * the sampler kernels are launched on. */
 int expmc_ctx_get_stream(const expmc_ctx* ctx, void** stream);
 int expmc_ctx_reset_counters(expmc_ctx* ctx);
+
+/* Sample sharding over GPUs (one process per GPU).  Every rank runs the SAME rows
+ * and requests; a batch's 512-sample chunk g is sampled on rank g % world only, and the chunk
+ * partials are summed across ranks with an NCCL all-reduce before the ordered combine.  Each
+ * chunk is non-zero on exactly one rank, so the sums are exact: results are bit-for-bit those
+ * of one GPU, on every rank (hence identical driver decisions everywhere).
+ *   expmc_nccl_unique_id      on one rank; broadcast the 128 bytes to the others
+ *   expmc_ctx_shard_samples   collective: ncclCommInitRank + enable sharding
+ *   expmc_ctx_set_shard       the chunk filter alone, no exchange (single-GPU emulation, tests)
+ *   expmc_ctx_last_partials   the last sampler window's chunk partials (for the emulation) */
+#define EXPMC_NCCL_ID_BYTES 128
+int expmc_nccl_unique_id(uint8_t* id);
+int expmc_ctx_shard_samples(expmc_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world);
+int expmc_ctx_set_shard(expmc_ctx* ctx, int32_t rank, int32_t world);
+int expmc_ctx_last_partials(const expmc_ctx* ctx, int64_t* count, double* sum, double* sum_sq, uint64_t* cost,
+                            uint64_t* jumps);
 
 /* run_level (mlmc.hpp:86-88; run_level_ex mlmc.cpp:76-148), entry mode, ONE request.
  * Errors as the reference: level outside [0,62] or beta <= 0 -> EXPMC_EINVAL; entry outside

@@ -19,6 +19,7 @@ from .api import (  # noqa: F401
     OutOfRange,
     SparseMatrix,
     bench_gather,
+    nccl_unique_id,
     bias_estimate,
     device_count,
     initial_level,

@@ -52,7 +52,8 @@ class LevelRecordC(C.Structure):
 
 class CountersC(C.Structure):
     _fields_ = [("kernel_launches", _U64), ("sampler_launches", _U64), ("sampler_ms", _D), ("h2d_bytes", _U64),
-                ("d2h_bytes", _U64), ("samples", _U64), ("jumps", _U64), ("fine_steps", _U64), ("rounds", _U64)]
+                ("d2h_bytes", _U64), ("samples", _U64), ("jumps", _U64), ("fine_steps", _U64), ("rounds", _U64),
+                ("nccl_bytes", _U64)]
 
 
 # (name, restype, argtypes) -- every symbol declared in include/expmc_b200.h
@@ -72,6 +73,10 @@ SYMBOLS = [
     ("expmc_ctx_set_sampler", C.c_int, [_P, _I32]),
     ("expmc_ctx_get_sampler", C.c_int, [_P, C.POINTER(_I32)]),
     ("expmc_bench_gather", C.c_int, [C.c_int, _U64, _I32, _I32, C.POINTER(_D)]),
+    ("expmc_nccl_unique_id", C.c_int, [_P]),
+    ("expmc_ctx_shard_samples", C.c_int, [_P, _P, _I32, _I32]),
+    ("expmc_ctx_set_shard", C.c_int, [_P, _I32, _I32]),
+    ("expmc_ctx_last_partials", C.c_int, [_P, C.POINTER(_I64), _P, _P, _P, _P]),
     ("expmc_run_level", C.c_int, [_P, _I64, _D, _I32, _I32, _U64, _U64, _U64, C.POINTER(LevelStatsC)]),
     ("expmc_run_level_batch", C.c_int, [_P, _D, _U32, _I64, _P, _P]),
     ("expmc_sample_debug", C.c_int, [_P, _D, _U32, _I64, _P, _P, _P, _P, _P, _P]),

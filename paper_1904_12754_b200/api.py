@@ -282,6 +282,27 @@ class Context:
         _check(L.lib.expmc_ctx_get_counters(self._h, C.byref(c)))
         return {k: getattr(c, k) for k, _ in L.CountersC._fields_}
 
+    # ---- sample sharding over GPUs (one process per GPU)
+    def shard_samples(self, nccl_id: bytes, rank: int, world: int):
+        """Collective over the `world` ranks: every rank then samples the chunks g % world == rank
+        of every batch and the chunk partials are summed exactly over NCCL (results are bit-for-bit
+        one GPU's)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        _check(L.lib.expmc_ctx_shard_samples(self._h, C.cast(buf, C.c_void_p), rank, world))
+
+    def set_shard(self, rank: int, world: int):
+        """The chunk filter alone (no exchange): single-GPU emulation of a rank."""
+        _check(L.lib.expmc_ctx_set_shard(self._h, rank, world))
+
+    def last_partials(self) -> dict:
+        n = C.c_int64()
+        _check(L.lib.expmc_ctx_last_partials(self._h, C.byref(n), None, None, None, None))
+        k = n.value
+        s, s2 = np.empty(k), np.empty(k)
+        c, j = np.empty(k, np.uint64), np.empty(k, np.uint64)
+        _check(L.lib.expmc_ctx_last_partials(self._h, C.byref(n), _ptr(s), _ptr(s2), _ptr(c), _ptr(j)))
+        return dict(sum=s, sum_sq=s2, cost=c, jumps=j)
+
     @property
     def stream_ptr(self) -> int:
         """cudaStream_t the sampler kernels run on (for CUDA-event timing on that stream)."""
@@ -388,6 +409,13 @@ def mlmc_driver_rows(ctx: Context, beta: float, rows, row_seeds, options: MlmcOp
     _check(L.lib.expmc_mlmc_driver_rows(ctx.handle, beta, C.byref(o), rows.size, _ptr(rows), _ptr(seeds), _ptr(res),
                                         _ptr(lv), max_levels))
     return res, lv
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for Context.shard_samples (create on one rank, broadcast to the rest)."""
+    buf = (C.c_uint8 * 128)()
+    _check(L.lib.expmc_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
 
 
 def bench_gather(device: int, nbytes: int, loads_per_thread: int = 64, reps: int = 5) -> float:

@@ -41,7 +41,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     # the image exports CC/CXX pointing at a gcc wrapper; nvcc's host compiler is explicit
     ccbin = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
     cmd = [NVCC, *ARCH, *FLAGS, "-ccbin", ccbin, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[f"-D{d}" for d in defines], *[os.path.join(CSRC, s) for s in SOURCES], "-o", lib + ".tmp"]
+           *[f"-D{d}" for d in defines], *[os.path.join(CSRC, s) for s in SOURCES], "-ldl", "-o", lib + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = lib + ".build.log"
     with open(log, "w") as f:

@@ -4,6 +4,8 @@
 // expmc_run_level[_batch] <- run_level / run_level_ex (mlmc.hpp:86-88, mlmc.cpp:76-168)
 // expmc_sample_debug    <- LevelSampler::single / ::coupled per sample (paths.cpp:99-141)
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -41,8 +43,14 @@ struct expmc_ctx {
     uint64_t* h_chunk0 = nullptr;
     Partial* h_totals = nullptr;
     size_t cap_h = 0;
-    Partial* d_partials = nullptr;
+    double* d_pf = nullptr;          // chunk partials window: sum | sum_sq
+    unsigned long long* d_pu = nullptr;  //                    cost | jumps
     uint64_t cap_partials = 0;
+    uint64_t last_window = 0;
+    // sample sharding across GPUs (one process per GPU): chunk g is sampled on rank g % world
+    int shard_rank = 0;
+    int shard_world = 1;
+    ncclComm_t nccl = nullptr;
     unsigned* d_counter = nullptr;
     SampleOut* d_dbg = nullptr;
     size_t cap_dbg = 0;
@@ -110,6 +118,57 @@ void ensure_items(expmc_ctx* c, size_t nitems) {
 }
 
 void bind(const expmc_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+// NCCL is resolved at run time, only when sample sharding is requested: the process may already
+// hold a libnccl.so.2 (PyTorch ships its own), and a link-time dependency would bind whichever
+// copy the loader met first for everybody.  dlopen returns the already-loaded one if present.
+struct Nccl {
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const Nccl& nccl() {
+    static Nccl api = [] {
+        Nccl a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+        a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        return a;
+    }();
+    if (!api.all_reduce || !api.comm_init_rank || !api.get_unique_id)
+        throw Status(EXPMC_ECUDA, "libnccl.so.2 not loadable: sample sharding unavailable");
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw Status(EXPMC_ECUDA, std::string(what) + ": " + (nccl().error_string ? nccl().error_string(r) : "NCCL error"));
+}
+
+// Sum the window's chunk partials across the ranks.  Each chunk was sampled by exactly one
+// rank and is +0 on the others, so every element's sum is exact and rank-order independent:
+// the combined totals are bit-for-bit those of a single GPU.
+void nccl_allreduce_partials(ncclComm_t comm, const ChunkPartials& p, uint64_t w, uint64_t, cudaStream_t s) {
+    const Nccl& n = nccl();
+    nccl_check(n.group_start(), "ncclGroupStart");
+    nccl_check(n.all_reduce(p.sum, p.sum, w, ncclFloat64, ncclSum, comm, s), "ncclAllReduce");
+    nccl_check(n.all_reduce(p.sum_sq, p.sum_sq, w, ncclFloat64, ncclSum, comm, s), "ncclAllReduce");
+    nccl_check(n.all_reduce(p.cost, p.cost, w, ncclUint64, ncclSum, comm, s), "ncclAllReduce");
+    nccl_check(n.all_reduce(p.jumps, p.jumps, w, ncclUint64, ncclSum, comm, s), "ncclAllReduce");
+    nccl_check(n.group_end(), "ncclGroupEnd");
+}
 
 DevItem make_item(const expmc_level_req& r, double beta, uint32_t lane) {
     DevItem it{};
@@ -188,16 +247,26 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
                "H2D chunk0");
     c->ctr.h2d_bytes += nitems * sizeof(DevItem) + (nitems + 1) * sizeof(uint64_t);
     cuda_check(cudaMemsetAsync(c->d_totals, 0, nitems * sizeof(Partial), c->stream), "memset totals");
-    if (!c->d_partials) {
+    if (!c->d_pf) {
         c->cap_partials = kWindowChunks;
-        dev_alloc(&c->d_partials, c->cap_partials);
+        dev_alloc(&c->d_pf, 2 * c->cap_partials);
+        dev_alloc(&c->d_pu, 2 * c->cap_partials);
         dev_alloc(&c->d_counter, 1);
     }
+    const ChunkPartials cp{c->d_pf, c->d_pf + c->cap_partials, c->d_pu, c->d_pu + c->cap_partials};
+    const uint32_t world = static_cast<uint32_t>(c->shard_world);
     const int warps_per_block = sampler_threads() / 32;
     size_t nev = 0;
     for (uint64_t g0 = 0; g0 < total; g0 += c->cap_partials) {
         const uint64_t g1 = std::min(total, g0 + c->cap_partials);
+        const uint64_t w = g1 - g0;
         cuda_check(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), c->stream), "memset counter");
+        if (world > 1) {  // chunks sampled by the other ranks stay exactly zero here
+            cuda_check(cudaMemsetAsync(cp.sum, 0, w * sizeof(double), c->stream), "memset partials");
+            cuda_check(cudaMemsetAsync(cp.sum_sq, 0, w * sizeof(double), c->stream), "memset partials");
+            cuda_check(cudaMemsetAsync(cp.cost, 0, w * sizeof(uint64_t), c->stream), "memset partials");
+            cuda_check(cudaMemsetAsync(cp.jumps, 0, w * sizeof(uint64_t), c->stream), "memset partials");
+        }
         SamplerArgs a;
         a.rows = c->rows;
         a.edges = c->edges();
@@ -206,10 +275,13 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         a.nitems = static_cast<uint32_t>(nitems);
         a.g_begin = g0;
         a.g_end = g1;
-        a.partials = c->d_partials;
+        a.partials = cp;
         a.counter = c->d_counter;
-        const uint64_t want_blocks = (g1 - g0 + warps_per_block - 1) / warps_per_block;
-        const int grid = static_cast<int>(std::min<uint64_t>(c->sampler_grid, want_blocks));
+        a.shard_rank = static_cast<uint32_t>(c->shard_rank);
+        a.shard_world = world;
+        const uint64_t own = (w + world - 1) / world;
+        const uint64_t want_blocks = (own + warps_per_block - 1) / warps_per_block;
+        const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(c->sampler_grid, want_blocks)));
         while (c->ev.size() < 2 * (nev + 1)) {
             cudaEvent_t e;
             cuda_check(cudaEventCreate(&e), "cudaEventCreate");
@@ -219,9 +291,14 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         launch_sampler(a, grid, c->sampler, c->stream);
         cuda_check(cudaEventRecord(c->ev[2 * nev + 1], c->stream), "event");
         ++nev;
-        launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, c->d_partials, c->d_totals, c->stream);
+        if (c->nccl) {  // exact cross-GPU sum of the window's chunk partials (one rank non-zero per chunk)
+            nccl_allreduce_partials(c->nccl, cp, w, c->cap_partials, c->stream);
+            c->ctr.nccl_bytes += 2 * w * (sizeof(double) + sizeof(uint64_t));
+        }
+        launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, c->d_totals, c->stream);
         c->ctr.kernel_launches += 2;
         c->ctr.sampler_launches += 1;
+        c->last_window = w;
     }
     cuda_check(cudaMemcpyAsync(c->h_totals, c->d_totals, nitems * sizeof(Partial), cudaMemcpyDeviceToHost, c->stream),
                "D2H totals");
@@ -373,7 +450,9 @@ void expmc_ctx_destroy(expmc_ctx* c) {
     cudaFree(c->d_items);
     cudaFree(c->d_chunk0);
     cudaFree(c->d_totals);
-    cudaFree(c->d_partials);
+    cudaFree(c->d_pf);
+    cudaFree(c->d_pu);
+    if (c->nccl) nccl().comm_destroy(c->nccl);
     cudaFree(c->d_counter);
     cudaFree(c->d_dbg);
     cudaFreeHost(c->h_items);
@@ -463,6 +542,60 @@ int expmc_ctx_get_sampler(const expmc_ctx* c, int32_t* mode) {
     return guarded([&] {
         need(c && mode, EXPMC_EINVAL, "null argument");
         *mode = c->sampler;
+    });
+}
+
+int expmc_nccl_unique_id(uint8_t* id) {
+    return guarded([&] {
+        need(id != nullptr, EXPMC_EINVAL, "null argument");
+        static_assert(sizeof(ncclUniqueId) == EXPMC_NCCL_ID_BYTES, "NCCL id size");
+        ncclUniqueId u;
+        nccl_check(nccl().get_unique_id(&u), "ncclGetUniqueId");
+        std::memcpy(id, &u, sizeof u);
+    });
+}
+
+int expmc_ctx_shard_samples(expmc_ctx* c, const uint8_t* id, int32_t rank, int32_t world) {
+    return guarded([&] {
+        need(c && id, EXPMC_EINVAL, "null argument");
+        need(world >= 1 && rank >= 0 && rank < world, EXPMC_EINVAL, "bad rank / world");
+        bind(c);
+        if (c->nccl) {
+            nccl().comm_destroy(c->nccl);
+            c->nccl = nullptr;
+        }
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof u);
+        nccl_check(nccl().comm_init_rank(&c->nccl, world, u, rank), "ncclCommInitRank");
+        c->shard_rank = rank;
+        c->shard_world = world;
+    });
+}
+
+int expmc_ctx_set_shard(expmc_ctx* c, int32_t rank, int32_t world) {
+    return guarded([&] {
+        need(c != nullptr, EXPMC_EINVAL, "null context");
+        need(world >= 1 && rank >= 0 && rank < world, EXPMC_EINVAL, "bad rank / world");
+        need(c->nccl == nullptr || world == c->shard_world, EXPMC_EINVAL, "context is attached to an NCCL group");
+        c->shard_rank = rank;
+        c->shard_world = world;
+    });
+}
+
+int expmc_ctx_last_partials(const expmc_ctx* c, int64_t* count, double* sum, double* sum_sq, uint64_t* cost,
+                            uint64_t* jumps) {
+    return guarded([&] {
+        need(c && count, EXPMC_EINVAL, "null argument");
+        bind(c);
+        const uint64_t w = c->last_window;
+        *count = static_cast<int64_t>(w);
+        if (w == 0) return;
+        cudaError_t e = cudaSuccess;
+        if (sum) e = cudaMemcpy(sum, c->d_pf, w * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && sum_sq) e = cudaMemcpy(sum_sq, c->d_pf + c->cap_partials, w * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && cost) e = cudaMemcpy(cost, c->d_pu, w * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && jumps) e = cudaMemcpy(jumps, c->d_pu + c->cap_partials, w * 8, cudaMemcpyDeviceToHost);
+        cuda_check(e, "copy partials");
     });
 }
 

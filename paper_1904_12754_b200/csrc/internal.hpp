@@ -63,6 +63,16 @@ struct alignas(16) Partial {
     unsigned long long jumps;
 };
 
+// Chunk partials of one sampler window, structure of arrays so that a sample-sharded run can
+// sum them across GPUs with two all-reduces (fp64 sums, u64 counts).  Every chunk is sampled
+// by exactly one rank and is zero elsewhere, so the cross-rank sum is exact (x + 0 = x).
+struct ChunkPartials {
+    double* sum;     // [W]
+    double* sum_sq;  // [W]  (contiguous after sum)
+    unsigned long long* cost;   // [W]
+    unsigned long long* jumps;  // [W]  (contiguous after cost)
+};
+
 // Per-sample debug output.
 struct SampleOut {
     double fine;
@@ -89,13 +99,15 @@ struct SamplerArgs {
     const uint64_t* chunk0;  // nitems + 1, exclusive prefix of chunk counts
     uint32_t nitems;
     uint64_t g_begin, g_end;  // global chunk window of this launch
-    Partial* partials;        // [g_end - g_begin]
+    ChunkPartials partials;   // [g_end - g_begin] each
     unsigned int* counter;    // dynamic chunk counter, zeroed before launch
+    uint32_t shard_rank;      // sample sharding: this launch samples the chunks g with
+    uint32_t shard_world;     //   g % shard_world == shard_rank (the others stay zero)
 };
 
 void launch_sampler(const SamplerArgs& a, int grid, int mode, cudaStream_t s);
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
-                    const Partial* partials, Partial* totals, cudaStream_t s);
+                    const ChunkPartials& partials, Partial* totals, cudaStream_t s);
 void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n,
                   SampleOut* out, int mode, cudaStream_t s);
 int sampler_blocks_per_sm(int mode);

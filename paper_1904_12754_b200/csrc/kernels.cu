@@ -65,11 +65,14 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
     __shared__ ItemConst s_ic[kWarps];  // per-warp item constants: read at use, not held in registers
     ItemConst& ic = s_ic[threadIdx.x >> 5];
     uint32_t hint = 0;
+    // sample sharding: this GPU owns the chunks g = own0 + k * world of the window
+    const uint64_t rem = a.g_begin % a.shard_world;
+    const uint64_t own0 = a.g_begin + (a.shard_rank + a.shard_world - rem) % a.shard_world;
     for (;;) {
         uint32_t gi = 0;
         if (lane == 0) gi = atomicAdd(a.counter, 1u);
         gi = __shfl_sync(full, gi, 0);
-        const uint64_t g = a.g_begin + gi;
+        const uint64_t g = own0 + static_cast<uint64_t>(gi) * a.shard_world;
         if (g >= a.g_end) return;
 
         const uint32_t item = find_item(a.chunk0, a.nitems, g, hint);
@@ -118,18 +121,17 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
             jumps += __shfl_xor_sync(full, jumps, o);
         }
         if (lane == 0) {
-            Partial p;
-            p.sum = sum;
-            p.sum_sq = sum_sq;
-            p.cost = cost;
-            p.jumps = jumps;
-            a.partials[g - a.g_begin] = p;
+            const uint64_t k = g - a.g_begin;
+            a.partials.sum[k] = sum;
+            a.partials.sum_sq[k] = sum_sq;
+            a.partials.cost[k] = cost;
+            a.partials.jumps[k] = jumps;
         }
     }
 }
 
 __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, uint64_t g_begin,
-                          uint64_t g_end, const Partial* __restrict__ partials, Partial* __restrict__ totals) {
+                          uint64_t g_end, ChunkPartials p, Partial* __restrict__ totals) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nitems) return;
     const uint64_t c0 = chunk0[i] > g_begin ? chunk0[i] : g_begin;
@@ -137,11 +139,11 @@ __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, 
     if (c0 >= c1) return;
     Partial t = totals[i];
     for (uint64_t g = c0; g < c1; ++g) {  // ascending chunk order (parallel.hpp:52)
-        const Partial p = partials[g - g_begin];
-        t.sum = __dadd_rn(t.sum, p.sum);
-        t.sum_sq = __dadd_rn(t.sum_sq, p.sum_sq);
-        t.cost += p.cost;
-        t.jumps += p.jumps;
+        const uint64_t k = g - g_begin;
+        t.sum = __dadd_rn(t.sum, p.sum[k]);
+        t.sum_sq = __dadd_rn(t.sum_sq, p.sum_sq[k]);
+        t.cost += p.cost[k];
+        t.jumps += p.jumps[k];
     }
     totals[i] = t;
 }
@@ -359,7 +361,7 @@ void launch_sampler(const SamplerArgs& a, int grid, int mode, cudaStream_t s) {
 }
 
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
-                    const Partial* partials, Partial* totals, cudaStream_t s) {
+                    const ChunkPartials& partials, Partial* totals, cudaStream_t s) {
     k_combine<<<grid_for(nitems, 256), 256, 0, s>>>(chunk0, nitems, g_begin, g_end, partials, totals);
     cuda_check(cudaGetLastError(), "k_combine launch");
 }
