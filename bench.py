@@ -172,10 +172,11 @@ def load_peaks():
 
 
 def load_traffic():
+    """DRAM bytes per k_sample launch from the committed ncu capture (profiles/ncu_traffic.json)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
         with open(path) as f:
-            return json.load(f)
+            return json.load(f).get("bytes_per_launch")
     return None
 
 
@@ -430,6 +431,8 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k_sample", "sampler_launches": ctr["sampler_launches"],
                          "kernel_ms": ctr["sampler_ms"], "step_share": ctr["sampler_ms"] / ms_local,
+                         "alg_bytes_per_launch": alg_bytes / max(1, ctr["sampler_launches"]),
+                         "traffic_source": "profiles/ncu_traffic.json (C2 main-round launch, ncu --set full)",
                          "alg_bytes": f"{ALG_BYTES_PER_JUMP} B/transition + {ALG_BYTES_PER_SAMPLE} B/sample",
                          "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
                          "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},
