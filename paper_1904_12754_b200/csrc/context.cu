@@ -11,6 +11,8 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -93,11 +95,46 @@ void dev_alloc(T** p, size_t count) {
     cuda_check(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
 }
 
+// Process-wide pool of pinned staging blocks.  Page-locking hundreds of MB (the C2 warm-up round
+// stages 5M requests) costs far more than the transfer, so blocks of destroyed contexts are kept
+// and handed to the next context that needs one at least as large.
+struct PinnedPool {
+    std::mutex m;
+    std::multimap<size_t, void*> free_blocks;
+};
+
+PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool;  // never destroyed: blocks live until process exit
+    return *p;
+}
+
+void* pinned_get(size_t bytes) {
+    {
+        PinnedPool& pool = pinned_pool();
+        std::lock_guard<std::mutex> g(pool.m);
+        auto it = pool.free_blocks.lower_bound(bytes);
+        if (it != pool.free_blocks.end() && it->first <= 2 * bytes + (size_t{64} << 20)) {
+            void* p = it->second;
+            pool.free_blocks.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cuda_check(cudaHostAlloc(&p, bytes, cudaHostAllocPortable), "cudaHostAlloc");
+    return p;
+}
+
+void pinned_put(void* p, size_t bytes) {
+    if (!p) return;
+    PinnedPool& pool = pinned_pool();
+    std::lock_guard<std::mutex> g(pool.m);
+    pool.free_blocks.emplace(bytes, p);
+}
+
 template <class T>
-void host_alloc(T** p, size_t count) {
-    if (*p) cudaFreeHost(*p);
-    *p = nullptr;
-    cuda_check(cudaMallocHost(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)), "cudaMallocHost");
+void host_alloc(T** p, size_t count, size_t old_count) {
+    pinned_put(*p, std::max<size_t>(old_count, 1) * sizeof(T));
+    *p = static_cast<T*>(pinned_get(std::max<size_t>(count, 1) * sizeof(T)));
 }
 
 void ensure_items(expmc_ctx* c, size_t nitems) {
@@ -110,9 +147,9 @@ void ensure_items(expmc_ctx* c, size_t nitems) {
     }
     if (nitems + 1 > c->cap_h) {
         const size_t cap = std::max<size_t>(nitems + 1, c->cap_h * 2);
-        host_alloc(&c->h_items, cap);
-        host_alloc(&c->h_chunk0, cap);
-        host_alloc(&c->h_totals, cap);
+        host_alloc(&c->h_items, cap, c->cap_h);
+        host_alloc(&c->h_chunk0, cap, c->cap_h);
+        host_alloc(&c->h_totals, cap, c->cap_h);
         c->cap_h = cap;
     }
 }
@@ -455,9 +492,11 @@ void expmc_ctx_destroy(expmc_ctx* c) {
     if (c->nccl) nccl().comm_destroy(c->nccl);
     cudaFree(c->d_counter);
     cudaFree(c->d_dbg);
-    cudaFreeHost(c->h_items);
-    cudaFreeHost(c->h_chunk0);
-    cudaFreeHost(c->h_totals);
+    if (c->cap_h) {  // staging blocks go back to the process-wide pool
+        pinned_put(c->h_items, c->cap_h * sizeof(DevItem));
+        pinned_put(c->h_chunk0, c->cap_h * sizeof(uint64_t));
+        pinned_put(c->h_totals, c->cap_h * sizeof(Partial));
+    }
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
