@@ -77,7 +77,7 @@ __device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const
     stream_reserve2(w.st);
     double tjump = INFINITY;
     if (w.cur.rate != 0.0) {
-        const double e = -fast_log(__dsub_rn(1.0, stream_pop(w.st)), s_log, c_log_poly);
+        const double e = -fast_log(__ull2double_rn((uint64_t{1} << 53) - stream_pop_bits(w.st)), -53, s_log, c_log_poly);
         tjump = __dadd_rn(w.t, fast_div(e, w.cur.rate));
     }
     if (!(tjump < ic.tend)) {  // holds to the end of the interval [0, beta]

@@ -23,7 +23,7 @@
 namespace expmc_b200 {
 
 // log1p polynomial of fast_log in constant memory: DFMA reads it as a c[] operand directly.
-__constant__ double c_log_poly[7] = EXPMC_LOG_POLY;
+__constant__ double c_log_poly[9] = EXPMC_LOG_POLY;
 __device__ const LogEntry g_log_table[128] = {
 #include "log_table.inc"
 };
@@ -49,8 +49,7 @@ __device__ __forceinline__ void stream_init(Stream& s, uint64_t seed, uint64_t s
     s.c2 = static_cast<uint32_t>(sample >> 32);
     s.c3 = key3;
     s.block = 0;
-    s.w0 = s.w1 = s.w2 = 0;
-    s.n = 0;
+    s.n = 0;  // w0..w2 are written before they are read
 }
 
 // Philox4x32 with 10 rounds and the Weyl key schedule (rng.hpp:44-62).
@@ -138,11 +137,24 @@ __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begi
     uint32_t k = 0;
     bool done = false;
     if (degf & kUniformRow) {
+#ifdef EXPMC_PICK_INT
         const uint64_t lo = k53 * deg;
         const uint64_t hi = __umul64hi(k53, static_cast<uint64_t>(deg));
         const uint64_t rem = lo & ((uint64_t{1} << 53) - 1);
         k = static_cast<uint32_t>((hi << 11) | (lo >> 53));
         done = rem >= deg && rem <= (uint64_t{1} << 53) - deg;
+#else
+        // t = fl(v deg) is within deg 2^-53 of v deg; a fractional part at least 2 deg 2^-53 away
+        // from 0 and 1 puts v deg at least deg 2^-53 from every integer: floor(t) is then the
+        // exact upper_bound and the boundary condition above holds.
+        const double dg = static_cast<double>(deg);
+        const double t = __dmul_rn(to_uniform(k53), dg);
+        const double fl = floor(t);
+        const double f = __dsub_rn(t, fl);
+        const double margin = __dmul_rn(dg, 0x1.0p-52);
+        k = static_cast<uint32_t>(fl);
+        done = f >= margin && f <= __dsub_rn(1.0, margin);
+#endif
     }
     if (!done) {
         const double v = to_uniform(k53);
@@ -215,8 +227,7 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
     w.remaining = ic.dt;
     w.acc_a = 0.0;
     w.acc_b = 0.0;
-    w.d0 = w.cur.d;
-    w.d1 = 0.0;
+    w.d0 = w.cur.d;  // d1 is written at the pair's middle node before it is read
     w.step = 0;
 }
 
@@ -231,11 +242,11 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
     stream_reserve2(w.st);  // the event's only Philox call site
     bool step_done = true;
     if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
-        const double u = stream_pop(w.st);
+        const uint64_t k53 = stream_pop_bits(w.st);
         ++draws;
-        // E = -log1p(-u), the event's only transcendental.  u = k 2^-53, so 1 - u is exact in
-        // fp64 and log(1 - u) is the same real number as log1p(-u) (fastmath.cuh: <= 1 ulp).
-        const double e = -fast_log(__dsub_rn(1.0, u), s_log, c_log_poly);
+        // E = -log1p(-u), the event's only transcendental.  u = K 2^-53, so 1 - u = (2^53 - K) 2^-53
+        // exactly and log(1 - u) is the same real number as log1p(-u) (fastmath.cuh: <= 1 ulp).
+        const double e = -fast_log(__ull2double_rn((uint64_t{1} << 53) - k53), -53, s_log, c_log_poly);
         if (e < __dmul_rn(w.cur.rate, w.remaining)) {  // == (u < q), see above
             w.remaining = __dsub_rn(w.remaining, fast_div(e, w.cur.rate));  // paths.cpp:54
             ++jumps;
