@@ -306,9 +306,13 @@ __device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& 
 // it (mlmc.cpp:103-108).  delta == 0 makes fine and coarse bitwise equal, so x = 0 exactly.
 __device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows) {
     if (!ic.base && w.acc_b == 0.0) return 0.0;
-    double fine, coarse;
-    walker_finish(w, ic, rows, fine, coarse);
-    return ic.base ? fine : __dsub_rn(fine, coarse);
+    // same values as walker_finish, with one exp call site shared by both modes
+    const double sg = static_cast<double>(w.sign);
+    const double u_end = __ldg(&rows[w.state].u);
+    const double ea = exp_or_one(w.acc_a);  // single: e^expo; coupled: e^coarse
+    if (ic.base) return __dmul_rn(__dmul_rn(sg, ea), u_end);
+    const double uf = __dmul_rn(sg, u_end);
+    return __dsub_rn(__dmul_rn(uf, exp(__dadd_rn(w.acc_a, w.acc_b))), __dmul_rn(uf, ea));
 }
 
 __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items, uint32_t i) {
