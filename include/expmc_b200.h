@@ -39,8 +39,12 @@ extern "C" {
 #define EXPMC_SAMPLER_REFERENCE 0
 #define EXPMC_SAMPLER_EVENT 1
 
-/* Sampling lanes of the reference's Philox key (mlmc.cpp:94-96). */
+/* Sampling lanes of the reference's Philox key (mlmc.cpp:94-96).  ENTRY estimates
+ * (e^{tA}u)_entry; FORWARD estimates sum_i (e^{tA}u)_i from paths started at a state drawn
+ * with probability u_i / sum(u) (SampleMode::forward, paths.cpp:12-36, 144-181) and runs on
+ * a context built from A^T (mlmc.hpp:47-49). */
 #define EXPMC_LANE_ENTRY 0u
+#define EXPMC_LANE_FORWARD 1u
 
 typedef struct expmc_ctx expmc_ctx;
 
@@ -192,8 +196,18 @@ int expmc_run_level(expmc_ctx* ctx, int64_t entry, double beta, int32_t level, i
                     uint64_t first_index, uint64_t additional, uint64_t seed,
                     expmc_level_stats* out);
 
+/* run_level in forward mode (mlmc.cpp:86, 112-120): ONE request on lane 1.  The context must
+ * hold A^T; its vector u is the initial distribution, with the reference's errors: a negative
+ * u_i -> EXPMC_EINVAL "forward sampling requires a nonnegative vector"; sum(u) <= 0 ->
+ * EXPMC_EINVAL "forward sampling requires sum(u) > 0" (make_initial_distribution,
+ * paths.cpp:12-28). */
+int expmc_run_level_forward(expmc_ctx* ctx, double beta, int32_t level, int32_t base_level,
+                            uint64_t first_index, uint64_t additional, uint64_t seed,
+                            expmc_level_stats* out);
+
 /* Batched run_level: nreq independent requests (any mix of rows/levels/ranges) in one GPU
- * pass; out[i] is bit-for-bit what expmc_run_level would return for req[i]. */
+ * pass; out[i] is bit-for-bit what expmc_run_level would return for req[i].  lane is
+ * EXPMC_LANE_ENTRY or EXPMC_LANE_FORWARD (req[i].entry ignored); others -> EXPMC_ENOTIMPL. */
 int expmc_run_level_batch(expmc_ctx* ctx, double beta, uint32_t lane, int64_t nreq,
                           const expmc_level_req* req, expmc_level_stats* out);
 
@@ -214,6 +228,14 @@ int expmc_mlmc_driver(expmc_ctx* ctx, int64_t entry, double beta, const expmc_op
 int expmc_mlmc_driver_rows(expmc_ctx* ctx, double beta, const expmc_options* options,
                            int64_t nrows, const int64_t* rows, const uint64_t* row_seed,
                            expmc_result* out, expmc_level_record* levels, int32_t max_levels);
+
+/* mlmc_driver in forward mode (MlmcProblem.mode = forward): nruns independent runs of the
+ * reference's driver on lane 1, run r seeded seeds[r] (seeds == NULL with nruns == 1: the
+ * reference's single call, seeded options->seed), advanced in lock-step batched rounds like
+ * expmc_mlmc_driver_rows.  levels: nruns x max_levels records (nullable). */
+int expmc_mlmc_driver_forward(expmc_ctx* ctx, double beta, const expmc_options* options, int64_t nruns,
+                              const uint64_t* seeds, expmc_result* out, expmc_level_record* levels,
+                              int32_t max_levels);
 
 /* Roofline denominator: random 32-B-sector gather throughput of `device` over a buffer of
  * `bytes` (L2-resident or HBM-sized), `loads_per_thread` independent sector loads per thread,

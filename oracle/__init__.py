@@ -101,6 +101,15 @@ class CSR:
         val = np.array([acc[k] for k in keys], np.float64)
         return CSR(n, rp, col, val)
 
+    def transpose(self) -> "CSR":
+        """A^T in canonical CSR (SparseMatrix::transpose; forward mode decomposes A^T,
+        mlmc.hpp:47-49)."""
+        rows = np.repeat(np.arange(self.n, dtype=np.int64), np.diff(self.row_ptr))
+        order = np.lexsort((rows, self.col))  # by new row (= old col), then new col (= old row)
+        rp = np.zeros(self.n + 1, np.int64)
+        np.add.at(rp, self.col + 1, 1)
+        return CSR(self.n, np.cumsum(rp).astype(np.int64), rows[order].copy(), self.val[order].copy())
+
 
 LEVEL_DT = np.dtype([("level", np.int32), ("pad", np.int32), ("sum", np.float64),
                      ("sum_sq", np.float64), ("samples", np.uint64), ("cost", np.uint64)])
@@ -286,6 +295,31 @@ class OracleChain(_Chain):
                      total_jumps=r.total_jumps, total_samples=r.total_samples, levels=lv[i, :r.nlevels].copy())
                 for i, r in enumerate(res)]
 
+    # ---- forward mode (lane 1): this chain must be the decomposition of A^T
+    def forward_samples(self, u, beta, level, base, seed, sample_idx):
+        r = self.samples(u, 0, beta, level, base, seed, sample_idx, lane=1)
+        return r
+
+    def forward_run_level(self, u, beta, level, base, first, count, seed, threads=1):
+        return self.run_level(u, 0, beta, level, base, first, count, seed, threads=threads, lane=1)
+
+    def forward_driver(self, u, beta, seeds=None, max_levels=40, **opt):
+        """One forward mlmc_driver run per seed (default: opt['seed'] or 0)."""
+        seeds = np.ascontiguousarray([opt.get("seed", 0)] if seeds is None else seeds, np.uint64)
+        u = np.ascontiguousarray(u, np.float64)
+        res = (_OrcResult * len(seeds))()
+        lv = np.zeros((len(seeds), max_levels), LEVEL_DT)
+        o = _options(**opt)
+        self.be._check(self.be.lib.orc_mlmc_driver_forward(self.h, _ptr(u), _D(beta), C.byref(o), _I64(len(seeds)),
+                                                           _ptr(seeds), res, _ptr(lv), C.c_int32(max_levels)))
+        return [dict(estimate=r.estimate, statistical_error=r.statistical_error, bias_estimate=r.bias_estimate,
+                     l0=r.l0, L=r.L, total_cost=r.total_cost, converged=bool(r.converged), nlevels=r.nlevels,
+                     total_jumps=r.total_jumps, total_samples=r.total_samples, levels=lv[i, :r.nlevels].copy())
+                for i, r in enumerate(res)]
+
+    def transposed(self) -> "OracleChain":
+        return OracleChain(self.be, self.a.transpose())
+
 
 class Reference(_Backend):
     kind = "reference"
@@ -400,6 +434,48 @@ class RefChain(_Chain):
                             l0=r.l0, L=r.L, total_cost=r.total_cost, converged=bool(r.converged), nlevels=r.nlevels,
                             total_jumps=jumps, total_samples=int(levels["samples"].sum()), levels=levels))
         return out
+
+    # ---- forward mode (SampleMode::forward): this chain must hold A^T
+    def forward_samples(self, u, beta, level, base, seed, sample_idx):
+        idx = np.ascontiguousarray(sample_idx, np.uint64)
+        k = len(idx)
+        u = np.ascontiguousarray(u, np.float64)
+        fine, coarse = np.empty(k), np.empty(k)
+        cost = np.empty(k, np.uint64)
+        self.be._check(self.be.lib.ref_forward_samples(self.h, _ptr(u), _D(beta), _INT(level), _INT(int(base)),
+                                                       _U64(seed), _I64(k), _ptr(idx), _ptr(fine), _ptr(coarse),
+                                                       _ptr(cost)))
+        return dict(fine=fine, coarse=coarse, cost=cost)
+
+    def forward_run_level(self, u, beta, level, base, first, count, seed, threads=1):
+        u = np.ascontiguousarray(u, np.float64)
+        s, s2 = _D(), _D()
+        m, c = _U64(), _U64()
+        self.be._check(self.be.lib.ref_forward_run_level(self.h, _ptr(u), _D(beta), _INT(level), _INT(int(base)),
+                                                         _U64(first), _U64(count), _U64(seed), _INT(threads),
+                                                         C.byref(s), C.byref(s2), C.byref(m), C.byref(c)))
+        return dict(sum=s.value, sum_sq=s2.value, samples=m.value, cost=c.value)
+
+    def forward_driver(self, u, beta, seeds=None, max_levels=40, **opt):
+        """One forward mlmc_driver run per seed (the reference takes options.seed)."""
+        seeds = [opt.pop("seed", 0)] if seeds is None else list(seeds)
+        u = np.ascontiguousarray(u, np.float64)
+        out = []
+        for sd in seeds:
+            res = _RefResult()
+            lv = np.zeros(max_levels, LEVEL_DT)
+            o = _options(seed=int(sd), **opt)
+            self.be._check(self.be.lib.ref_forward_driver(self.h, _ptr(u), _D(beta), C.byref(o), C.byref(res),
+                                                          _ptr(lv), C.c_int32(max_levels)))
+            out.append(dict(estimate=res.estimate, statistical_error=res.statistical_error,
+                            bias_estimate=res.bias_estimate, l0=res.l0, L=res.L, total_cost=res.total_cost,
+                            converged=bool(res.converged), nlevels=res.nlevels, levels=lv[:res.nlevels].copy()))
+        return out
+
+    def transposed(self) -> "RefChain":
+        h = C.c_void_p()
+        self.be._check(self.be.lib.ref_transpose(self.h, C.byref(h)))
+        return RefChain(self.be, None, handle=h)
 
     def dense_expmv(self, u, beta):
         u = np.ascontiguousarray(u, np.float64)

@@ -201,10 +201,62 @@ typedef struct {
     int64_t end_state;
 } orc_sample;
 
-/* LevelSampler::single, paths.cpp:99-114 (nojump_ from the ctor, paths.cpp:88-90) */
+/* make_initial_distribution, paths.cpp:12-28: forward mode's start-state CDF over u. */
+typedef struct {
+    double* cdf;
+    int64_t n;
+    double total;
+} orc_init;
+
+static int init_build(const double* u, int64_t n, orc_init* init) {
+    init->cdf = NULL;
+    init->n = n;
+    init->total = 0.0;
+    if (n <= 0) return fail(1, "forward sampling requires sum(u) > 0");
+    init->cdf = (double*)malloc((size_t)n * sizeof(double));
+    double total = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        if (u[j] < 0.0) {
+            free(init->cdf);
+            init->cdf = NULL;
+            return fail(1, "forward sampling requires a nonnegative vector");
+        }
+        total += u[j];
+        init->cdf[j] = total;
+    }
+    if (!(total > 0.0)) {
+        free(init->cdf);
+        init->cdf = NULL;
+        return fail(1, "forward sampling requires sum(u) > 0");
+    }
+    for (int64_t j = 0; j < n; ++j) init->cdf[j] /= total;
+    init->cdf[n - 1] = 1.0;
+    init->total = total;
+    return 0;
+}
+
+/* sample_initial, paths.cpp:32-36: upper_bound of one uniform in the CDF. */
+static int64_t sample_initial(const orc_init* init, orc_stream* s) {
+    const double v = orc_next_uniform(s);
+    int64_t lo = 0, count = init->n;
+    while (count > 0) {
+        const int64_t step = count / 2;
+        if (!(v < init->cdf[lo + step])) {
+            lo += step + 1;
+            count -= step + 1;
+        } else {
+            count = step;
+        }
+    }
+    return lo;
+}
+
+/* LevelSampler::single, paths.cpp:99-114 (nojump_ from the ctor, paths.cpp:88-90); with
+ * init != NULL LevelSampler::forward_single, paths.cpp:144-157 (start drawn from u, the
+ * terminal factor sum(u) instead of u[end]). */
 static orc_sample sample_single(const orc_chain* c, const double* u, int64_t entry, double dt,
-                                int64_t steps, orc_stream* s) {
-    int64_t state = entry;
+                                int64_t steps, orc_stream* s, const orc_init* init) {
+    int64_t state = init ? sample_initial(init, s) : entry;
     int sign = 1;
     uint64_t draws = 0, jumps = 0;
     double expo = 0.0;
@@ -215,7 +267,7 @@ static orc_sample sample_single(const orc_chain* c, const double* u, int64_t ent
         expo += dt * 0.5 * (c->d[s0] + c->d[state]);
     }
     orc_sample r;
-    r.fine = sign * exp(expo) * u[state];
+    r.fine = sign * exp(expo) * (init ? init->total : u[state]);
     r.coarse = 0.0;
     r.cost = draws + (uint64_t)steps;
     r.jumps = jumps;
@@ -223,10 +275,10 @@ static orc_sample sample_single(const orc_chain* c, const double* u, int64_t ent
     return r;
 }
 
-/* LevelSampler::coupled, paths.cpp:116-141 */
+/* LevelSampler::coupled, paths.cpp:116-141; forward_coupled with init, paths.cpp:159-181 */
 static orc_sample sample_coupled(const orc_chain* c, const double* u, int64_t entry, double dt,
-                                 int64_t steps, orc_stream* s) {
-    int64_t state = entry;
+                                 int64_t steps, orc_stream* s, const orc_init* init) {
+    int64_t state = init ? sample_initial(init, s) : entry;
     int sign = 1;
     uint64_t draws = 0, jumps = 0;
     double coarse = 0.0, delta = 0.0;
@@ -239,7 +291,7 @@ static orc_sample sample_coupled(const orc_chain* c, const double* u, int64_t en
         coarse += dt * (c->d[s0] + c->d[state]);
         delta += dt * (c->d[s1] - half_ends);
     }
-    const double uf = sign * u[state];
+    const double uf = sign * (init ? init->total : u[state]);
     orc_sample r;
     r.fine = uf * exp(coarse + delta);
     r.coarse = uf * exp(coarse);
@@ -259,22 +311,27 @@ int orc_samples(const orc_chain* c, const double* u, int64_t entry, double beta,
                 double* fine, double* coarse, uint64_t* cost, uint64_t* jumps, int64_t* end_state) {
     int rc = check_level(level);
     if (rc) return rc;
-    if (entry < 0 || entry >= c->n) return fail(2, "entry index outside matrix");
+    const int forward = lane == ORC_LANE_FORWARD;
+    if (!forward && (entry < 0 || entry >= c->n)) return fail(2, "entry index outside matrix");
     const int64_t steps = (int64_t)1 << level;
     const double dt = beta / (double)steps;
     if (!(dt > 0.0)) return fail(1, "step size must be positive");
     if (!base && steps % 2 != 0) return fail(1, "coupled sampling needs an even step count");
+    orc_init init = {NULL, 0, 0.0};
+    if (forward && (rc = init_build(u, c->n, &init))) return rc;
+    const orc_init* ip = forward ? &init : NULL;
     for (int64_t i = 0; i < count; ++i) {
         orc_stream s;
         orc_stream_init(&s, seed, (uint32_t)level, sample_idx[i], lane);
-        const orc_sample r = base ? sample_single(c, u, entry, dt, steps, &s)
-                                  : sample_coupled(c, u, entry, dt, steps, &s);
+        const orc_sample r = base ? sample_single(c, u, entry, dt, steps, &s, ip)
+                                  : sample_coupled(c, u, entry, dt, steps, &s, ip);
         fine[i] = r.fine;
         coarse[i] = r.coarse;
         cost[i] = r.cost;
         if (jumps) jumps[i] = r.jumps;
         if (end_state) end_state[i] = r.end_state;
     }
+    free(init.cdf);
     return 0;
 }
 
@@ -288,13 +345,17 @@ int orc_run_level(const orc_chain* c, const double* u, int64_t entry, double bet
                   int threads, orc_level_stats* out) {
     int rc = check_level(level);
     if (rc) return rc;
-    if (entry < 0 || entry >= c->n) return fail(2, "entry index outside matrix");
+    const int forward = lane == ORC_LANE_FORWARD;
+    if (!forward && (entry < 0 || entry >= c->n)) return fail(2, "entry index outside matrix");
     if (!(beta > 0.0)) return fail(1, "beta must be positive");
     const int64_t steps = (int64_t)1 << level;
     const double dt = beta / (double)steps;
     if (!base && steps % 2 != 0) return fail(1, "coupled sampling needs an even step count");
     memset(out, 0, sizeof *out);
     if (count == 0) return 0;
+    orc_init init = {NULL, 0, 0.0};
+    if (forward && (rc = init_build(u, c->n, &init))) return rc;  /* mlmc.cpp:86 */
+    const orc_init* ip = forward ? &init : NULL;
     const uint64_t first_chunk = first / ORC_CHUNK;
     const uint64_t last_chunk = (first + count - 1) / ORC_CHUNK;
     const int64_t nch = (int64_t)(last_chunk - first_chunk + 1);
@@ -312,10 +373,10 @@ int orc_run_level(const orc_chain* c, const double* u, int64_t entry, double bet
             double x;
             orc_sample r;
             if (base) {
-                r = sample_single(c, u, entry, dt, steps, &s);
+                r = sample_single(c, u, entry, dt, steps, &s, ip);
                 x = r.fine;
             } else {
-                r = sample_coupled(c, u, entry, dt, steps, &s);
+                r = sample_coupled(c, u, entry, dt, steps, &s, ip);
                 x = r.fine - r.coarse;
             }
             a.sum += x; /* SumAcc::add, parallel.hpp:64-69 */
@@ -334,6 +395,7 @@ int orc_run_level(const orc_chain* c, const double* u, int64_t entry, double bet
         out->samples += part[ci].samples;
     }
     free(part);
+    free(init.cdf);
     return 0;
 }
 
@@ -394,11 +456,11 @@ static double lvl_unit_cost(const lvl_t* l) {
 
 #define ORC_MAX_LEVELS 64
 
-/* mlmc_driver, mlmc.cpp:170-260, entry mode, one row at a time */
+/* mlmc_driver, mlmc.cpp:170-260, entry (lane 0) or forward (lane 1) mode, one run at a time */
 static int driver_one(const orc_chain* c, const double* u, int64_t entry, double beta,
-                      const orc_options* o, uint64_t seed, orc_result* res, orc_level_record* rec,
-                      int32_t max_levels) {
-    if (entry < 0 || entry >= c->n) return fail(2, "entry index outside matrix");
+                      const orc_options* o, uint64_t seed, uint32_t lane, orc_result* res,
+                      orc_level_record* rec, int32_t max_levels) {
+    if (lane != ORC_LANE_FORWARD && (entry < 0 || entry >= c->n)) return fail(2, "entry index outside matrix");
     if (!(beta > 0.0)) return fail(1, "beta must be positive");
     if (!(o->epsilon > 0.0)) return fail(1, "epsilon must be positive");
     int l0;
@@ -418,7 +480,7 @@ static int driver_one(const orc_chain* c, const double* u, int64_t entry, double
         orc_level_stats d_;                                                                \
         lvl_t* e_ = &lv[(level)-l0];                                                       \
         int rc_ = orc_run_level(c, u, entry, beta, (level), (level) == l0, e_->samples,     \
-                                (add), seed, 0u, o->threads, &d_);                         \
+                                (add), seed, lane, o->threads, &d_);                       \
         if (rc_) return rc_;                                                               \
         e_->sum += d_.sum;                                                                 \
         e_->sum_sq += d_.sum_sq;                                                           \
@@ -495,7 +557,18 @@ int orc_mlmc_driver_rows(const orc_chain* c, const double* u, double beta, const
                          int64_t nrows, const int64_t* rows, const uint64_t* row_seed,
                          orc_result* out, orc_level_record* levels, int32_t max_levels) {
     for (int64_t r = 0; r < nrows; ++r) {
-        int rc = driver_one(c, u, rows[r], beta, o, row_seed[r], &out[r],
+        int rc = driver_one(c, u, rows[r], beta, o, row_seed[r], ORC_LANE_ENTRY, &out[r],
+                            levels ? levels + r * max_levels : NULL, max_levels);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+int orc_mlmc_driver_forward(const orc_chain* c, const double* u, double beta, const orc_options* o,
+                            int64_t nruns, const uint64_t* seeds, orc_result* out,
+                            orc_level_record* levels, int32_t max_levels) {
+    for (int64_t r = 0; r < nruns; ++r) {
+        int rc = driver_one(c, u, 0, beta, o, seeds[r], ORC_LANE_FORWARD, &out[r],
                             levels ? levels + r * max_levels : NULL, max_levels);
         if (rc) return rc;
     }

@@ -57,6 +57,12 @@ void orc_chain_export(const orc_chain* c, double* d, double* rate, int64_t* row_
 int64_t orc_chain_n(const orc_chain* c);
 int64_t orc_chain_edges(const orc_chain* c);
 
+/* Sampling lanes (mlmc.cpp:94-96).  lane ORC_LANE_FORWARD selects forward mode
+ * (LevelSampler::forward_single/coupled, paths.cpp:144-181): entry is ignored, the start
+ * state is drawn from u / sum(u), and the chain must be the decomposition of A^T. */
+#define ORC_LANE_ENTRY 0u
+#define ORC_LANE_FORWARD 1u
+
 int orc_samples(const orc_chain* c, const double* u, int64_t entry, double beta, int level,
                 int base, uint64_t seed, uint32_t lane, int64_t count, const uint64_t* sample_idx,
                 double* fine, double* coarse, uint64_t* cost, uint64_t* jumps, int64_t* end_state);
@@ -108,6 +114,11 @@ typedef struct {
 int orc_mlmc_driver_rows(const orc_chain* c, const double* u, double beta, const orc_options* o,
                          int64_t nrows, const int64_t* rows, const uint64_t* row_seed,
                          orc_result* out, orc_level_record* levels, int32_t max_levels);
+
+/* mlmc_driver in forward mode: nruns independent runs, run r seeded seeds[r]. */
+int orc_mlmc_driver_forward(const orc_chain* c, const double* u, double beta, const orc_options* o,
+                            int64_t nruns, const uint64_t* seeds, orc_result* out,
+                            orc_level_record* levels, int32_t max_levels);
 
 int orc_initial_level(double beta, double d_max, int* out);
 int orc_optimal_allocation(int64_t n, const double* v, const double* c, double eps, uint64_t* out);

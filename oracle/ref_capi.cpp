@@ -254,6 +254,98 @@ int ref_mlmc_driver_rows(void* h, const double* u, double beta, const RefOptions
     });
 }
 
+// Forward mode (SampleMode::forward, mlmc.cpp:86,112-121; paths.cpp:12-36,143-181): the matrix
+// handle must hold A^T; stream lane 1.
+int ref_forward_samples(void* h, const double* u, double beta, int level, int base, uint64_t seed, int64_t count,
+                        const uint64_t* sample_idx, double* fine, double* coarse, uint64_t* cost) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        const index_t steps = index_t{1} << level;
+        const double dt = beta / static_cast<double>(steps);
+        const LevelSampler sampler(m->dec, dt, steps);
+        const InitialDistribution init =
+            make_initial_distribution(std::span<const double>(u, static_cast<std::size_t>(m->dec.n)));
+        for (int64_t i = 0; i < count; ++i) {
+            RngStream s = stream_for(seed, static_cast<uint32_t>(level), sample_idx[i], 1u);
+            if (base) {
+                const FunctionalSample f = sampler.forward_single(init, s);
+                fine[i] = f.value;
+                coarse[i] = 0.0;
+                cost[i] = f.cost;
+            } else {
+                const CoupledSample c = sampler.forward_coupled(init, s);
+                fine[i] = c.eta_fine;
+                coarse[i] = c.eta_coarse;
+                cost[i] = c.cost;
+            }
+        }
+    });
+}
+
+int ref_forward_run_level(void* h, const double* u, double beta, int level, int base, uint64_t first,
+                          uint64_t count, uint64_t seed, int threads, double* sum, double* sum_sq, uint64_t* samples,
+                          uint64_t* cost) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.beta = beta;
+        p.mode = SampleMode::forward;
+        const LevelStats st = run_level(p, level, base != 0, first, count, seed, threads);
+        *sum = st.sum;
+        *sum_sq = st.sum_sq;
+        *samples = st.samples;
+        *cost = st.cost;
+    });
+}
+
+int ref_forward_driver(void* h, const double* u, double beta, const RefOptions* o, RefResult* out,
+                       RefLevel* levels_out, int32_t max_levels) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.beta = beta;
+        p.mode = SampleMode::forward;
+        MlmcOptions opt;
+        opt.epsilon = o->epsilon;
+        opt.seed = o->seed;
+        opt.threads = o->threads;
+        opt.l0_override = o->l0_override;
+        opt.warmup = o->warmup;
+        opt.max_levels_above_l0 = o->max_levels_above_l0;
+        opt.max_iterations = o->max_iterations;
+        const MlmcResult res = mlmc_driver(p, opt);
+        out->estimate = res.estimate;
+        out->statistical_error = res.statistical_error;
+        out->bias_estimate = res.bias_estimate;
+        out->l0 = res.l0;
+        out->L = res.L;
+        out->total_cost = res.total_cost;
+        out->converged = res.converged ? 1 : 0;
+        out->nlevels = static_cast<int32_t>(res.levels.size());
+        for (std::size_t l = 0; levels_out && l < res.levels.size() && l < static_cast<std::size_t>(max_levels); ++l) {
+            levels_out[l].level = res.levels[l].level;
+            levels_out[l].pad = 0;
+            levels_out[l].sum = res.levels[l].sum;
+            levels_out[l].sum_sq = res.levels[l].sum_sq;
+            levels_out[l].samples = res.levels[l].samples;
+            levels_out[l].cost = res.levels[l].cost;
+        }
+    });
+}
+
+int ref_transpose(void* h, void** out) {
+    return guarded([&] {
+        auto* m = new RefMatrix;
+        m->a = static_cast<RefMatrix*>(h)->a.transposed();
+        m->dec = decompose(m->a);
+        *out = m;
+    });
+}
+
 int ref_initial_level(double beta, double d_max, int* out) {
     return guarded([&] { *out = initial_level(beta, d_max); });
 }

@@ -11,12 +11,15 @@ from .api import (  # noqa: F401
     DomainError,
     ExpmcError,
     InvalidArgument,
+    LANE_ENTRY,
+    LANE_FORWARD,
     LevelStats,
     MlmcOptions,
     MlmcProblem,
     MlmcResult,
     NotImplementedMode,
     OutOfRange,
+    SampleMode,
     SparseMatrix,
     bench_gather,
     nccl_unique_id,
@@ -24,6 +27,7 @@ from .api import (  # noqa: F401
     device_count,
     initial_level,
     mlmc_driver,
+    mlmc_driver_forward,
     mlmc_driver_rows,
     optimal_allocation,
     run_level,

@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("EXPMC_LIB") or os.path.join(_HERE, "_lib", "libexpmc_
 _I32, _I64, _U32, _U64, _D = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 
 EXPMC_OK, EXPMC_EINVAL, EXPMC_ERANGE, EXPMC_EDOMAIN, EXPMC_ECUDA, EXPMC_ENOTIMPL, EXPMC_EINTERNAL = 0, 1, 2, 3, 4, 5, 9
-LANE_ENTRY = 0
+LANE_ENTRY, LANE_FORWARD = 0, 1
 SAMPLER_REFERENCE, SAMPLER_EVENT = 0, 1
 
 
@@ -78,10 +78,12 @@ SYMBOLS = [
     ("expmc_ctx_set_shard", C.c_int, [_P, _I32, _I32]),
     ("expmc_ctx_last_partials", C.c_int, [_P, C.POINTER(_I64), _P, _P, _P, _P]),
     ("expmc_run_level", C.c_int, [_P, _I64, _D, _I32, _I32, _U64, _U64, _U64, C.POINTER(LevelStatsC)]),
+    ("expmc_run_level_forward", C.c_int, [_P, _D, _I32, _I32, _U64, _U64, _U64, C.POINTER(LevelStatsC)]),
     ("expmc_run_level_batch", C.c_int, [_P, _D, _U32, _I64, _P, _P]),
     ("expmc_sample_debug", C.c_int, [_P, _D, _U32, _I64, _P, _P, _P, _P, _P, _P]),
     ("expmc_mlmc_driver", C.c_int, [_P, _I64, _D, C.POINTER(OptionsC), C.POINTER(ResultC), _P, _I32]),
     ("expmc_mlmc_driver_rows", C.c_int, [_P, _D, C.POINTER(OptionsC), _I64, _P, _P, _P, _P, _I32]),
+    ("expmc_mlmc_driver_forward", C.c_int, [_P, _D, C.POINTER(OptionsC), _I64, _P, _P, _P, _I32]),
     ("expmc_gen_ba", C.c_int, [_I64, _I64, _U64, C.POINTER(_P)]),
     ("expmc_gen_rmat", C.c_int, [_I32, _I64, _D, _D, _D, _U64, C.POINTER(_P)]),
     ("expmc_gen_convdiff3d", C.c_int, [_I64, _D, _I32, C.POINTER(_P)]),

@@ -6,10 +6,12 @@ CUDA library through the C-ABI (include/expmc_b200.h).
     ---------------------------------------       -------------------------------------------
     SparseMatrix::from_triplets (sparse.cpp:12)   SparseMatrix.from_triplets
     decompose(A) (chain.cpp:75)                   Context(A, u, device)  (tables built on GPU)
-    MlmcProblem{dec, u, entry, beta} (mlmc.hpp:50) MlmcProblem(ctx, entry, beta)
+    MlmcProblem{dec, u, entry, beta, mode}         MlmcProblem(ctx, entry, beta, mode)
+      (mlmc.hpp:45-57; forward: dec of A^T)         (forward: Context(A.transpose(), u))
     run_level(p, l, base, first, add, seed)       run_level(p, l, base, first, add, seed)
     mlmc_driver(p, opts) (mlmc.cpp:170)           mlmc_driver(p, opts)
     --                                            mlmc_driver_rows(ctx, beta, rows, seeds, opts)
+    --                                            mlmc_driver_forward(ctx, beta, seeds, opts)
     initial_level / optimal_allocation /          initial_level / optimal_allocation /
       bias_estimate (mlmc.cpp:19-51)                bias_estimate (same host C++ as the driver)
 
@@ -20,11 +22,15 @@ CudaError.  There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import enum
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib as L
+
+
+LANE_ENTRY, LANE_FORWARD = L.LANE_ENTRY, L.LANE_FORWARD  # Philox lanes (mlmc.cpp:94-96)
 
 
 class ExpmcError(RuntimeError):
@@ -314,9 +320,11 @@ class Context:
         _check(L.lib.expmc_ctx_reset_counters(self._h))
 
     # ---- batched primitives
-    def run_level_batch(self, beta: float, entry, level, base_level, first_index, count, seed) -> np.ndarray:
+    def run_level_batch(self, beta: float, entry, level, base_level, first_index, count, seed,
+                        lane: int = L.LANE_ENTRY) -> np.ndarray:
         """Vectorised run_level: every argument broadcasts to the request count.  Returns a
-        structured array (sum, sum_sq, samples, cost, jumps)."""
+        structured array (sum, sum_sq, samples, cost, jumps).  lane=LANE_FORWARD: forward mode
+        (entry ignored)."""
         e, lv, b, f, c, s = np.broadcast_arrays(np.asarray(entry, np.int64), np.asarray(level, np.int32),
                                                 np.asarray(base_level, np.int32), np.asarray(first_index, np.uint64),
                                                 np.asarray(count, np.uint64), np.asarray(seed, np.uint64))
@@ -325,10 +333,10 @@ class Context:
         req["entry"], req["seed"], req["first_index"] = e.ravel(), s.ravel(), f.ravel()
         req["count"], req["level"], req["base_level"] = c.ravel(), lv.ravel(), b.ravel()
         out = np.zeros(k, _STATS_DT)
-        _check(L.lib.expmc_run_level_batch(self._h, beta, L.LANE_ENTRY, k, _ptr(req), _ptr(out)))
+        _check(L.lib.expmc_run_level_batch(self._h, beta, lane, k, _ptr(req), _ptr(out)))
         return out
 
-    def sample_debug(self, beta: float, entry, level, base_level, seed, sample_idx) -> dict:
+    def sample_debug(self, beta: float, entry, level, base_level, seed, sample_idx, lane: int = L.LANE_ENTRY) -> dict:
         e, lv, b, s, i = np.broadcast_arrays(np.asarray(entry, np.int64), np.asarray(level, np.int32),
                                              np.asarray(base_level, np.int32), np.asarray(seed, np.uint64),
                                              np.asarray(sample_idx, np.uint64))
@@ -338,7 +346,7 @@ class Context:
         req["count"], req["level"], req["base_level"] = 1, lv.ravel(), b.ravel()
         fine, coarse = np.empty(k), np.empty(k)
         cost, jumps, end = np.empty(k, np.uint64), np.empty(k, np.uint64), np.empty(k, np.int64)
-        _check(L.lib.expmc_sample_debug(self._h, beta, L.LANE_ENTRY, k, _ptr(req), _ptr(fine), _ptr(coarse),
+        _check(L.lib.expmc_sample_debug(self._h, beta, lane, k, _ptr(req), _ptr(fine), _ptr(coarse),
                                         _ptr(cost), _ptr(jumps), _ptr(end)))
         return dict(fine=fine, coarse=coarse, cost=cost, jumps=jumps, end_state=end)
 
@@ -359,21 +367,43 @@ assert _RESULT_DT.itemsize == C.sizeof(L.ResultC)
 assert LEVEL_RECORD_DT.itemsize == C.sizeof(L.LevelRecordC)
 
 
+class SampleMode(enum.IntEnum):
+    """mlmc.hpp:45.  fem is outside this build's scope and raises
+    NotImplementedMode."""
+
+    entry = 0
+    forward = 1
+    fem = 2
+
+
 @dataclass
 class MlmcProblem:
-    """mlmc.hpp:50-57, entry mode: the context carries dec and u."""
+    """mlmc.hpp:47-57: the context carries dec and u.  entry mode estimates (e^{beta A} u)_entry
+    on Context(A, u); forward mode estimates sum(e^{beta A} u) on Context(A^T, u)."""
 
     ctx: Context
     entry: int = 0
     beta: float = 1.0
+    mode: SampleMode = SampleMode.entry
+
+
+def _mode(problem: MlmcProblem) -> SampleMode:
+    m = SampleMode(problem.mode)
+    if m == SampleMode.fem:
+        raise NotImplementedMode("fem sampling (lane 2) is not built")
+    return m
 
 
 def run_level(problem: MlmcProblem, level: int, base_level: bool, first_index: int, additional: int,
               seed: int, threads: int = 0) -> LevelStats:
     """mlmc.hpp:86-88."""
     out = L.LevelStatsC()
-    _check(L.lib.expmc_run_level(problem.ctx.handle, problem.entry, problem.beta, level, int(bool(base_level)),
-                                 first_index, additional, seed, C.byref(out)))
+    if _mode(problem) == SampleMode.forward:
+        _check(L.lib.expmc_run_level_forward(problem.ctx.handle, problem.beta, level, int(bool(base_level)),
+                                             first_index, additional, seed, C.byref(out)))
+    else:
+        _check(L.lib.expmc_run_level(problem.ctx.handle, problem.entry, problem.beta, level, int(bool(base_level)),
+                                     first_index, additional, seed, C.byref(out)))
     return LevelStats(level, out.sum, out.sum_sq, out.samples, out.cost, out.jumps)
 
 
@@ -390,9 +420,27 @@ def mlmc_driver(problem: MlmcProblem, options: MlmcOptions = MlmcOptions(), max_
     res = np.zeros(1, _RESULT_DT)
     lv = np.zeros(max_levels, LEVEL_RECORD_DT)
     o = options._c()
-    _check(L.lib.expmc_mlmc_driver(problem.ctx.handle, problem.entry, problem.beta, C.byref(o),
-                                   C.cast(_ptr(res), C.POINTER(L.ResultC)), _ptr(lv), max_levels))
+    if _mode(problem) == SampleMode.forward:
+        _check(L.lib.expmc_mlmc_driver_forward(problem.ctx.handle, problem.beta, C.byref(o), 1, None, _ptr(res),
+                                               _ptr(lv), max_levels))
+    else:
+        _check(L.lib.expmc_mlmc_driver(problem.ctx.handle, problem.entry, problem.beta, C.byref(o),
+                                       C.cast(_ptr(res), C.POINTER(L.ResultC)), _ptr(lv), max_levels))
     return _result(res[0], lv[: int(res[0]["nlevels"])])
+
+
+def mlmc_driver_forward(ctx: Context, beta: float, seeds, options: MlmcOptions = MlmcOptions(),
+                        max_levels: int = 64, want_levels: bool = True):
+    """Forward-mode estimator of sum(e^{beta A} u) on Context(A^T, u): one reference
+    mlmc_driver decision sequence per seed, all runs batched on the GPU.  Returns (results
+    structured array, levels [nruns, max_levels] or None)."""
+    seeds = np.ascontiguousarray(seeds, np.uint64).ravel()
+    res = np.zeros(seeds.size, _RESULT_DT)
+    lv = np.zeros((seeds.size, max_levels), LEVEL_RECORD_DT) if want_levels else None
+    o = options._c()
+    _check(L.lib.expmc_mlmc_driver_forward(ctx.handle, beta, C.byref(o), seeds.size, _ptr(seeds), _ptr(res),
+                                           _ptr(lv), max_levels))
+    return res, lv
 
 
 def mlmc_driver_rows(ctx: Context, beta: float, rows, row_seeds, options: MlmcOptions = MlmcOptions(),

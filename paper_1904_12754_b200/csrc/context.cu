@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -54,6 +55,11 @@ struct expmc_ctx {
     int shard_world = 1;
     ncclComm_t nccl = nullptr;
     unsigned* d_counter = nullptr;
+    // forward mode: CDF of u and sum(u) (make_initial_distribution, paths.cpp:12-28), built on
+    // the first forward request and dropped by set_vector
+    double* d_init_cdf = nullptr;
+    double init_total = 0.0;
+    bool init_valid = false;
     SampleOut* d_dbg = nullptr;
     size_t cap_dbg = 0;
 
@@ -207,6 +213,42 @@ void nccl_allreduce_partials(ncclComm_t comm, const ChunkPartials& p, uint64_t w
     nccl_check(n.group_end(), "ncclGroupEnd");
 }
 
+// make_initial_distribution (paths.cpp:12-28) over the u held in the row records: the same
+// sequential running sum, division by the total and last entry pinned to 1, so the device
+// upper_bound sees the reference's CDF bit for bit.  Errors carry the reference's messages.
+void ensure_forward_init(expmc_ctx* c) {
+    if (c->init_valid) return;
+    need(c->n > 0, EXPMC_EINVAL, "forward sampling requires sum(u) > 0");
+    const size_t n = static_cast<size_t>(c->n);
+    std::vector<double> cdf(n);
+    cuda_check(cudaMemcpy2DAsync(cdf.data(), sizeof(double), reinterpret_cast<const char*>(c->rows) + offsetof(RowRec, u),
+                                 sizeof(RowRec), sizeof(double), n, cudaMemcpyDeviceToHost, c->stream),
+               "D2H u");
+    cuda_check(cudaStreamSynchronize(c->stream), "D2H u");
+    c->ctr.d2h_bytes += n * sizeof(double);
+    double total = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+        need(!(cdf[j] < 0.0), EXPMC_EINVAL, "forward sampling requires a nonnegative vector");
+        total += cdf[j];
+        cdf[j] = total;
+    }
+    need(total > 0.0, EXPMC_EINVAL, "forward sampling requires sum(u) > 0");
+    for (double& x : cdf) x /= total;
+    cdf.back() = 1.0;
+    if (!c->d_init_cdf) dev_alloc(&c->d_init_cdf, n);
+    cuda_check(cudaMemcpyAsync(c->d_init_cdf, cdf.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+               "H2D initial CDF");
+    cuda_check(cudaStreamSynchronize(c->stream), "H2D initial CDF");
+    c->ctr.h2d_bytes += n * sizeof(double);
+    c->init_total = total;
+    c->init_valid = true;
+}
+
+ForwardInit forward_init(const expmc_ctx* c) {
+    return c->init_valid ? ForwardInit{c->d_init_cdf, c->init_total, static_cast<uint32_t>(c->n)}
+                         : ForwardInit{nullptr, 0.0, 0u};
+}
+
 DevItem make_item(const expmc_level_req& r, double beta, uint32_t lane) {
     DevItem it{};
     const uint64_t steps = uint64_t{1} << r.level;
@@ -215,16 +257,18 @@ DevItem make_item(const expmc_level_req& r, double beta, uint32_t lane) {
     it.count = r.count;
     it.dt = beta / static_cast<double>(steps);  // mlmc.cpp:81
     it.nsteps = steps;
-    it.entry = static_cast<uint32_t>(r.entry);
+    it.entry = lane == EXPMC_LANE_FORWARD ? 0u : static_cast<uint32_t>(r.entry);
     it.key3 = (static_cast<uint32_t>(r.level) & 0xFFFFFFu) | (lane << 24);  // rng.hpp:29
     it.base = r.base_level ? 1u : 0u;
+    it.mode = lane;
     return it;
 }
 
 // validate_problem (mlmc.cpp:150-159) + run_level_ex's level check (mlmc.cpp:79) + the
 // coupled even-step check (paths.cpp:119).
-void validate_req(const expmc_ctx* c, const expmc_level_req& r, double beta) {
-    need(r.entry >= 0 && r.entry < c->n, EXPMC_ERANGE, "entry index outside matrix");
+// Forward requests carry no entry (the start state is drawn from u).
+void validate_req(const expmc_ctx* c, const expmc_level_req& r, double beta, uint32_t lane) {
+    if (lane != EXPMC_LANE_FORWARD) need(r.entry >= 0 && r.entry < c->n, EXPMC_ERANGE, "entry index outside matrix");
     need(beta > 0.0, EXPMC_EINVAL, "beta must be positive");
     need(r.level >= 0 && r.level <= 62, EXPMC_EINVAL, "level outside [0, 62]");
     need(beta / static_cast<double>(uint64_t{1} << r.level) > 0.0, EXPMC_EINVAL, "step size must be positive");
@@ -247,18 +291,20 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
     for (int64_t i = 0; i < nreq; ++i) {
         out[i] = expmc_level_stats{0.0, 0.0, 0, 0, 0};
         try {
-            validate_req(c, req[i], beta);
+            validate_req(c, req[i], beta, lane);
         } catch (const Status&) {
             bad = std::min(bad, i);
         }
     }
-    if (bad < nreq) validate_req(c, req[bad], beta);  // rethrows with the right code
+    if (bad < nreq) validate_req(c, req[bad], beta, lane);  // rethrows with the right code
     std::vector<int64_t> slot;  // request index of each item (count > 0)
     slot.reserve(static_cast<size_t>(nreq));
     for (int64_t i = 0; i < nreq; ++i)
         if (req[i].count > 0) slot.push_back(i);
     const size_t nitems = slot.size();
     if (nitems == 0) return;
+    const bool forward = lane == EXPMC_LANE_FORWARD;
+    if (forward) ensure_forward_init(c);  // run_level builds it before sampling (mlmc.cpp)
     c->ctr.rounds += 1;
     need(nitems < (size_t{1} << 31), EXPMC_EINVAL, "too many run_level requests in one batch");
     ensure_items(c, nitems);
@@ -316,6 +362,7 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         a.counter = c->d_counter;
         a.shard_rank = static_cast<uint32_t>(c->shard_rank);
         a.shard_world = world;
+        a.init = forward_init(c);
         const uint64_t own = (w + world - 1) / world;
         const uint64_t want_blocks = (own + warps_per_block - 1) / warps_per_block;
         const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(c->sampler_grid, want_blocks)));
@@ -325,7 +372,7 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
             c->ev.push_back(e);
         }
         cuda_check(cudaEventRecord(c->ev[2 * nev], c->stream), "event");
-        launch_sampler(a, grid, c->sampler, c->stream);
+        launch_sampler(a, grid, c->sampler, forward, c->stream);
         cuda_check(cudaEventRecord(c->ev[2 * nev + 1], c->stream), "event");
         ++nev;
         if (c->nccl) {  // exact cross-GPU sum of the window's chunk partials (one rank non-zero per chunk)
@@ -491,6 +538,7 @@ void expmc_ctx_destroy(expmc_ctx* c) {
     cudaFree(c->d_pu);
     if (c->nccl) nccl().comm_destroy(c->nccl);
     cudaFree(c->d_counter);
+    cudaFree(c->d_init_cdf);
     cudaFree(c->d_dbg);
     if (c->cap_h) {  // staging blocks go back to the process-wide pool
         pinned_put(c->h_items, c->cap_h * sizeof(DevItem));
@@ -528,6 +576,7 @@ int expmc_ctx_set_vector(expmc_ctx* c, const double* u) {
         c->ctr.kernel_launches += 1;
         cudaError_t e = cudaStreamSynchronize(c->stream);
         cudaFree(d_u);
+        c->init_valid = false;  // the forward CDF follows u
         cuda_check(e, "set vector");
     });
 }
@@ -673,11 +722,21 @@ int expmc_run_level(expmc_ctx* c, int64_t entry, double beta, int32_t level, int
     });
 }
 
+int expmc_run_level_forward(expmc_ctx* c, double beta, int32_t level, int32_t base_level, uint64_t first_index,
+                            uint64_t additional, uint64_t seed, expmc_level_stats* out) {
+    return guarded([&] {
+        need(c && out, EXPMC_EINVAL, "null argument");
+        expmc_level_req r{0, seed, first_index, additional, level, base_level};
+        run_level_batch(c, beta, EXPMC_LANE_FORWARD, &r, 1, out);
+    });
+}
+
 int expmc_run_level_batch(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, const expmc_level_req* req,
                           expmc_level_stats* out) {
     return guarded([&] {
         need(c && (nreq == 0 || (req && out)), EXPMC_EINVAL, "null argument");
-        need(lane == EXPMC_LANE_ENTRY, EXPMC_ENOTIMPL, "only entry-mode sampling (lane 0) is built");
+        need(lane == EXPMC_LANE_ENTRY || lane == EXPMC_LANE_FORWARD, EXPMC_ENOTIMPL,
+             "only entry (lane 0) and forward (lane 1) sampling are built");
         run_level_batch(c, beta, lane, req, nreq, out);
     });
 }
@@ -686,16 +745,19 @@ int expmc_sample_debug(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, c
                        double* eta_fine, double* eta_coarse, uint64_t* cost, uint64_t* jumps, int64_t* end_state) {
     return guarded([&] {
         need(c && (nreq == 0 || req), EXPMC_EINVAL, "null argument");
-        need(lane == EXPMC_LANE_ENTRY, EXPMC_ENOTIMPL, "only entry-mode sampling (lane 0) is built");
+        need(lane == EXPMC_LANE_ENTRY || lane == EXPMC_LANE_FORWARD, EXPMC_ENOTIMPL,
+             "only entry (lane 0) and forward (lane 1) sampling are built");
         if (nreq == 0) return;
         bind(c);
         std::vector<DevItem> items(static_cast<size_t>(nreq));
         for (int64_t i = 0; i < nreq; ++i) {
             expmc_level_req r = req[i];
             r.count = 1;
-            validate_req(c, r, beta);
+            validate_req(c, r, beta, lane);
             items[i] = make_item(r, beta, lane);
         }
+        const bool forward = lane == EXPMC_LANE_FORWARD;
+        if (forward) ensure_forward_init(c);
         ensure_items(c, static_cast<size_t>(nreq));
         if (static_cast<size_t>(nreq) > c->cap_dbg) {
             dev_alloc(&c->d_dbg, nreq);
@@ -703,7 +765,8 @@ int expmc_sample_debug(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, c
         }
         cuda_check(cudaMemcpyAsync(c->d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
                    "H2D");
-        launch_debug(c->rows, c->edges(), c->d_items, static_cast<uint32_t>(nreq), c->d_dbg, c->sampler, c->stream);
+        launch_debug(c->rows, c->edges(), c->d_items, static_cast<uint32_t>(nreq), forward_init(c), c->d_dbg, c->sampler,
+                     forward, c->stream);
         c->ctr.kernel_launches += 1;
         std::vector<SampleOut> o(static_cast<size_t>(nreq));
         cuda_check(cudaMemcpyAsync(o.data(), c->d_dbg, nreq * sizeof(SampleOut), cudaMemcpyDeviceToHost, c->stream),

@@ -153,11 +153,14 @@ void advance(RowState& r, const DriverConfig& cfg, std::vector<double>& v, std::
     }
 }
 
+// rows == nullptr: forward mode (lane 1), each "row" an independent run of the functional
+// sum(e^{tA} u) with its own seed; validate_problem skips the entry check (mlmc.cpp:154).
 void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t nrows, const int64_t* rows,
                 const uint64_t* row_seed, expmc_result* out, expmc_level_record* levels, int32_t max_levels) {
     expmc_ctx_info info{};
     if (expmc_ctx_get_info(ctx, &info) != EXPMC_OK) throw Status(EXPMC_EINVAL, "null context");
-    for (int64_t r = 0; r < nrows; ++r)  // validate_problem, mlmc.cpp:150-159
+    const uint32_t lane = rows ? EXPMC_LANE_ENTRY : EXPMC_LANE_FORWARD;
+    for (int64_t r = 0; rows && r < nrows; ++r)  // validate_problem, mlmc.cpp:150-159
         if (rows[r] < 0 || rows[r] >= info.n) throw Status(EXPMC_ERANGE, "entry index outside matrix");
     if (!(beta > 0.0)) throw Status(EXPMC_EINVAL, "beta must be positive");
     if (!(opt.epsilon > 0.0)) throw Status(EXPMC_EINVAL, "epsilon must be positive");
@@ -169,7 +172,7 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
 #pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < nrows; ++r) {
         RowState& s = st[static_cast<size_t>(r)];
-        s.entry = rows[r];
+        s.entry = rows ? rows[r] : 0;
         s.seed = row_seed[r];
         s.l0 = l0;
         s.cap = cap;
@@ -208,7 +211,7 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
             }
         }
         const auto t1 = clk::now();
-        run_level_batch(ctx, beta, EXPMC_LANE_ENTRY, req.data(), static_cast<int64_t>(req.size()), res.data());
+        run_level_batch(ctx, beta, lane, req.data(), static_cast<int64_t>(req.size()), res.data());
         const auto t2 = clk::now();
         keep.assign(na, 0);
         int err_code = 0;
@@ -326,6 +329,20 @@ int expmc_mlmc_driver(expmc_ctx* ctx, int64_t entry, double beta, const expmc_op
         if (!ctx || !opt || !out) throw Status(EXPMC_EINVAL, "null argument");
         const uint64_t seed = opt->seed;
         drive_rows(ctx, beta, *opt, 1, &entry, &seed, out, levels, max_levels);
+    });
+}
+
+int expmc_mlmc_driver_forward(expmc_ctx* ctx, double beta, const expmc_options* opt, int64_t nruns,
+                              const uint64_t* seeds, expmc_result* out, expmc_level_record* levels,
+                              int32_t max_levels) {
+    return guarded([&] {
+        if (!ctx || !opt || (nruns > 0 && !out)) throw Status(EXPMC_EINVAL, "null argument");
+        const uint64_t one = opt->seed;
+        if (!seeds) {
+            if (nruns != 1) throw Status(EXPMC_EINVAL, "null argument");
+            seeds = &one;
+        }
+        drive_rows(ctx, beta, *opt, nruns, nullptr, seeds, out, levels, max_levels);
     });
 }
 

@@ -36,11 +36,13 @@ struct EdWalker {
     double dfirst;
 };
 
-__device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+template <bool F>
+__device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
                                          uint64_t sample) {
     stream_init(w.st, ic.seed, sample, ic.key3);
-    w.cur = load_row(rows, ic.entry);
-    w.state = ic.entry;
+    const uint32_t s0 = draw_start<F>(w.st, ic, fi);
+    w.cur = load_row(rows, s0);
+    w.state = s0;
     w.sign = 1;
     w.dconst = 1u;
     w.kcur = 0;
@@ -103,10 +105,11 @@ __device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const
     return false;
 }
 
-__device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+template <bool F>
+__device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
                                           double& fine, double& coarse) {
     const double sg = static_cast<double>(w.sign);
-    const double u_end = __ldg(&rows[w.state].u);
+    const double u_end = terminal_factor<F>(ic, fi, rows, w.state);
     const double h = __dmul_rn(0.5, ic.dt);
     if (ic.base) {
         const double expo = __dmul_rn(h, w.acc_a);
@@ -121,47 +124,50 @@ __device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic
     }
 }
 
-__device__ __forceinline__ double ed_sample(const EdWalker& w, const ItemConst& ic, const RowRec* __restrict__ rows) {
+template <bool F>
+__device__ __forceinline__ double ed_sample(const EdWalker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows) {
     if (!ic.base && w.dconst) return 0.0;
     double fine, coarse;
-    ed_finish(w, ic, rows, fine, coarse);
+    ed_finish<F>(w, ic, fi, rows, fine, coarse);
     return ic.base ? fine : __dsub_rn(fine, coarse);
 }
 
-// ---- policies the chunk kernel is templated on
+// ---- policies the chunk kernel is templated on (F: forward mode, lane 1)
+template <bool F>
 struct RefPolicy {
     using W = Walker;
-    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const RowRec* rows, uint64_t s) {
-        walker_start(w, ic, rows, s);
+    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows, uint64_t s) {
+        walker_start<F>(w, ic, fi, rows, s);
     }
     static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const RowRec* rows, const EdgeTables& e,
                                                  const LogEntry* lg, unsigned long long& dr, unsigned long long& j) {
         return walker_event(w, ic, rows, e, lg, dr, j);
     }
-    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const RowRec* rows) {
-        return walker_sample(w, ic, rows);
+    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows) {
+        return walker_sample<F>(w, ic, fi, rows);
     }
-    static __device__ __forceinline__ void finish(const W& w, const ItemConst& ic, const RowRec* rows, double& f,
+    static __device__ __forceinline__ void finish(const W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows, double& f,
                                                   double& c) {
-        walker_finish(w, ic, rows, f, c);
+        walker_finish<F>(w, ic, fi, rows, f, c);
     }
 };
 
+template <bool F>
 struct EdPolicy {
     using W = EdWalker;
-    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const RowRec* rows, uint64_t s) {
-        ed_start(w, ic, rows, s);
+    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows, uint64_t s) {
+        ed_start<F>(w, ic, fi, rows, s);
     }
     static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const RowRec* rows, const EdgeTables& e,
                                                  const LogEntry* lg, unsigned long long& dr, unsigned long long& j) {
         return ed_event(w, ic, rows, e, lg, dr, j);
     }
-    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const RowRec* rows) {
-        return ed_sample(w, ic, rows);
+    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows) {
+        return ed_sample<F>(w, ic, fi, rows);
     }
-    static __device__ __forceinline__ void finish(const W& w, const ItemConst& ic, const RowRec* rows, double& f,
+    static __device__ __forceinline__ void finish(const W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows, double& f,
                                                   double& c) {
-        ed_finish(w, ic, rows, f, c);
+        ed_finish<F>(w, ic, fi, rows, f, c);
     }
 };
 

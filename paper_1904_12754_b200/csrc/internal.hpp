@@ -52,7 +52,14 @@ struct alignas(16) DevItem {
     uint32_t entry;
     uint32_t key3;    // (level & 0xFFFFFF) | lane << 24   (rng.hpp:29)
     uint32_t base;
-    uint32_t pad;
+    uint32_t mode;    // lane: 0 entry, 1 forward (the kernel instantiation is chosen per batch)
+};
+
+// Forward-mode initial distribution on the device (InitialDistribution, paths.hpp:310-315).
+struct ForwardInit {
+    const double* cdf;
+    double total;
+    uint32_t n;
 };
 
 // Per-chunk partial and per-item running total (SumAcc, parallel.hpp:57-78, + jumps).
@@ -100,16 +107,17 @@ struct SamplerArgs {
     uint32_t nitems;
     uint64_t g_begin, g_end;  // global chunk window of this launch
     ChunkPartials partials;   // [g_end - g_begin] each
+    ForwardInit init;
     unsigned int* counter;    // dynamic chunk counter, zeroed before launch
     uint32_t shard_rank;      // sample sharding: this launch samples the chunks g with
     uint32_t shard_world;     //   g % shard_world == shard_rank (the others stay zero)
 };
 
-void launch_sampler(const SamplerArgs& a, int grid, int mode, cudaStream_t s);
+void launch_sampler(const SamplerArgs& a, int grid, int mode, bool forward, cudaStream_t s);
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
                     const ChunkPartials& partials, Partial* totals, cudaStream_t s);
 void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n,
-                  SampleOut* out, int mode, cudaStream_t s);
+                  const ForwardInit& init, SampleOut* out, int mode, bool forward, cudaStream_t s);
 int sampler_blocks_per_sm(int mode);
 int sampler_threads();
 

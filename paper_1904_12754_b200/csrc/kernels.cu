@@ -99,14 +99,14 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
             if (!active) {
                 const uint32_t mine = next + __popc(need & lt_mask);
                 if (mine < cnt) {
-                    P::start(w, ic, a.rows, lo + mine);
+                    P::start(w, ic, a.init, a.rows, lo + mine);
                     active = true;
                 }
             }
             next += __popc(need);
             if (!__any_sync(full, active)) break;
             if (active && P::event(w, ic, a.rows, a.edges, s_log, cost, jumps)) {
-                const double x = P::sample(w, ic, a.rows);
+                const double x = P::sample(w, ic, a.init, a.rows);
                 sum = __dadd_rn(sum, x);
                 sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
                 cost += ic.nsteps;
@@ -150,7 +150,7 @@ __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, 
 
 template <class P>
 __global__ void k_debug(const RowRec* __restrict__ rows, EdgeTables edges,
-                        const DevItem* __restrict__ items, uint32_t n, SampleOut* __restrict__ out) {
+                        const DevItem* __restrict__ items, uint32_t n, ForwardInit init, SampleOut* __restrict__ out) {
     __shared__ LogEntry s_log[128];
     load_log_table(s_log);
     __syncthreads();
@@ -158,12 +158,12 @@ __global__ void k_debug(const RowRec* __restrict__ rows, EdgeTables edges,
     if (i >= n) return;
     const ItemConst ic = load_item(items, i);
     typename P::W w;
-    P::start(w, ic, rows, items[i].first);
+    P::start(w, ic, init, rows, items[i].first);
     unsigned long long draws = 0, jumps = 0;
     while (!P::event(w, ic, rows, edges, s_log, draws, jumps)) {
     }
     SampleOut o;
-    P::finish(w, ic, rows, o.fine, o.coarse);
+    P::finish(w, ic, init, rows, o.fine, o.coarse);
     o.cost = draws + ic.nsteps;
     o.jumps = jumps;
     o.end_state = w.state;
@@ -348,15 +348,22 @@ int sampler_threads() { return kThreads; }
 int sampler_blocks_per_sm(int mode) {
     int b = 0;
     if (mode == EXPMC_SAMPLER_EVENT)
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<EdPolicy>, kThreads, 0), "occupancy");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<EdPolicy<false>>, kThreads, 0), "occupancy");
     else
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<RefPolicy>, kThreads, 0), "occupancy");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<RefPolicy<false>>, kThreads, 0), "occupancy");
     return b > 0 ? b : 1;
 }
 
-void launch_sampler(const SamplerArgs& a, int grid, int mode, cudaStream_t s) {
-    if (mode == EXPMC_SAMPLER_EVENT) k_sample<EdPolicy><<<grid, kThreads, 0, s>>>(a);
-    else k_sample<RefPolicy><<<grid, kThreads, 0, s>>>(a);
+// Entry and forward mode are separate instantiations: a batch is one lane, and the entry-mode
+// kernel (the hot path) carries no trace of the forward start draw.
+void launch_sampler(const SamplerArgs& a, int grid, int mode, bool forward, cudaStream_t s) {
+    if (mode == EXPMC_SAMPLER_EVENT) {
+        if (forward) k_sample<EdPolicy<true>><<<grid, kThreads, 0, s>>>(a);
+        else k_sample<EdPolicy<false>><<<grid, kThreads, 0, s>>>(a);
+    } else {
+        if (forward) k_sample<RefPolicy<true>><<<grid, kThreads, 0, s>>>(a);
+        else k_sample<RefPolicy<false>><<<grid, kThreads, 0, s>>>(a);
+    }
     cuda_check(cudaGetLastError(), "k_sample launch");
 }
 
@@ -366,10 +373,16 @@ void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, u
     cuda_check(cudaGetLastError(), "k_combine launch");
 }
 
-void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n, SampleOut* out, int mode,
-                  cudaStream_t s) {
-    if (mode == EXPMC_SAMPLER_EVENT) k_debug<EdPolicy><<<grid_for(n, 128), 128, 0, s>>>(rows, edges, items, n, out);
-    else k_debug<RefPolicy><<<grid_for(n, 128), 128, 0, s>>>(rows, edges, items, n, out);
+void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n, const ForwardInit& init,
+                  SampleOut* out, int mode, bool forward, cudaStream_t s) {
+    const int g = grid_for(n, 128);
+    if (mode == EXPMC_SAMPLER_EVENT) {
+        if (forward) k_debug<EdPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+        else k_debug<EdPolicy<false>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+    } else {
+        if (forward) k_debug<RefPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+        else k_debug<RefPolicy<false>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+    }
     cuda_check(cudaGetLastError(), "k_debug launch");
 }
 

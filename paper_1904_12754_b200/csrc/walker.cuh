@@ -205,6 +205,34 @@ struct ItemConst {
     uint32_t base;
 };
 
+// sample_initial (paths.cpp:32-36): the path's first draw picks the start state by
+// upper_bound over the CDF of u -- an exact binary search over the same fp64 CDF.
+template <bool F>
+__device__ __forceinline__ uint32_t draw_start(Stream& st, const ItemConst& ic, const ForwardInit& fi) {
+    if (!F) return ic.entry;
+    stream_reserve2(st);
+    const double v = stream_pop(st);
+    uint32_t lo = 0, count = fi.n;
+    while (count > 0u) {
+        const uint32_t step = count >> 1;
+        const uint32_t it = lo + step;
+        if (!(v < __ldg(fi.cdf + it))) {
+            lo = it + 1u;
+            count -= step + 1u;
+        } else {
+            count = step;
+        }
+    }
+    return lo;
+}
+
+// The terminal factor: u[end] (entry mode, paths.cpp:112,138) or sum(u) (forward, 156,178).
+template <bool F>
+__device__ __forceinline__ double terminal_factor(const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
+                                                  uint32_t state) {
+    return F ? fi.total : __ldg(&rows[state].u);
+}
+
 struct Walker {
     Stream st;
     Row cur;               // row record of the current state
@@ -217,11 +245,13 @@ struct Walker {
     uint64_t step;         // completed fine steps
 };
 
-__device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+template <bool F>
+__device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
                                              uint64_t sample) {
     stream_init(w.st, ic.seed, sample, ic.key3);
-    w.cur = load_row(rows, ic.entry);  // L1-resident: every lane of the warp starts here
-    w.state = ic.entry;
+    const uint32_t s0 = draw_start<F>(w.st, ic, fi);
+    w.cur = load_row(rows, s0);  // entry mode: L1-resident, every lane of the warp starts here
+    w.state = s0;
     w.sign = 1;
     w.half = 0;
     w.remaining = ic.dt;
@@ -288,10 +318,11 @@ __device__ __forceinline__ double exp_or_one(double x) { return x == 0.0 ? 1.0 :
 
 // Terminal values: single -> (sign * e^expo) * u[end] (paths.cpp:112);
 // coupled -> uf = sign * u[end]; (uf e^{coarse+delta}, uf e^{coarse}) (paths.cpp:138-140).
-__device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+template <bool F>
+__device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
                                               double& fine, double& coarse) {
     const double sg = static_cast<double>(w.sign);
-    const double u_end = __ldg(&rows[w.state].u);  // same sector as the last row record read
+    const double u_end = terminal_factor<F>(ic, fi, rows, w.state);  // same sector as the last row record read
     if (ic.base) {
         fine = __dmul_rn(__dmul_rn(sg, exp_or_one(w.acc_a)), u_end);
         coarse = 0.0;
@@ -304,11 +335,12 @@ __device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& 
 
 // The level-statistics sample x = P_l (base) or P_l - P_{l-1} (coupled), as run_level_ex adds
 // it (mlmc.cpp:103-108).  delta == 0 makes fine and coarse bitwise equal, so x = 0 exactly.
-__device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows) {
+template <bool F>
+__device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows) {
     if (!ic.base && w.acc_b == 0.0) return 0.0;
     // same values as walker_finish, with one exp call site shared by both modes
     const double sg = static_cast<double>(w.sign);
-    const double u_end = __ldg(&rows[w.state].u);
+    const double u_end = terminal_factor<F>(ic, fi, rows, w.state);
     const double ea = exp_or_one(w.acc_a);  // single: e^expo; coupled: e^coarse
     if (ic.base) return __dmul_rn(__dmul_rn(sg, ea), u_end);
     const double uf = __dmul_rn(sg, u_end);

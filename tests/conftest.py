@@ -15,6 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.json")
+GOLDEN_FORWARD = os.path.join(ROOT, "tests", "golden", "golden_forward.json")
 
 
 def pytest_configure(config):
@@ -32,6 +33,12 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden():
     with open(GOLDEN) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def golden_forward():
+    with open(GOLDEN_FORWARD) as f:
         return json.load(f)
 
 

@@ -126,5 +126,70 @@ def main():
     print(path, os.path.getsize(path), "bytes")
 
 
+def forward():
+    """golden_forward.json: SampleMode::forward (paths.cpp:12-36, 144-181; mlmc.cpp:86, 112-120)
+    through the reference on A^T (the matrix stored is the one the context is built on)."""
+    ref = Reference()
+    out = {"generator": "tests/golden/make_golden.py forward() (reference: /root/reference/proj/core via oracle/_ref)"}
+    base = {
+        "k2": ref.chain(CSR.from_dense([[0.0, 1.0], [1.0, 0.0]])),             # test_paths.cpp:102
+        "signed3": ref.chain(CSR.from_dense([[0.1, -1.0, 0.5], [0.7, -0.2, -0.2], [-0.4, 0.0, 0.3]])),
+        "absorb3": ref.chain(CSR.from_dense([[0.0, 1.0, 0.5], [0.0, -1.0, 0.0], [0.25, 0.25, 0.0]])),
+        "grid8": ref.chain(grid(8)),
+        "smallw150": ref.smallw(150, 2, 0.15, 21),
+        "pref300": ref.pref(300, 3, 7),
+    }
+    rng = np.random.default_rng(1)
+    out["matrices"] = {}
+    for name, ch in base.items():
+        t = ch.transposed()
+        n = t.n
+        u = np.round(rng.uniform(0.0, 2.0, n), 6)
+        u[n // 3] = 0.0  # a zero-probability start state
+        dec = t.decomposition()
+        beta = 0.8 if name not in ("smallw150", "pref300") else 1.0 / dec["d_max"]
+        samples = []
+        for level in range(0, 5):
+            for b in ([1, 0] if level > 0 else [1]):
+                seed = 500 + 17 * level + b
+                idx = np.array(list(range(24)) + [511, 512, 2 ** 33 + 3, 2 ** 40 + 1], np.uint64)
+                s = t.forward_samples(u, beta, level, b, seed, idx)
+                samples.append(dict(level=level, base=b, seed=seed, idx=[int(x) for x in idx], fine=hx(s["fine"]),
+                                    coarse=hx(s["coarse"]), cost=[int(c) for c in s["cost"]]))
+        runs = []
+        for (level, b, first, count) in [(0, 1, 0, 1000), (1, 0, 37, 2500), (3, 0, 1000, 700), (4, 0, 0, 1)]:
+            seed = 91 + level
+            r = t.forward_run_level(u, beta, level, b, first, count, seed, threads=4)
+            runs.append(dict(level=level, base=b, first=first, count=count, seed=seed, sum=float(r["sum"]).hex(),
+                             sum_sq=float(r["sum_sq"]).hex(), samples=int(r["samples"]), cost=int(r["cost"])))
+        out["matrices"][name] = dict(csr_t=csr_json(t.a), u=hx(u), beta=float(beta).hex(),
+                                     exact_sum=float(np.sum(ch.dense_expmv(u, beta))).hex(),
+                                     samples=samples, run_level=runs)
+    # drivers: sum(e^{tA}u) for smallw150 (eps 3 on a sum of ~4.6e3) and grid16 (eps 0.5)
+    drivers = {}
+    g16 = ref.chain(grid(16))
+    for (name, ch, beta, eps, seeds) in [("smallw150", base["smallw150"], 0.7, 3.0, [3, 4]),
+                                         ("grid16", g16, 1.0, 0.5, [11, 12])]:
+        t = ch.transposed()
+        u = 0.5 + (np.arange(t.n) % 3).astype(np.float64)
+        res = t.forward_driver(u, beta, seeds=seeds, epsilon=eps, threads=4)
+        drivers[name] = dict(csr_t=csr_json(t.a), u=hx(u), beta=float(beta).hex(), epsilon=eps, seeds=seeds,
+                             exact_sum=float(np.sum(ch.dense_expmv(u, beta))).hex(), results=[
+                                 dict(estimate=float(r["estimate"]).hex(),
+                                      statistical_error=float(r["statistical_error"]).hex(),
+                                      bias_estimate=float(r["bias_estimate"]).hex(), l0=r["l0"], L=r["L"],
+                                      total_cost=int(r["total_cost"]), converged=r["converged"],
+                                      levels=[dict(level=int(x["level"]), sum=float(x["sum"]).hex(),
+                                                   sum_sq=float(x["sum_sq"]).hex(), samples=int(x["samples"]),
+                                                   cost=int(x["cost"])) for x in r["levels"]]) for r in res])
+    out["drivers"] = drivers
+    path = os.path.join(HERE, "golden_forward.json")
+    with open(path, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print(path, os.path.getsize(path), "bytes")
+
+
 if __name__ == "__main__":
-    main()
+    if "--forward-only" not in sys.argv:
+        main()
+    forward()
