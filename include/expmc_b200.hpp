@@ -11,11 +11,17 @@
 //                            seed, threads);
 //   MlmcResult r = mlmc_driver(p, opts);         MlmcResult r = mlmc_driver(p, opts);
 //   (one driver call per component)              mlmc_driver_rows(ctx, beta, rows, seeds, opts)
+//   p.mode = SampleMode::forward (dec of A^T)    p.mode = SampleMode::forward (ctx of A^T)
+//   total_communicability(A, beta, opts)         total_communicability(A, beta, opts)
+//   node_communicability(A, node, beta, opts)    node_communicability(A, node, beta, opts)
 //
 // Link with paper_1904_12754_b200/_lib/libexpmc_b200.so.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <numeric>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -113,12 +119,45 @@ class Context {
     expmc_ctx_info info_{};
 };
 
-/// mlmc.hpp:50-57, entry mode.
+/// A^T in canonical CSR (SparseMatrix::transposed): forward mode runs on the tables of A^T.
+inline CsrView transposed(const CsrView& a) {
+    CsrView t;
+    t.n = a.n;
+    t.row_ptr.assign(static_cast<size_t>(a.n) + 1, 0);
+    for (int64_t k = 0; k < static_cast<int64_t>(a.col.size()); ++k) ++t.row_ptr[static_cast<size_t>(a.col[k]) + 1];
+    std::partial_sum(t.row_ptr.begin(), t.row_ptr.end(), t.row_ptr.begin());
+    t.col.resize(a.col.size());
+    t.val.resize(a.val.size());
+    std::vector<int64_t> next(t.row_ptr.begin(), t.row_ptr.end() - 1);
+    for (int64_t i = 0; i < a.n; ++i)  // rows ascending: each new row's columns come out sorted
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            const int64_t at = next[static_cast<size_t>(a.col[k])]++;
+            t.col[at] = i;
+            t.val[at] = a.val[k];
+        }
+    return t;
+}
+
+/// mlmc.hpp:45.  fem is outside this build (the C-ABI answers EXPMC_ENOTIMPL).
+enum class SampleMode { entry, forward, fem };
+
+/// mlmc.hpp:47-57: entry mode on the context of A, forward mode on the context of A^T.
 struct MlmcProblem {
     Context* ctx = nullptr;
     std::int64_t entry = 0;
     double beta = 1.0;
+    SampleMode mode = SampleMode::entry;
 };
+
+/// spectral_scale (chain.cpp:98-102): 1 / d_max.
+inline double spectral_scale(const Context& ctx) {
+    if (!(ctx.info().d_max > 0.0)) throw std::domain_error("d_max <= 0: no spectral scale, supply beta explicitly");
+    return 1.0 / ctx.info().d_max;
+}
+
+inline void check_mode(SampleMode m) {
+    if (m == SampleMode::fem) throw std::runtime_error("fem sampling (lane 2) is not built");
+}
 
 inline int initial_level(double beta, double d_max) {
     int32_t l = 0;
@@ -144,8 +183,14 @@ inline double bias_estimate(const std::vector<double>& means) {
 inline LevelStats run_level(const MlmcProblem& p, int level, bool base_level, std::uint64_t first_index,
                             std::uint64_t additional, std::uint64_t seed, int /*threads*/ = 0) {
     if (p.ctx == nullptr) throw std::invalid_argument("problem has no decomposition");
+    check_mode(p.mode);
     expmc_level_stats s{};
-    check(expmc_run_level(p.ctx->get(), p.entry, p.beta, level, base_level ? 1 : 0, first_index, additional, seed, &s));
+    if (p.mode == SampleMode::forward)
+        check(expmc_run_level_forward(p.ctx->get(), p.beta, level, base_level ? 1 : 0, first_index, additional, seed,
+                                      &s));
+    else
+        check(expmc_run_level(p.ctx->get(), p.entry, p.beta, level, base_level ? 1 : 0, first_index, additional,
+                              seed, &s));
     return LevelStats{level, s.sum, s.sum_sq, s.samples, s.cost, s.jumps};
 }
 
@@ -172,8 +217,29 @@ inline MlmcResult mlmc_driver(const MlmcProblem& p, const MlmcOptions& opt) {
     expmc_result r{};
     std::vector<expmc_level_record> lv(kMax);
     const expmc_options o = opt.c();
-    check(expmc_mlmc_driver(p.ctx->get(), p.entry, p.beta, &o, &r, lv.data(), kMax));
+    check_mode(p.mode);
+    if (p.mode == SampleMode::forward)
+        check(expmc_mlmc_driver_forward(p.ctx->get(), p.beta, &o, 1, nullptr, &r, lv.data(), kMax));
+    else
+        check(expmc_mlmc_driver(p.ctx->get(), p.entry, p.beta, &o, &r, lv.data(), kMax));
     return to_result(r, lv.data());
+}
+
+/// total_communicability (communicability.cpp:10-21): 1^T e^{beta A} 1 by forward-mode MLMC
+/// on A^T; beta defaults to spectral_scale of A^T's decomposition.
+inline MlmcResult total_communicability(const CsrView& a, std::optional<double> beta, const MlmcOptions& opt,
+                                        int device = 0) {
+    Context ctx(transposed(a), std::vector<double>(static_cast<size_t>(a.n), 1.0), device);
+    MlmcProblem p{&ctx, 0, beta ? *beta : spectral_scale(ctx), SampleMode::forward};
+    return mlmc_driver(p, opt);
+}
+
+/// node_communicability (communicability.cpp:23-35): (e^{beta A} 1)_node, entry mode.
+inline MlmcResult node_communicability(const CsrView& a, std::int64_t node, std::optional<double> beta,
+                                       const MlmcOptions& opt, int device = 0) {
+    Context ctx(a, std::vector<double>(static_cast<size_t>(a.n), 1.0), device);
+    MlmcProblem p{&ctx, node, beta ? *beta : spectral_scale(ctx), SampleMode::entry};
+    return mlmc_driver(p, opt);
 }
 
 /// The all-components estimator: one reference decision sequence per row, batched on the GPU.

@@ -28,6 +28,9 @@ from .api import (  # noqa: F401
     initial_level,
     mlmc_driver,
     mlmc_driver_forward,
+    node_communicability,
+    spectral_scale,
+    total_communicability,
     mlmc_driver_rows,
     optimal_allocation,
     run_level,

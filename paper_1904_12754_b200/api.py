@@ -459,6 +459,31 @@ def mlmc_driver_rows(ctx: Context, beta: float, rows, row_seeds, options: MlmcOp
     return res, lv
 
 
+def spectral_scale(ctx: Context) -> float:
+    """chain.cpp:98-102: 1 / d_max of the context's decomposition."""
+    if not ctx.d_max > 0.0:
+        raise DomainError("d_max <= 0: no spectral scale, supply beta explicitly")
+    return 1.0 / ctx.d_max
+
+
+def total_communicability(a: SparseMatrix, beta: float | None = None, options: MlmcOptions = MlmcOptions(),
+                          device: int = 0, sampler: str = "reference") -> MlmcResult:
+    """communicability.cpp:10-21: 1^T e^{beta A} 1 by forward-mode MLMC on A^T (one scalar
+    MLMC problem); beta defaults to spectral_scale of A^T's decomposition."""
+    with Context(a.transposed(), np.ones(a.n), device, sampler) as ctx:
+        b = spectral_scale(ctx) if beta is None else beta
+        return mlmc_driver(MlmcProblem(ctx, 0, b, SampleMode.forward), options)
+
+
+def node_communicability(a: SparseMatrix, node: int, beta: float | None = None,
+                         options: MlmcOptions = MlmcOptions(), device: int = 0,
+                         sampler: str = "reference") -> MlmcResult:
+    """communicability.cpp:23-35: (e^{beta A} 1)_node, entry mode."""
+    with Context(a, np.ones(a.n), device, sampler) as ctx:
+        b = spectral_scale(ctx) if beta is None else beta
+        return mlmc_driver(MlmcProblem(ctx, node, b, SampleMode.entry), options)
+
+
 def nccl_unique_id() -> bytes:
     """128-byte NCCL id for Context.shard_samples (create on one rank, broadcast to the rest)."""
     buf = (C.c_uint8 * 128)()

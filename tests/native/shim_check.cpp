@@ -63,6 +63,11 @@ static void host_checks() {
     CHECK(throws<std::invalid_argument>([] { bias_estimate({1.0}); }));
     CHECK(throws<std::invalid_argument>([] { initial_level(0.0, 1.0); }));
     CHECK(throws<std::invalid_argument>([] { optimal_allocation({1.0}, {0.0}, 0.1); }));
+    // transposed: canonical CSR of A^T
+    const CsrView a = dense(3, {0.1, -1.0, 0.5, 0.7, -0.2, -0.2, -0.4, 0.0, 0.3});
+    const CsrView t = transposed(a);
+    const CsrView te = dense(3, {0.1, 0.7, -0.4, -1.0, -0.2, 0.0, 0.5, -0.2, 0.3});
+    CHECK(t.row_ptr == te.row_ptr && t.col == te.col && t.val == te.val);
 }
 
 static void gpu_checks() {
@@ -113,6 +118,27 @@ static void gpu_checks() {
         for (const LevelStats& l : r.levels) CHECK(l.samples == 1000);
     }
     CHECK(throws<std::invalid_argument>([] { Context bad(dense(2, {0.0, NAN, 0.0, 0.0}), {1.0, 1.0}); }));
+    // forward mode (test_paths.cpp:275-293) and communicability (communicability.cpp:10-35)
+    {
+        const CsrView k2 = dense(2, {0.0, 1.0, 1.0, 0.0});
+        Context ctx(transposed(k2), {1.0, 1.0});
+        const LevelStats s = run_level(MlmcProblem{&ctx, 0, 1.0, SampleMode::forward}, 2, true, 0, 500, 11);
+        CHECK(std::abs(s.mean() - 2.0 * std::exp(1.0)) <= 1e-14 * s.mean());
+        MlmcOptions o;
+        o.epsilon = 1e-3;
+        const MlmcResult tc = total_communicability(k2, 1.0, o);
+        CHECK(tc.converged && std::abs(tc.estimate - 2.0 * std::exp(1.0)) <= 1e-13);
+        const MlmcResult nc = node_communicability(k2, 1, 1.0, o);
+        CHECK(nc.converged && std::abs(nc.estimate - std::exp(1.0)) <= 1e-3);
+        Context neg(transposed(k2), {1.0, -0.5});
+        CHECK(throws<std::invalid_argument>(
+            [&] { run_level(MlmcProblem{&neg, 0, 1.0, SampleMode::forward}, 2, true, 0, 10, 1); }));
+        Context zero(transposed(k2), {0.0, 0.0});
+        CHECK(throws<std::invalid_argument>(
+            [&] { mlmc_driver(MlmcProblem{&zero, 0, 1.0, SampleMode::forward}, MlmcOptions{}); }));
+        Context zmat(dense(2, {0.0, 0.0, 0.0, 0.0}), {1.0, 1.0});
+        CHECK(throws<std::domain_error>([&] { spectral_scale(zmat); }));
+    }
 }
 
 int main(int argc, char** argv) {

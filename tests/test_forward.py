@@ -268,3 +268,24 @@ def test_gpu_forward_event_sampler_statistical(gpu, golden_forward):
     for a, b in zip(stats["reference"], stats["event"]):
         se = math.sqrt(a.variance() / a.samples + b.variance() / b.samples)
         assert abs(a.mean() - b.mean()) < 4 * se + 1e-12
+
+
+@pytest.mark.gpu
+def test_gpu_total_and_node_communicability(gpu, golden_forward, oracle_lib):
+    """communicability.cpp:10-35 on pref(300, 3, 7) (test_mc.cpp:125-143 analogue): the forward
+    driver's 1^T e^{beta A} 1 and the entry driver's (e^{beta A} 1)_node against dense_expmv."""
+    import paper_1904_12754_b200 as P
+
+    t = csr_t(golden_forward["matrices"]["pref300"])
+    a = P.SparseMatrix(t.n, t.row_ptr, t.col, t.val).transposed()
+    beta = 1.0 / oracle_lib.chain(t).d_max  # spectral_scale(dec of A^T), chain.cpp:98-102
+    exact = oracle_lib.dense_expmv(CSR(a.n, a.row_ptr, a.col, a.val), np.ones(a.n), beta)
+    eps = 0.5
+    tc = P.total_communicability(a, options=P.MlmcOptions(epsilon=eps, seed=4))
+    assert tc.converged
+    assert abs(tc.estimate - exact.sum()) < 3 * tc.statistical_error + eps
+    for node in (0, 150):
+        nc = P.node_communicability(a, node, beta, P.MlmcOptions(epsilon=1e-2, seed=node))
+        assert nc.converged and abs(nc.estimate - exact[node]) < 3 * nc.statistical_error + 1e-2
+    with pytest.raises(P.DomainError):
+        P.total_communicability(P.SparseMatrix.from_dense(np.zeros((2, 2))))
