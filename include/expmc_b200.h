@@ -45,6 +45,10 @@ extern "C" {
  * a context built from A^T (mlmc.hpp:47-49). */
 #define EXPMC_LANE_ENTRY 0u
 #define EXPMC_LANE_FORWARD 1u
+/* FEM (SampleMode::fem, paths.cpp:183-245): entry mode plus the Duhamel integral of a load
+ * vector along the path with composite-Simpson weights; runs on a context built with
+ * expmc_ctx_create_scaled (the chain of -M^{-1}K) and a load set by expmc_ctx_set_load. */
+#define EXPMC_LANE_FEM 2u
 
 typedef struct expmc_ctx expmc_ctx;
 
@@ -87,6 +91,7 @@ typedef struct {
     uint64_t samples;
     uint64_t cost; /* model units: exponential draws + fine steps (paths.hpp:22-23) */
     uint64_t jumps;
+    double integ_sum; /* fem: sum of integ_fine - integ_coarse (LevelDelta::integ_sum, mlmc.cpp:61) */
 } expmc_level_stats;
 
 /* MlmcOptions (mlmc.hpp:59-67); `seed` is used by expmc_mlmc_driver only (the row API takes
@@ -120,6 +125,7 @@ typedef struct {
     double projected_cost; /* model units the last allocation asked for (sum_l M_l C_l) */
     int32_t over_budget;   /* 1: stopped by max_cost */
     int32_t pad;
+    double quadrature_bound; /* fem: bias_estimate of the load-integral means (mlmc.hpp:37) */
 } expmc_result;
 
 /* One entry of MlmcResult::levels (LevelStats, mlmc.hpp:18-24). */
@@ -158,8 +164,17 @@ int expmc_device_count(int* out);
 int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx** out);
 void expmc_ctx_destroy(expmc_ctx* ctx);
 int expmc_ctx_get_info(const expmc_ctx* ctx, expmc_ctx_info* out);
+/* decompose_scaled (chain.cpp:80-85): the tables of diag(row_scale) A -- the generator
+ * -M^{-1}K of a lumped-mass FEM system (fem.cpp:62-66) without materialising it.  Errors as
+ * the reference, row by row: non-finite row_scale[i] -> EXPMC_EINVAL "row scale is NaN or
+ * Inf", non-finite scaled entry -> EXPMC_EINVAL; entries scaled to zero vanish. */
+int expmc_ctx_create_scaled(const expmc_csr* A, const double* row_scale, const double* u, int device,
+                            expmc_ctx** out);
 /* Rebind u (MlmcProblem::u): length n. */
 int expmc_ctx_set_vector(expmc_ctx* ctx, const double* u);
+/* Bind the fem load vector (MlmcProblem::load, mlmc.hpp:53; length n).  Until it is set,
+ * fem requests fail with EXPMC_EINVAL "load length does not match decomposition". */
+int expmc_ctx_set_load(expmc_ctx* ctx, const double* load);
 /* Export the decomposition (ChainDecomposition, chain.hpp:27-40): d, rate [n], row_ptr [n+1],
  * jump_cdf, jump_target [n_edges], sign [n_edges]; any pointer may be NULL. */
 int expmc_ctx_export_tables(const expmc_ctx* ctx, double* d, double* rate, int64_t* row_ptr,
@@ -217,6 +232,33 @@ int expmc_run_level_batch(expmc_ctx* ctx, double beta, uint32_t lane, int64_t nr
 int expmc_sample_debug(expmc_ctx* ctx, double beta, uint32_t lane, int64_t nreq,
                        const expmc_level_req* req, double* eta_fine, double* eta_coarse,
                        uint64_t* cost, uint64_t* jumps, int64_t* end_state);
+
+/* Per-sample record of any lane: value = the run_level sample x (mlmc.cpp:103-133); fem also
+ * reports the load integrals (FemCoupledSample, paths.hpp). */
+typedef struct {
+    double eta_fine;    /* base: the value */
+    double eta_coarse;
+    double value;
+    double integ_fine;
+    double integ_coarse;
+    uint64_t cost;
+    uint64_t jumps;
+    int64_t end_state;
+} expmc_sample_record;
+int expmc_sample_debug_ex(expmc_ctx* ctx, double beta, uint32_t lane, int64_t nreq,
+                          const expmc_level_req* req, expmc_sample_record* out);
+
+/* run_level in fem mode (mlmc.cpp:76-148, lane 2), ONE request; out->integ_sum carries the
+ * load-integral side channel.  Errors: load not set -> EXPMC_EINVAL; coupled at level < 2 ->
+ * EXPMC_EINVAL "coupled quadrature needs a step count divisible by 4" (paths.cpp:212-213). */
+int expmc_run_level_fem(expmc_ctx* ctx, int64_t entry, double beta, int32_t level, int32_t base_level,
+                        uint64_t first_index, uint64_t additional, uint64_t seed, expmc_level_stats* out);
+
+/* mlmc_driver in fem mode for nrows entries (l0 >= 1, mlmc.cpp:177; result.quadrature_bound,
+ * mlmc.cpp:226-241). */
+int expmc_mlmc_driver_fem(expmc_ctx* ctx, double beta, const expmc_options* options, int64_t nrows,
+                          const int64_t* rows, const uint64_t* row_seed, expmc_result* out,
+                          expmc_level_record* levels, int32_t max_levels);
 
 /* mlmc_driver (mlmc.hpp:94; mlmc.cpp:170-260) for ONE entry, options->seed as the seed. */
 int expmc_mlmc_driver(expmc_ctx* ctx, int64_t entry, double beta, const expmc_options* options,

@@ -108,7 +108,24 @@ class Context {
         check(expmc_ctx_create(&csr, u.data(), device, &ctx_));
         check(expmc_ctx_get_info(ctx_, &info_));
     }
+    /// decompose_scaled (chain.cpp:80-85): the tables of diag(row_scale) A.
+    Context(const CsrView& a, const std::vector<double>& row_scale, const std::vector<double>& u, int device) {
+        if (static_cast<int64_t>(u.size()) != a.n)
+            throw std::invalid_argument("vector length does not match decomposition");
+        if (static_cast<int64_t>(row_scale.size()) != a.n)
+            throw std::invalid_argument("row scale length does not match matrix dimension");
+        const expmc_csr csr{a.n, a.row_ptr.empty() ? 0 : a.row_ptr.back(), a.row_ptr.data(), a.col.data(),
+                            a.val.data()};
+        check(expmc_ctx_create_scaled(&csr, row_scale.data(), u.data(), device, &ctx_));
+        check(expmc_ctx_get_info(ctx_, &info_));
+    }
     ~Context() { expmc_ctx_destroy(ctx_); }
+    /// MlmcProblem::load for fem mode.
+    void set_load(const std::vector<double>& load) {
+        if (static_cast<int64_t>(load.size()) != info_.n)
+            throw std::invalid_argument("load length does not match decomposition");
+        check(expmc_ctx_set_load(ctx_, load.data()));
+    }
     Context(const Context&) = delete;
     Context& operator=(const Context&) = delete;
     expmc_ctx* get() const { return ctx_; }
@@ -155,9 +172,7 @@ inline double spectral_scale(const Context& ctx) {
     return 1.0 / ctx.info().d_max;
 }
 
-inline void check_mode(SampleMode m) {
-    if (m == SampleMode::fem) throw std::runtime_error("fem sampling (lane 2) is not built");
-}
+inline void check_mode(SampleMode) {}
 
 inline int initial_level(double beta, double d_max) {
     int32_t l = 0;
@@ -188,6 +203,9 @@ inline LevelStats run_level(const MlmcProblem& p, int level, bool base_level, st
     if (p.mode == SampleMode::forward)
         check(expmc_run_level_forward(p.ctx->get(), p.beta, level, base_level ? 1 : 0, first_index, additional, seed,
                                       &s));
+    else if (p.mode == SampleMode::fem)
+        check(expmc_run_level_fem(p.ctx->get(), p.entry, p.beta, level, base_level ? 1 : 0, first_index, additional,
+                                  seed, &s));
     else
         check(expmc_run_level(p.ctx->get(), p.entry, p.beta, level, base_level ? 1 : 0, first_index, additional,
                               seed, &s));
@@ -199,6 +217,7 @@ inline MlmcResult to_result(const expmc_result& r, const expmc_level_record* lv)
     o.estimate = r.estimate;
     o.statistical_error = r.statistical_error;
     o.bias_estimate = r.bias_estimate;
+    o.quadrature_bound = r.quadrature_bound;
     o.l0 = r.l0;
     o.L = r.L;
     o.total_cost = r.total_cost;
@@ -218,9 +237,13 @@ inline MlmcResult mlmc_driver(const MlmcProblem& p, const MlmcOptions& opt) {
     std::vector<expmc_level_record> lv(kMax);
     const expmc_options o = opt.c();
     check_mode(p.mode);
-    if (p.mode == SampleMode::forward)
+    if (p.mode == SampleMode::forward) {
         check(expmc_mlmc_driver_forward(p.ctx->get(), p.beta, &o, 1, nullptr, &r, lv.data(), kMax));
-    else
+    } else if (p.mode == SampleMode::fem) {
+        const std::int64_t row = p.entry;
+        const std::uint64_t seed = opt.seed;
+        check(expmc_mlmc_driver_fem(p.ctx->get(), p.beta, &o, 1, &row, &seed, &r, lv.data(), kMax));
+    } else
         check(expmc_mlmc_driver(p.ctx->get(), p.entry, p.beta, &o, &r, lv.data(), kMax));
     return to_result(r, lv.data());
 }
@@ -232,6 +255,31 @@ inline MlmcResult total_communicability(const CsrView& a, std::optional<double> 
     Context ctx(transposed(a), std::vector<double>(static_cast<size_t>(a.n), 1.0), device);
     MlmcProblem p{&ctx, 0, beta ? *beta : spectral_scale(ctx), SampleMode::forward};
     return mlmc_driver(p, opt);
+}
+
+/// fem.hpp FemSystem: lumped-mass system M u' = -K u + F, u(0) = u0.
+struct FemSystem {
+    std::vector<double> mass_diag;
+    CsrView stiffness;
+    std::vector<double> load;
+    std::vector<double> u0;
+    std::int64_t size() const { return stiffness.n; }
+};
+
+/// solve_convdiff_point (fem.cpp:51-73): u(node, t) by fem-mode MLMC on the chain of -M^{-1}K.
+inline MlmcResult solve_convdiff_point(const FemSystem& sys, std::int64_t node, double t, const MlmcOptions& opt,
+                                       int device = 0) {
+    if (!(t > 0.0)) throw std::invalid_argument("time must be positive");
+    if (node < 0 || node >= sys.size()) throw std::out_of_range("node index outside system");
+    const size_t n = static_cast<size_t>(sys.size());
+    std::vector<double> row_scale(n), scaled_load(n);
+    for (size_t i = 0; i < n; ++i) {
+        row_scale[i] = -1.0 / sys.mass_diag[i];
+        scaled_load[i] = sys.load[i] / sys.mass_diag[i];
+    }
+    Context ctx(sys.stiffness, row_scale, sys.u0, device);
+    ctx.set_load(scaled_load);
+    return mlmc_driver(MlmcProblem{&ctx, node, t, SampleMode::fem}, opt);
 }
 
 /// node_communicability (communicability.cpp:23-35): (e^{beta A} 1)_node, entry mode.

@@ -317,6 +317,51 @@ class OracleChain(_Chain):
                      total_jumps=r.total_jumps, total_samples=r.total_samples, levels=lv[i, :r.nlevels].copy())
                 for i, r in enumerate(res)]
 
+    # ---- fem mode (lane 2): the chain of -M^{-1}K, load = M^{-1}F
+    def fem_samples(self, u, load, entry, beta, level, base, seed, sample_idx):
+        idx = np.ascontiguousarray(sample_idx, np.uint64)
+        k = len(idx)
+        u = np.ascontiguousarray(u, np.float64)
+        load = np.ascontiguousarray(load, np.float64)
+        out = {x: np.empty(k) for x in ("value", "eta_f", "eta_c", "integ_f", "integ_c")}
+        end = np.empty(k, np.int64)
+        cost, jumps = np.empty(k, np.uint64), np.empty(k, np.uint64)
+        self.be._check(self.be.lib.orc_fem_samples(
+            self.h, _ptr(u), _ptr(load), _I64(entry), _D(beta), _INT(level), _INT(int(base)), _U64(seed), _I64(k),
+            _ptr(idx), _ptr(out["value"]), _ptr(out["eta_f"]), _ptr(out["eta_c"]), _ptr(out["integ_f"]),
+            _ptr(out["integ_c"]), _ptr(end), _ptr(cost), _ptr(jumps)))
+        out.update(end_state=end, cost=cost, jumps=jumps)
+        return out
+
+    def fem_run_level(self, u, load, entry, beta, level, base, first, count, seed, threads=1):
+        u = np.ascontiguousarray(u, np.float64)
+        load = np.ascontiguousarray(load, np.float64)
+        st = _OrcStats()
+        ig = _D()
+        self.be._check(self.be.lib.orc_fem_run_level(self.h, _ptr(u), _ptr(load), _I64(entry), _D(beta), _INT(level),
+                                                     _INT(int(base)), _U64(first), _U64(count), _U64(seed),
+                                                     _INT(threads), C.byref(st), C.byref(ig)))
+        return dict(sum=st.sum, sum_sq=st.sum_sq, samples=st.samples, cost=st.cost, jumps=st.jumps,
+                    integ_sum=ig.value)
+
+    def fem_driver_rows(self, u, load, beta, rows, row_seeds, max_levels=40, **opt):
+        rows = np.ascontiguousarray(rows, np.int64)
+        seeds = np.ascontiguousarray(row_seeds, np.uint64)
+        u = np.ascontiguousarray(u, np.float64)
+        load = np.ascontiguousarray(load, np.float64)
+        res = (_OrcResult * len(rows))()
+        quad = np.zeros(len(rows))
+        lv = np.zeros((len(rows), max_levels), LEVEL_DT)
+        o = _options(**opt)
+        self.be._check(self.be.lib.orc_mlmc_driver_fem(self.h, _ptr(u), _ptr(load), _D(beta), C.byref(o),
+                                                       _I64(len(rows)), _ptr(rows), _ptr(seeds), res, _ptr(quad),
+                                                       _ptr(lv), C.c_int32(max_levels)))
+        return [dict(estimate=r.estimate, statistical_error=r.statistical_error, bias_estimate=r.bias_estimate,
+                     quadrature_bound=float(quad[i]), l0=r.l0, L=r.L, total_cost=r.total_cost,
+                     converged=bool(r.converged), nlevels=r.nlevels, total_jumps=r.total_jumps,
+                     total_samples=r.total_samples, levels=lv[i, :r.nlevels].copy())
+                for i, r in enumerate(res)]
+
     def transposed(self) -> "OracleChain":
         return OracleChain(self.be, self.a.transpose())
 
@@ -345,6 +390,52 @@ class Reference(_Backend):
         h = C.c_void_p()
         self._check(self.lib.ref_smallw(_I64(n), _I64(k), _D(p), _U64(seed), C.byref(h)))
         return RefChain(self, None, handle=h)
+
+    def chain_scaled(self, a: CSR, row_scale) -> "RefChain":
+        """decompose_scaled (chain.cpp:80-85)."""
+        sc = np.ascontiguousarray(row_scale, np.float64)
+        h = C.c_void_p()
+        self._check(self.lib.ref_matrix_create_scaled(_I64(a.n), _ptr(a.row_ptr), _ptr(a.col), _ptr(a.val), _ptr(sc),
+                                                      C.byref(h)))
+        return RefChain(self, None, handle=h)
+
+    def read_matrix_market(self, path) -> "RefChain":
+        h = C.c_void_p()
+        self._check(self.lib.ref_read_matrix_market(os.fsencode(path), C.byref(h)))
+        return RefChain(self, None, handle=h)
+
+    def read_vector(self, path):
+        n = _I64()
+        self._check(self.lib.ref_read_vector(os.fsencode(path), _I64(0), None, C.byref(n)))
+        out = np.empty(n.value)
+        self._check(self.lib.ref_read_vector(os.fsencode(path), _I64(n.value), _ptr(out), C.byref(n)))
+        return out
+
+    def load_fem_system(self, mass, stiffness, load, u0):
+        """load_fem_system (fem.cpp:12-37) -> dict(mass_diag, stiffness: CSR, load, u0)."""
+        n, nnz = _I64(), _I64()
+        args = [os.fsencode(x) for x in (mass, stiffness, load, u0)]
+        self._check(self.lib.ref_load_fem_system(*args, C.byref(n), C.byref(nnz), None, None, None, None, None, None))
+        md, ld, u0v = np.empty(n.value), np.empty(n.value), np.empty(n.value)
+        rp, col, val = np.empty(n.value + 1, np.int64), np.empty(nnz.value, np.int64), np.empty(nnz.value)
+        self._check(self.lib.ref_load_fem_system(*args, C.byref(n), C.byref(nnz), _ptr(md), _ptr(rp), _ptr(col),
+                                                 _ptr(val), _ptr(ld), _ptr(u0v)))
+        return dict(mass_diag=md, stiffness=CSR(n.value, rp, col, val), load=ld, u0=u0v)
+
+    def solve_convdiff_point(self, mass_diag, stiffness: CSR, load, u0, node, t, max_levels=40, **opt):
+        """solve_convdiff_point (fem.cpp:51-73)."""
+        md = np.ascontiguousarray(mass_diag, np.float64)
+        ld = np.ascontiguousarray(load, np.float64)
+        u0 = np.ascontiguousarray(u0, np.float64)
+        res = _RefResult()
+        lv = np.zeros(max_levels, LEVEL_DT)
+        q = _D()
+        o = _options(**opt)
+        a = stiffness
+        self._check(self.lib.ref_solve_convdiff_point(_I64(a.n), _ptr(md), _ptr(a.row_ptr), _ptr(a.col), _ptr(a.val),
+                                                      _ptr(ld), _ptr(u0), _I64(node), _D(t), C.byref(o), C.byref(res),
+                                                      _ptr(lv), C.c_int32(max_levels), C.byref(q)))
+        return _ref_result(res, lv, quadrature_bound=q.value)
 
     def initial_level(self, beta, d_max):
         out = C.c_int()
@@ -477,6 +568,47 @@ class RefChain(_Chain):
         self.be._check(self.be.lib.ref_transpose(self.h, C.byref(h)))
         return RefChain(self.be, None, handle=h)
 
+    # ---- fem mode (SampleMode::fem)
+    def fem_samples(self, u, load, entry, beta, level, base, seed, sample_idx):
+        idx = np.ascontiguousarray(sample_idx, np.uint64)
+        k = len(idx)
+        u = np.ascontiguousarray(u, np.float64)
+        load = np.ascontiguousarray(load, np.float64)
+        out = {x: np.empty(k) for x in ("value", "eta_f", "eta_c", "integ_f", "integ_c")}
+        end = np.empty(k, np.int64)
+        cost = np.empty(k, np.uint64)
+        self.be._check(self.be.lib.ref_fem_samples(
+            self.h, _ptr(u), _ptr(load), _I64(entry), _D(beta), _INT(level), _INT(int(base)), _U64(seed), _I64(k),
+            _ptr(idx), _ptr(out["value"]), _ptr(out["eta_f"]), _ptr(out["eta_c"]), _ptr(out["integ_f"]),
+            _ptr(out["integ_c"]), _ptr(end), _ptr(cost)))
+        out.update(end_state=end, cost=cost)
+        return out
+
+    def fem_run_level(self, u, load, entry, beta, level, base, first, count, seed, threads=1):
+        u = np.ascontiguousarray(u, np.float64)
+        load = np.ascontiguousarray(load, np.float64)
+        s, s2 = _D(), _D()
+        m, c = _U64(), _U64()
+        self.be._check(self.be.lib.ref_fem_run_level(self.h, _ptr(u), _ptr(load), _I64(entry), _D(beta), _INT(level),
+                                                     _INT(int(base)), _U64(first), _U64(count), _U64(seed),
+                                                     _INT(threads), C.byref(s), C.byref(s2), C.byref(m), C.byref(c)))
+        return dict(sum=s.value, sum_sq=s2.value, samples=m.value, cost=c.value)
+
+    def fem_driver_rows(self, u, load, beta, rows, row_seeds, max_levels=40, **opt):
+        u = np.ascontiguousarray(u, np.float64)
+        load = np.ascontiguousarray(load, np.float64)
+        out = []
+        for row, sd in zip(rows, row_seeds):
+            res = _RefResult()
+            lv = np.zeros(max_levels, LEVEL_DT)
+            q = _D()
+            o = _options(seed=int(sd), **opt)
+            self.be._check(self.be.lib.ref_fem_driver(self.h, _ptr(u), _ptr(load), _I64(int(row)), _D(beta),
+                                                      C.byref(o), C.byref(res), _ptr(lv), C.c_int32(max_levels),
+                                                      C.byref(q)))
+            out.append(_ref_result(res, lv, quadrature_bound=q.value))
+        return out
+
     def dense_expmv(self, u, beta):
         u = np.ascontiguousarray(u, np.float64)
         out = np.empty(self.n, np.float64)
@@ -488,6 +620,14 @@ class RefChain(_Chain):
         out = np.empty(self.n, np.float64)
         self.be._check(self.be.lib.ref_strang_reference(self.h, _ptr(u), _D(beta), _I64(steps), _ptr(out)))
         return out
+
+
+def _ref_result(res, lv, **extra):
+    d = dict(estimate=res.estimate, statistical_error=res.statistical_error, bias_estimate=res.bias_estimate,
+             l0=res.l0, L=res.L, total_cost=res.total_cost, converged=bool(res.converged), nlevels=res.nlevels,
+             levels=lv[:res.nlevels].copy())
+    d.update(extra)
+    return d
 
 
 def have_reference() -> bool:

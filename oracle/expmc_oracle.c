@@ -301,6 +301,119 @@ static orc_sample sample_coupled(const orc_chain* c, const double* u, int64_t en
     return r;
 }
 
+static int check_level(int level);
+
+/* scaled_simpson (mlmc.cpp:66-75): composite Simpson weight of node j of `panels`, scaled by
+ * the step through h = step / 3. */
+static double simpson_w(int64_t j, int64_t panels, double h) {
+    const int end = (j == 0 || j == panels);
+    return h * (end ? 1.0 : (j % 2 == 1 ? 4.0 : 2.0));
+}
+
+typedef struct {
+    double value, eta_f, eta_c, integ_f, integ_c;
+    uint64_t cost, jumps;
+    int64_t end_state;
+} orc_fem_sample;
+
+/* LevelSampler::fem_single, paths.cpp:183-203 (weights: run_level_ex, mlmc.cpp:89-90) */
+static orc_fem_sample fem_single(const orc_chain* c, const double* u, const double* load, int64_t entry,
+                                 double dt, int64_t steps, orc_stream* s) {
+    const double h = dt / 3.0;
+    int64_t state = entry;
+    int sign = 1;
+    uint64_t draws = 0, jumps = 0;
+    double expo = 0.0;
+    double integ = simpson_w(0, steps, h) * load[entry];
+    for (int64_t n = 0; n < steps; ++n) {
+        const int64_t s0 = state;
+        state = evolve_common(c, state, &sign, &draws, &jumps, dt, -expm1(-c->rate[state] * dt), s);
+        expo += dt * 0.5 * (c->d[s0] + c->d[state]);
+        integ += simpson_w(n + 1, steps, h) * sign * exp(expo) * load[state];
+    }
+    orc_fem_sample r;
+    r.value = sign * exp(expo) * u[state] + integ;
+    r.eta_f = r.eta_c = r.integ_f = r.integ_c = 0.0;
+    r.cost = draws + (uint64_t)steps;
+    r.jumps = jumps;
+    r.end_state = state;
+    return r;
+}
+
+/* LevelSampler::fem_coupled, paths.cpp:205-245; the run_level sample
+ * u[terminal] (eta_f - eta_c) + (integ_f - integ_c), mlmc.cpp:126-133 */
+static orc_fem_sample fem_coupled(const orc_chain* c, const double* u, const double* load, int64_t entry,
+                                  double dt, int64_t steps, orc_stream* s) {
+    const double hf = dt / 3.0, hc = (2.0 * dt) / 3.0;
+    const int64_t half = steps / 2;
+    int64_t state = entry;
+    int sign = 1;
+    uint64_t draws = 0, jumps = 0;
+    double coarse = 0.0, delta = 0.0, eta_f = 1.0, eta_c = 1.0;
+    double integ_f = simpson_w(0, steps, hf) * load[entry];
+    double integ_c = simpson_w(0, half, hc) * load[entry];
+    for (int64_t m = 0; m < half; ++m) {
+        const int64_t s0 = state;
+        state = evolve_common(c, state, &sign, &draws, &jumps, dt, -expm1(-c->rate[state] * dt), s);
+        const int64_t s1 = state;
+        const double mid = coarse + delta + dt * 0.5 * (c->d[s0] + c->d[s1]);
+        integ_f += simpson_w(2 * m + 1, steps, hf) * sign * exp(mid) * load[s1];
+        state = evolve_common(c, state, &sign, &draws, &jumps, dt, -expm1(-c->rate[state] * dt), s);
+        const double half_ends = 0.5 * (c->d[s0] + c->d[state]);
+        coarse += dt * (c->d[s0] + c->d[state]);
+        delta += dt * (c->d[s1] - half_ends);
+        eta_f = sign * exp(coarse + delta);
+        eta_c = sign * exp(coarse);
+        integ_f += simpson_w(2 * m + 2, steps, hf) * eta_f * load[state];
+        integ_c += simpson_w(m + 1, half, hc) * eta_c * load[state];
+    }
+    orc_fem_sample r;
+    const double du = u[state] * (eta_f - eta_c);
+    const double di = integ_f - integ_c;
+    r.value = du + di;
+    r.eta_f = eta_f;
+    r.eta_c = eta_c;
+    r.integ_f = integ_f;
+    r.integ_c = integ_c;
+    r.cost = draws + (uint64_t)steps;
+    r.jumps = jumps;
+    r.end_state = state;
+    return r;
+}
+
+static int check_fem(const orc_chain* c, const double* load, int64_t entry, int level, int base) {
+    if (entry < 0 || entry >= c->n) return fail(2, "entry index outside matrix");
+    if (!load) return fail(1, "load length does not match decomposition");
+    if (!base && level < 2) return fail(1, "coupled quadrature needs a step count divisible by 4");
+    return 0;
+}
+
+int orc_fem_samples(const orc_chain* c, const double* u, const double* load, int64_t entry, double beta,
+                    int level, int base, uint64_t seed, int64_t count, const uint64_t* sample_idx,
+                    double* value, double* eta_f, double* eta_c, double* integ_f, double* integ_c,
+                    int64_t* end_state, uint64_t* cost, uint64_t* jumps) {
+    int rc = check_level(level);
+    if (rc || (rc = check_fem(c, load, entry, level, base))) return rc;
+    const int64_t steps = (int64_t)1 << level;
+    const double dt = beta / (double)steps;
+    if (!(dt > 0.0)) return fail(1, "step size must be positive");
+    for (int64_t i = 0; i < count; ++i) {
+        orc_stream s;
+        orc_stream_init(&s, seed, (uint32_t)level, sample_idx[i], ORC_LANE_FEM);
+        const orc_fem_sample r = base ? fem_single(c, u, load, entry, dt, steps, &s)
+                                      : fem_coupled(c, u, load, entry, dt, steps, &s);
+        value[i] = r.value;
+        if (eta_f) eta_f[i] = r.eta_f;
+        if (eta_c) eta_c[i] = r.eta_c;
+        if (integ_f) integ_f[i] = r.integ_f;
+        if (integ_c) integ_c[i] = r.integ_c;
+        if (end_state) end_state[i] = base ? -1 : r.end_state;
+        if (cost) cost[i] = r.cost;
+        if (jumps) jumps[i] = r.jumps;
+    }
+    return 0;
+}
+
 static int check_level(int level) {
     if (level < 0 || level > 62) return fail(1, "level outside [0, 62]");
     return 0;
@@ -399,6 +512,63 @@ int orc_run_level(const orc_chain* c, const double* u, int64_t entry, double bet
     return 0;
 }
 
+/* run_level_ex in fem mode (mlmc.cpp:76-148): the same 512-sample chunking, plus the SumAcc
+ * side channel `extra` = sum of (integ_f - integ_c) of the coupled samples (parallel.hpp:60). */
+int orc_fem_run_level(const orc_chain* c, const double* u, const double* load, int64_t entry, double beta,
+                      int level, int base, uint64_t first, uint64_t count, uint64_t seed, int threads,
+                      orc_level_stats* out, double* integ_sum) {
+    int rc = check_level(level);
+    if (rc) return rc;
+    if (entry < 0 || entry >= c->n) return fail(2, "entry index outside matrix");
+    if (!load) return fail(1, "load length does not match decomposition");
+    if (!(beta > 0.0)) return fail(1, "beta must be positive");
+    const int64_t steps = (int64_t)1 << level;
+    const double dt = beta / (double)steps;
+    memset(out, 0, sizeof *out);
+    *integ_sum = 0.0;
+    if (count == 0) return 0;
+    if (!base && level < 2) return fail(1, "coupled quadrature needs a step count divisible by 4");
+    const uint64_t first_chunk = first / ORC_CHUNK;
+    const uint64_t last_chunk = (first + count - 1) / ORC_CHUNK;
+    const int64_t nch = (int64_t)(last_chunk - first_chunk + 1);
+    orc_level_stats* part = (orc_level_stats*)calloc((size_t)nch, sizeof *part);
+    double* extra = (double*)calloc((size_t)nch, sizeof *extra);
+    if (threads <= 0) threads = 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+    for (int64_t ci = 0; ci < nch; ++ci) {
+        const uint64_t chunk = first_chunk + (uint64_t)ci;
+        const uint64_t lo = first > chunk * ORC_CHUNK ? first : chunk * ORC_CHUNK;
+        const uint64_t hi = (first + count) < (chunk + 1) * ORC_CHUNK ? (first + count) : (chunk + 1) * ORC_CHUNK;
+        orc_level_stats a = {0.0, 0.0, 0, 0, 0};
+        double ex = 0.0;
+        for (uint64_t smp = lo; smp < hi; ++smp) {
+            orc_stream s;
+            orc_stream_init(&s, seed, (uint32_t)level, smp, ORC_LANE_FEM);
+            const orc_fem_sample r = base ? fem_single(c, u, load, entry, dt, steps, &s)
+                                          : fem_coupled(c, u, load, entry, dt, steps, &s);
+            a.sum += r.value;
+            a.sum_sq += r.value * r.value;
+            a.cost += r.cost;
+            a.jumps += r.jumps;
+            ++a.samples;
+            if (!base) ex += r.integ_f - r.integ_c;
+        }
+        part[ci] = a;
+        extra[ci] = ex;
+    }
+    for (int64_t ci = 0; ci < nch; ++ci) {
+        out->sum += part[ci].sum;
+        out->sum_sq += part[ci].sum_sq;
+        out->cost += part[ci].cost;
+        out->jumps += part[ci].jumps;
+        out->samples += part[ci].samples;
+        *integ_sum += extra[ci];
+    }
+    free(part);
+    free(extra);
+    return 0;
+}
+
 /* ---------------------------------------------------------------- driver helpers */
 
 int orc_initial_level(double beta, double d_max, int* out) { /* mlmc.cpp:19-23 */
@@ -441,6 +611,7 @@ int orc_bias_estimate(int64_t n, const double* means, double* out) { /* mlmc.cpp
 typedef struct {
     double sum, sum_sq;
     uint64_t samples, cost, jumps;
+    double integ; /* fem: Level::integ_sum, mlmc.cpp:184-198 */
 } lvl_t;
 
 static double lvl_mean(const lvl_t* l) { return l->samples ? l->sum / (double)l->samples : 0.0; }
@@ -456,10 +627,11 @@ static double lvl_unit_cost(const lvl_t* l) {
 
 #define ORC_MAX_LEVELS 64
 
-/* mlmc_driver, mlmc.cpp:170-260, entry (lane 0) or forward (lane 1) mode, one run at a time */
+/* mlmc_driver, mlmc.cpp:170-260, entry (lane 0), forward (lane 1) or fem (lane 2, with load;
+ * quad = the result's quadrature_bound) mode, one run at a time */
 static int driver_one(const orc_chain* c, const double* u, int64_t entry, double beta,
-                      const orc_options* o, uint64_t seed, uint32_t lane, orc_result* res,
-                      orc_level_record* rec, int32_t max_levels) {
+                      const orc_options* o, uint64_t seed, uint32_t lane, const double* load,
+                      orc_result* res, double* quad_out, orc_level_record* rec, int32_t max_levels) {
     if (lane != ORC_LANE_FORWARD && (entry < 0 || entry >= c->n)) return fail(2, "entry index outside matrix");
     if (!(beta > 0.0)) return fail(1, "beta must be positive");
     if (!(o->epsilon > 0.0)) return fail(1, "epsilon must be positive");
@@ -470,6 +642,7 @@ static int driver_one(const orc_chain* c, const double* u, int64_t entry, double
         int rc = orc_initial_level(beta, c->d_max, &l0);
         if (rc) return rc;
     }
+    if (lane == ORC_LANE_FEM && l0 < 1) l0 = 1; /* mlmc.cpp:177 */
     const int cap = l0 + o->max_levels_above_l0;
     const double target = o->epsilon / sqrt(2.0);
     lvl_t lv[ORC_MAX_LEVELS];
@@ -478,10 +651,15 @@ static int driver_one(const orc_chain* c, const double* u, int64_t entry, double
 #define EXTEND(level, add)                                                                 \
     do {                                                                                   \
         orc_level_stats d_;                                                                \
+        double ig_ = 0.0;                                                                  \
         lvl_t* e_ = &lv[(level)-l0];                                                       \
-        int rc_ = orc_run_level(c, u, entry, beta, (level), (level) == l0, e_->samples,     \
-                                (add), seed, lane, o->threads, &d_);                       \
+        int rc_ = lane == ORC_LANE_FEM                                                     \
+                      ? orc_fem_run_level(c, u, load, entry, beta, (level), (level) == l0,  \
+                                          e_->samples, (add), seed, o->threads, &d_, &ig_) \
+                      : orc_run_level(c, u, entry, beta, (level), (level) == l0,           \
+                                      e_->samples, (add), seed, lane, o->threads, &d_);    \
         if (rc_) return rc_;                                                               \
+        e_->integ += ig_;                                                                  \
         e_->sum += d_.sum;                                                                 \
         e_->sum_sq += d_.sum_sq;                                                           \
         e_->samples += d_.samples;                                                         \
@@ -495,7 +673,7 @@ static int driver_one(const orc_chain* c, const double* u, int64_t entry, double
         ++nlv;
         EXTEND(l, o->warmup);
     }
-    double stat_error = 0.0, bias = 0.0;
+    double stat_error = 0.0, bias = 0.0, quad = 0.0;
     int converged = 0;
     for (int iter = 0; iter < o->max_iterations; ++iter) {
         double v[ORC_MAX_LEVELS], cc[ORC_MAX_LEVELS];
@@ -516,6 +694,12 @@ static int driver_one(const orc_chain* c, const double* u, int64_t entry, double
         for (int i = 1; i < nlv; ++i) means[i - 1] = lvl_mean(&lv[i]);
         rc = orc_bias_estimate(nlv - 1, means, &bias);
         if (rc) return rc;
+        if (lane == ORC_LANE_FEM) { /* quad = bias_estimate(integ_means), mlmc.cpp:226-235 */
+            double im[ORC_MAX_LEVELS];
+            for (int i = 1; i < nlv; ++i) im[i - 1] = lv[i].integ / (double)lv[i].samples;
+            rc = orc_bias_estimate(nlv - 1, im, &quad);
+            if (rc) return rc;
+        }
         if (stat_error <= target && bias <= target) {
             converged = 1;
             break;
@@ -536,6 +720,7 @@ static int driver_one(const orc_chain* c, const double* u, int64_t entry, double
     res->bias_estimate = bias;
     res->converged = converged;
     res->nlevels = nlv;
+    if (quad_out) *quad_out = quad;
     for (int i = 0; i < nlv; ++i) {
         res->estimate += lvl_mean(&lv[i]);
         res->total_cost += lv[i].cost;
@@ -557,7 +742,7 @@ int orc_mlmc_driver_rows(const orc_chain* c, const double* u, double beta, const
                          int64_t nrows, const int64_t* rows, const uint64_t* row_seed,
                          orc_result* out, orc_level_record* levels, int32_t max_levels) {
     for (int64_t r = 0; r < nrows; ++r) {
-        int rc = driver_one(c, u, rows[r], beta, o, row_seed[r], ORC_LANE_ENTRY, &out[r],
+        int rc = driver_one(c, u, rows[r], beta, o, row_seed[r], ORC_LANE_ENTRY, NULL, &out[r], NULL,
                             levels ? levels + r * max_levels : NULL, max_levels);
         if (rc) return rc;
     }
@@ -568,7 +753,18 @@ int orc_mlmc_driver_forward(const orc_chain* c, const double* u, double beta, co
                             int64_t nruns, const uint64_t* seeds, orc_result* out,
                             orc_level_record* levels, int32_t max_levels) {
     for (int64_t r = 0; r < nruns; ++r) {
-        int rc = driver_one(c, u, 0, beta, o, seeds[r], ORC_LANE_FORWARD, &out[r],
+        int rc = driver_one(c, u, 0, beta, o, seeds[r], ORC_LANE_FORWARD, NULL, &out[r], NULL,
+                            levels ? levels + r * max_levels : NULL, max_levels);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+int orc_mlmc_driver_fem(const orc_chain* c, const double* u, const double* load, double beta,
+                        const orc_options* o, int64_t nrows, const int64_t* rows, const uint64_t* row_seed,
+                        orc_result* out, double* quad, orc_level_record* levels, int32_t max_levels) {
+    for (int64_t r = 0; r < nrows; ++r) {
+        int rc = driver_one(c, u, rows[r], beta, o, row_seed[r], ORC_LANE_FEM, load, &out[r], &quad[r],
                             levels ? levels + r * max_levels : NULL, max_levels);
         if (rc) return rc;
     }

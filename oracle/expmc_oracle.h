@@ -62,6 +62,7 @@ int64_t orc_chain_edges(const orc_chain* c);
  * state is drawn from u / sum(u), and the chain must be the decomposition of A^T. */
 #define ORC_LANE_ENTRY 0u
 #define ORC_LANE_FORWARD 1u
+#define ORC_LANE_FEM 2u
 
 int orc_samples(const orc_chain* c, const double* u, int64_t entry, double beta, int level,
                 int base, uint64_t seed, uint32_t lane, int64_t count, const uint64_t* sample_idx,
@@ -119,6 +120,20 @@ int orc_mlmc_driver_rows(const orc_chain* c, const double* u, double beta, const
 int orc_mlmc_driver_forward(const orc_chain* c, const double* u, double beta, const orc_options* o,
                             int64_t nruns, const uint64_t* seeds, orc_result* out,
                             orc_level_record* levels, int32_t max_levels);
+
+/* fem mode (lane 2; LevelSampler::fem_single / fem_coupled, paths.cpp:183-245, on the chain of
+ * -M^{-1}K with load = M^{-1}F).  value = the run_level sample; for coupled samples also
+ * eta_f/eta_c/integ_f/integ_c and the terminal state (base: -1). */
+int orc_fem_samples(const orc_chain* c, const double* u, const double* load, int64_t entry, double beta,
+                    int level, int base, uint64_t seed, int64_t count, const uint64_t* sample_idx,
+                    double* value, double* eta_f, double* eta_c, double* integ_f, double* integ_c,
+                    int64_t* end_state, uint64_t* cost, uint64_t* jumps);
+int orc_fem_run_level(const orc_chain* c, const double* u, const double* load, int64_t entry, double beta,
+                      int level, int base, uint64_t first, uint64_t count, uint64_t seed, int threads,
+                      orc_level_stats* out, double* integ_sum);
+int orc_mlmc_driver_fem(const orc_chain* c, const double* u, const double* load, double beta,
+                        const orc_options* o, int64_t nrows, const int64_t* rows, const uint64_t* row_seed,
+                        orc_result* out, double* quad, orc_level_record* levels, int32_t max_levels);
 
 int orc_initial_level(double beta, double d_max, int* out);
 int orc_optimal_allocation(int64_t n, const double* v, const double* c, double eps, uint64_t* out);

@@ -11,6 +11,9 @@
 //   mlmc_driver                     mlmc.cpp:170-260
 //   dense_expmv / strang_reference  oracle.cpp:31-60, 79-99
 //   smallw / pref                   netgen.cpp:30-107
+//   forward mode                    paths.cpp:12-36, 144-181
+//   fem mode, decompose_scaled,     paths.cpp:183-245, chain.cpp:80-85, mlmc.cpp:66-75,
+//     solve_convdiff_point, io        fem.cpp:10-73, io.cpp:69-167
 // Exceptions map to status codes: 1 invalid_argument, 2 out_of_range, 3 domain_error, 9 other.
 
 #include <cstdint>
@@ -21,6 +24,9 @@
 #include <vector>
 
 #include "expmc/chain.hpp"
+#include "expmc/communicability.hpp"
+#include "expmc/fem.hpp"
+#include "expmc/io.hpp"
 #include "expmc/mlmc.hpp"
 #include "expmc/netgen.hpp"
 #include "expmc/oracle.hpp"
@@ -394,6 +400,212 @@ int ref_smallw(int64_t n, int64_t k, double p, uint64_t seed, void** out) {
         m->a = smallw(n, k, p, seed);
         m->dec = decompose(m->a);
         *out = m;
+    });
+}
+
+// ---------------------------------------------------------------- fem mode
+// decompose_scaled (chain.cpp:80-85): tables of diag(row_scale) A.
+int ref_matrix_create_scaled(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                             const double* row_scale, void** out) {
+    return guarded([&] {
+        auto* m = new RefMatrix;
+        try {
+            m->a = from_csr(n, row_ptr, col, val);
+            m->dec = decompose_scaled(m->a, std::span<const double>(row_scale, static_cast<std::size_t>(n)));
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+// scaled_simpson (mlmc.cpp:66-75) is internal to mlmc.cpp; restated for the per-sample shim.
+std::vector<double> simpson_scaled(index_t panels, double step) {
+    std::vector<double> w(static_cast<std::size_t>(panels) + 1);
+    const double h = step / 3.0;
+    for (std::size_t j = 0; j < w.size(); ++j) {
+        const bool end = (j == 0 || j + 1 == w.size());
+        w[j] = h * (end ? 1.0 : (j % 2 == 1 ? 4.0 : 2.0));
+    }
+    return w;
+}
+
+MlmcOptions to_options(const RefOptions* o) {
+    MlmcOptions opt;
+    opt.epsilon = o->epsilon;
+    opt.seed = o->seed;
+    opt.threads = o->threads;
+    opt.l0_override = o->l0_override;
+    opt.warmup = o->warmup;
+    opt.max_levels_above_l0 = o->max_levels_above_l0;
+    opt.max_iterations = o->max_iterations;
+    return opt;
+}
+
+void from_result(const MlmcResult& res, RefResult* out, RefLevel* levels_out, int32_t max_levels) {
+    out->estimate = res.estimate;
+    out->statistical_error = res.statistical_error;
+    out->bias_estimate = res.bias_estimate;
+    out->l0 = res.l0;
+    out->L = res.L;
+    out->total_cost = res.total_cost;
+    out->converged = res.converged ? 1 : 0;
+    out->nlevels = static_cast<int32_t>(res.levels.size());
+    for (std::size_t l = 0; levels_out && l < res.levels.size() && l < static_cast<std::size_t>(max_levels); ++l) {
+        levels_out[l].level = res.levels[l].level;
+        levels_out[l].pad = 0;
+        levels_out[l].sum = res.levels[l].sum;
+        levels_out[l].sum_sq = res.levels[l].sum_sq;
+        levels_out[l].samples = res.levels[l].samples;
+        levels_out[l].cost = res.levels[l].cost;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+// fem_single / fem_coupled (paths.cpp:183-245) with run_level_ex's weights (mlmc.cpp:89-92),
+// stream_for(seed, level, idx[i], 2).  value = the run_level sample: fem_single's value, or
+// u[terminal] (eta_f - eta_c) + (integ_f - integ_c) (mlmc.cpp:126-133).
+int ref_fem_samples(void* h, const double* u, const double* load, int64_t entry, double beta, int level, int base,
+                    uint64_t seed, int64_t count, const uint64_t* sample_idx, double* value, double* eta_f,
+                    double* eta_c, double* integ_f, double* integ_c, int64_t* terminal, uint64_t* cost) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        const std::size_t n = static_cast<std::size_t>(m->dec.n);
+        const index_t steps = index_t{1} << level;
+        const double dt = beta / static_cast<double>(steps);
+        const LevelSampler sampler(m->dec, dt, steps);
+        const std::vector<double> fw = simpson_scaled(steps, dt);
+        const std::vector<double> cw = base ? std::vector<double>{} : simpson_scaled(steps / 2, 2.0 * dt);
+        const std::span<const double> us(u, n), ls(load, n);
+        for (int64_t i = 0; i < count; ++i) {
+            RngStream s = stream_for(seed, static_cast<uint32_t>(level), sample_idx[i], 2u);
+            if (base) {
+                const FemSample f = sampler.fem_single(us, ls, entry, fw, s);
+                value[i] = f.value;
+                eta_f[i] = eta_c[i] = integ_f[i] = integ_c[i] = 0.0;
+                terminal[i] = -1;
+                cost[i] = f.cost;
+            } else {
+                const FemCoupledSample c = sampler.fem_coupled(ls, entry, fw, cw, s);
+                const double du = u[c.terminal_state] * (c.eta_fine - c.eta_coarse);
+                const double di = c.integ_fine - c.integ_coarse;
+                value[i] = du + di;
+                eta_f[i] = c.eta_fine;
+                eta_c[i] = c.eta_coarse;
+                integ_f[i] = c.integ_fine;
+                integ_c[i] = c.integ_coarse;
+                terminal[i] = c.terminal_state;
+                cost[i] = c.cost;
+            }
+        }
+    });
+}
+
+int ref_fem_run_level(void* h, const double* u, const double* load, int64_t entry, double beta, int level, int base,
+                      uint64_t first, uint64_t count, uint64_t seed, int threads, double* sum, double* sum_sq,
+                      uint64_t* samples, uint64_t* cost) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.load = std::span<const double>(load, static_cast<std::size_t>(m->dec.n));
+        p.entry = entry;
+        p.beta = beta;
+        p.mode = SampleMode::fem;
+        const LevelStats st = run_level(p, level, base != 0, first, count, seed, threads);
+        *sum = st.sum;
+        *sum_sq = st.sum_sq;
+        *samples = st.samples;
+        *cost = st.cost;
+    });
+}
+
+int ref_fem_driver(void* h, const double* u, const double* load, int64_t entry, double beta, const RefOptions* o,
+                   RefResult* out, RefLevel* levels_out, int32_t max_levels, double* quadrature_bound) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.load = std::span<const double>(load, static_cast<std::size_t>(m->dec.n));
+        p.entry = entry;
+        p.beta = beta;
+        p.mode = SampleMode::fem;
+        const MlmcResult res = mlmc_driver(p, to_options(o));
+        from_result(res, out, levels_out, max_levels);
+        *quadrature_bound = res.quadrature_bound;
+    });
+}
+
+// solve_convdiff_point (fem.cpp:51-73) on a FemSystem given by arrays.
+int ref_solve_convdiff_point(int64_t n, const double* mass_diag, const int64_t* row_ptr, const int64_t* col,
+                             const double* val, const double* load, const double* u0, int64_t node, double t,
+                             const RefOptions* o, RefResult* out, RefLevel* levels_out, int32_t max_levels,
+                             double* quadrature_bound) {
+    return guarded([&] {
+        FemSystem sys;
+        sys.mass_diag.assign(mass_diag, mass_diag + n);
+        sys.stiffness = from_csr(n, row_ptr, col, val);
+        sys.load.assign(load, load + n);
+        sys.u0.assign(u0, u0 + n);
+        const MlmcResult res = solve_convdiff_point(sys, node, t, to_options(o));
+        from_result(res, out, levels_out, max_levels);
+        *quadrature_bound = res.quadrature_bound;
+    });
+}
+
+// load_fem_system (fem.cpp:12-37): sizes first (arrays NULL), then the data.
+int ref_load_fem_system(const char* mass, const char* stiffness, const char* load_path, const char* u0_path,
+                        int64_t* n, int64_t* nnz, double* mass_diag, int64_t* row_ptr, int64_t* col, double* val,
+                        double* load, double* u0) {
+    return guarded([&] {
+        const FemSystem sys = load_fem_system(mass, stiffness, load_path, u0_path);
+        *n = sys.size();
+        *nnz = sys.stiffness.nnz();
+        if (!mass_diag) return;
+        std::memcpy(mass_diag, sys.mass_diag.data(), sys.mass_diag.size() * sizeof(double));
+        export_csr(sys.stiffness, row_ptr, col, val);
+        std::memcpy(load, sys.load.data(), sys.load.size() * sizeof(double));
+        std::memcpy(u0, sys.u0.data(), sys.u0.size() * sizeof(double));
+    });
+}
+
+// read_matrix_market (io.cpp:69-128) -> matrix handle; read_vector (io.cpp:154-167).
+int ref_read_matrix_market(const char* path, void** out) {
+    return guarded([&] {
+        auto* m = new RefMatrix;
+        try {
+            m->a = read_matrix_market(path);
+            m->dec = decompose(m->a);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+int ref_read_vector(const char* path, int64_t cap, double* out, int64_t* n) {
+    return guarded([&] {
+        const std::vector<double> v = read_vector(path);
+        *n = static_cast<int64_t>(v.size());
+        if (out) std::memcpy(out, v.data(), std::min<int64_t>(cap, *n) * sizeof(double));
+    });
+}
+
+int ref_total_communicability(void* h, double beta, const RefOptions* o, RefResult* out) {
+    return guarded([&] {
+        const MlmcResult res = total_communicability(static_cast<RefMatrix*>(h)->a,
+                                                     beta > 0.0 ? std::optional<double>(beta) : std::nullopt,
+                                                     to_options(o));
+        from_result(res, out, nullptr, 0);
     });
 }
 

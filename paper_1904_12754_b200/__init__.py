@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     ExpmcError,
     InvalidArgument,
     LANE_ENTRY,
+    LANE_FEM,
     LANE_FORWARD,
     LevelStats,
     MlmcOptions,
@@ -27,7 +28,11 @@ from .api import (  # noqa: F401
     device_count,
     initial_level,
     mlmc_driver,
+    FemSystem,
+    fem_context,
+    mlmc_driver_fem,
     mlmc_driver_forward,
+    solve_convdiff_point,
     node_communicability,
     spectral_scale,
     total_communicability,

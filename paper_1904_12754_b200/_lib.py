@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("EXPMC_LIB") or os.path.join(_HERE, "_lib", "libexpmc_
 _I32, _I64, _U32, _U64, _D = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 
 EXPMC_OK, EXPMC_EINVAL, EXPMC_ERANGE, EXPMC_EDOMAIN, EXPMC_ECUDA, EXPMC_ENOTIMPL, EXPMC_EINTERNAL = 0, 1, 2, 3, 4, 5, 9
-LANE_ENTRY, LANE_FORWARD = 0, 1
+LANE_ENTRY, LANE_FORWARD, LANE_FEM = 0, 1, 2
 SAMPLER_REFERENCE, SAMPLER_EVENT = 0, 1
 
 
@@ -32,7 +32,7 @@ class LevelReq(C.Structure):
 
 
 class LevelStatsC(C.Structure):
-    _fields_ = [("sum", _D), ("sum_sq", _D), ("samples", _U64), ("cost", _U64), ("jumps", _U64)]
+    _fields_ = [("sum", _D), ("sum_sq", _D), ("samples", _U64), ("cost", _U64), ("jumps", _U64), ("integ_sum", _D)]
 
 
 class OptionsC(C.Structure):
@@ -43,7 +43,13 @@ class OptionsC(C.Structure):
 class ResultC(C.Structure):
     _fields_ = [("estimate", _D), ("statistical_error", _D), ("bias_estimate", _D), ("l0", _I32), ("L", _I32),
                 ("total_cost", _U64), ("converged", _I32), ("nlevels", _I32), ("total_jumps", _U64),
-                ("total_samples", _U64), ("projected_cost", _D), ("over_budget", _I32), ("pad", _I32)]
+                ("total_samples", _U64), ("projected_cost", _D), ("over_budget", _I32), ("pad", _I32),
+                ("quadrature_bound", _D)]
+
+
+class SampleRecordC(C.Structure):
+    _fields_ = [("eta_fine", _D), ("eta_coarse", _D), ("value", _D), ("integ_fine", _D), ("integ_coarse", _D),
+                ("cost", _U64), ("jumps", _U64), ("end_state", _I64)]
 
 
 class LevelRecordC(C.Structure):
@@ -65,7 +71,9 @@ SYMBOLS = [
     ("expmc_ctx_create", C.c_int, [C.POINTER(Csr), _P, C.c_int, C.POINTER(_P)]),
     ("expmc_ctx_destroy", None, [_P]),
     ("expmc_ctx_get_info", C.c_int, [_P, C.POINTER(CtxInfo)]),
+    ("expmc_ctx_create_scaled", C.c_int, [C.POINTER(Csr), _P, _P, C.c_int, C.POINTER(_P)]),
     ("expmc_ctx_set_vector", C.c_int, [_P, _P]),
+    ("expmc_ctx_set_load", C.c_int, [_P, _P]),
     ("expmc_ctx_export_tables", C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     ("expmc_ctx_get_counters", C.c_int, [_P, C.POINTER(CountersC)]),
     ("expmc_ctx_reset_counters", C.c_int, [_P]),
@@ -81,6 +89,9 @@ SYMBOLS = [
     ("expmc_run_level_forward", C.c_int, [_P, _D, _I32, _I32, _U64, _U64, _U64, C.POINTER(LevelStatsC)]),
     ("expmc_run_level_batch", C.c_int, [_P, _D, _U32, _I64, _P, _P]),
     ("expmc_sample_debug", C.c_int, [_P, _D, _U32, _I64, _P, _P, _P, _P, _P, _P]),
+    ("expmc_sample_debug_ex", C.c_int, [_P, _D, _U32, _I64, _P, _P]),
+    ("expmc_run_level_fem", C.c_int, [_P, _I64, _D, _I32, _I32, _U64, _U64, _U64, C.POINTER(LevelStatsC)]),
+    ("expmc_mlmc_driver_fem", C.c_int, [_P, _D, C.POINTER(OptionsC), _I64, _P, _P, _P, _P, _I32]),
     ("expmc_mlmc_driver", C.c_int, [_P, _I64, _D, C.POINTER(OptionsC), C.POINTER(ResultC), _P, _I32]),
     ("expmc_mlmc_driver_rows", C.c_int, [_P, _D, C.POINTER(OptionsC), _I64, _P, _P, _P, _P, _I32]),
     ("expmc_mlmc_driver_forward", C.c_int, [_P, _D, C.POINTER(OptionsC), _I64, _P, _P, _P, _I32]),

@@ -30,7 +30,7 @@ import numpy as np
 from . import _lib as L
 
 
-LANE_ENTRY, LANE_FORWARD = L.LANE_ENTRY, L.LANE_FORWARD  # Philox lanes (mlmc.cpp:94-96)
+LANE_ENTRY, LANE_FORWARD, LANE_FEM = L.LANE_ENTRY, L.LANE_FORWARD, L.LANE_FEM  # Philox lanes (mlmc.cpp:94-96)
 
 
 class ExpmcError(RuntimeError):
@@ -218,7 +218,10 @@ class Context:
 
     SAMPLERS = {"reference": L.SAMPLER_REFERENCE, "event": L.SAMPLER_EVENT}
 
-    def __init__(self, a: SparseMatrix, u, device: int = 0, sampler: str = "reference"):
+    def __init__(self, a: SparseMatrix, u, device: int = 0, sampler: str = "reference", row_scale=None,
+                 load=None):
+        """row_scale: decompose_scaled (chain.cpp:80-85), the tables of diag(row_scale) A;
+        load: the fem load vector (MlmcProblem::load)."""
         self._h = C.c_void_p()
         u = np.ascontiguousarray(u, np.float64)
         if u.shape != (a.n,):
@@ -227,7 +230,13 @@ class Context:
         col = np.ascontiguousarray(a.col, np.int64)
         val = np.ascontiguousarray(a.val, np.float64)
         csr = L.Csr(a.n, int(rp[-1]) if len(rp) else 0, _ptr(rp), _ptr(col), _ptr(val))
-        _check(L.lib.expmc_ctx_create(C.byref(csr), _ptr(u), device, C.byref(self._h)))
+        if row_scale is None:
+            _check(L.lib.expmc_ctx_create(C.byref(csr), _ptr(u), device, C.byref(self._h)))
+        else:
+            sc = np.ascontiguousarray(row_scale, np.float64)
+            if sc.shape != (a.n,):
+                raise InvalidArgument("row scale length does not match matrix dimension")
+            _check(L.lib.expmc_ctx_create_scaled(C.byref(csr), _ptr(sc), _ptr(u), device, C.byref(self._h)))
         info = L.CtxInfo()
         _check(L.lib.expmc_ctx_get_info(self._h, C.byref(info)))
         self.n = info.n
@@ -238,6 +247,8 @@ class Context:
         self.num_sms = info.num_sms
         self.table_bytes = info.table_bytes
         self.set_sampler(sampler)
+        if load is not None:
+            self.set_load(load)
 
     def set_sampler(self, sampler: str):
         """'reference' (draw-for-draw the reference's sampler, exact parity) or 'event'
@@ -273,6 +284,28 @@ class Context:
         if u.shape != (self.n,):
             raise InvalidArgument("vector length does not match decomposition")
         _check(L.lib.expmc_ctx_set_vector(self._h, _ptr(u)))
+
+    def set_load(self, load):
+        """MlmcProblem::load for fem mode (length n)."""
+        g = np.ascontiguousarray(load, np.float64)
+        if g.shape != (self.n,):
+            raise InvalidArgument("load length does not match decomposition")
+        _check(L.lib.expmc_ctx_set_load(self._h, _ptr(g)))
+
+    def sample_records(self, beta: float, entry, level, base_level, seed, sample_idx,
+                       lane: int = L.LANE_ENTRY) -> np.ndarray:
+        """Per-sample records of any lane (SAMPLE_RECORD_DT: eta_fine, eta_coarse, value,
+        integ_fine, integ_coarse, cost, jumps, end_state)."""
+        e, lv, b, sd, i = np.broadcast_arrays(np.asarray(entry, np.int64), np.asarray(level, np.int32),
+                                              np.asarray(base_level, np.int32), np.asarray(seed, np.uint64),
+                                              np.asarray(sample_idx, np.uint64))
+        k = e.size
+        req = np.zeros(k, _REQ_DT)
+        req["entry"], req["seed"], req["first_index"] = e.ravel(), sd.ravel(), i.ravel()
+        req["count"], req["level"], req["base_level"] = 1, lv.ravel(), b.ravel()
+        out = np.zeros(k, SAMPLE_RECORD_DT)
+        _check(L.lib.expmc_sample_debug_ex(self._h, beta, lane, k, _ptr(req), _ptr(out)))
+        return out
 
     def decomposition(self) -> dict:
         n, m = self.n, self.n_edges
@@ -354,22 +387,26 @@ class Context:
 _REQ_DT = np.dtype([("entry", np.int64), ("seed", np.uint64), ("first_index", np.uint64), ("count", np.uint64),
                     ("level", np.int32), ("base_level", np.int32)])
 _STATS_DT = np.dtype([("sum", np.float64), ("sum_sq", np.float64), ("samples", np.uint64), ("cost", np.uint64),
-                      ("jumps", np.uint64)])
+                      ("jumps", np.uint64), ("integ_sum", np.float64)])
 _RESULT_DT = np.dtype([("estimate", np.float64), ("statistical_error", np.float64), ("bias_estimate", np.float64),
                        ("l0", np.int32), ("L", np.int32), ("total_cost", np.uint64), ("converged", np.int32),
                        ("nlevels", np.int32), ("total_jumps", np.uint64), ("total_samples", np.uint64),
-                       ("projected_cost", np.float64), ("over_budget", np.int32), ("pad", np.int32)])
+                       ("projected_cost", np.float64), ("over_budget", np.int32), ("pad", np.int32),
+                       ("quadrature_bound", np.float64)])
+SAMPLE_RECORD_DT = np.dtype([("eta_fine", np.float64), ("eta_coarse", np.float64), ("value", np.float64),
+                             ("integ_fine", np.float64), ("integ_coarse", np.float64), ("cost", np.uint64),
+                             ("jumps", np.uint64), ("end_state", np.int64)])
 LEVEL_RECORD_DT = np.dtype([("level", np.int32), ("pad", np.int32), ("sum", np.float64), ("sum_sq", np.float64),
                             ("samples", np.uint64), ("cost", np.uint64)])
 assert _REQ_DT.itemsize == C.sizeof(L.LevelReq)
 assert _STATS_DT.itemsize == C.sizeof(L.LevelStatsC)
 assert _RESULT_DT.itemsize == C.sizeof(L.ResultC)
 assert LEVEL_RECORD_DT.itemsize == C.sizeof(L.LevelRecordC)
+assert SAMPLE_RECORD_DT.itemsize == C.sizeof(L.SampleRecordC)
 
 
 class SampleMode(enum.IntEnum):
-    """mlmc.hpp:45.  fem is outside this build's scope and raises
-    NotImplementedMode."""
+    """mlmc.hpp:45."""
 
     entry = 0
     forward = 1
@@ -388,19 +425,20 @@ class MlmcProblem:
 
 
 def _mode(problem: MlmcProblem) -> SampleMode:
-    m = SampleMode(problem.mode)
-    if m == SampleMode.fem:
-        raise NotImplementedMode("fem sampling (lane 2) is not built")
-    return m
+    return SampleMode(problem.mode)
 
 
 def run_level(problem: MlmcProblem, level: int, base_level: bool, first_index: int, additional: int,
               seed: int, threads: int = 0) -> LevelStats:
     """mlmc.hpp:86-88."""
     out = L.LevelStatsC()
-    if _mode(problem) == SampleMode.forward:
+    mode = _mode(problem)
+    if mode == SampleMode.forward:
         _check(L.lib.expmc_run_level_forward(problem.ctx.handle, problem.beta, level, int(bool(base_level)),
                                              first_index, additional, seed, C.byref(out)))
+    elif mode == SampleMode.fem:
+        _check(L.lib.expmc_run_level_fem(problem.ctx.handle, problem.entry, problem.beta, level,
+                                         int(bool(base_level)), first_index, additional, seed, C.byref(out)))
     else:
         _check(L.lib.expmc_run_level(problem.ctx.handle, problem.entry, problem.beta, level, int(bool(base_level)),
                                      first_index, additional, seed, C.byref(out)))
@@ -410,7 +448,8 @@ def run_level(problem: MlmcProblem, level: int, base_level: bool, first_index: i
 def _result(r, levels) -> MlmcResult:
     lv = [LevelStats(int(x["level"]), float(x["sum"]), float(x["sum_sq"]), int(x["samples"]), int(x["cost"]))
           for x in levels]
-    return MlmcResult(float(r["estimate"]), float(r["statistical_error"]), float(r["bias_estimate"]), 0.0, lv,
+    return MlmcResult(float(r["estimate"]), float(r["statistical_error"]), float(r["bias_estimate"]),
+                      float(r["quadrature_bound"]), lv,
                       int(r["l0"]), int(r["L"]), int(r["total_cost"]), bool(r["converged"]), int(r["total_jumps"]),
                       int(r["total_samples"]), float(r["projected_cost"]), bool(r["over_budget"]))
 
@@ -420,9 +459,15 @@ def mlmc_driver(problem: MlmcProblem, options: MlmcOptions = MlmcOptions(), max_
     res = np.zeros(1, _RESULT_DT)
     lv = np.zeros(max_levels, LEVEL_RECORD_DT)
     o = options._c()
-    if _mode(problem) == SampleMode.forward:
+    mode = _mode(problem)
+    if mode == SampleMode.forward:
         _check(L.lib.expmc_mlmc_driver_forward(problem.ctx.handle, problem.beta, C.byref(o), 1, None, _ptr(res),
                                                _ptr(lv), max_levels))
+    elif mode == SampleMode.fem:
+        rows = np.array([problem.entry], np.int64)
+        seeds = np.array([options.seed], np.uint64)
+        _check(L.lib.expmc_mlmc_driver_fem(problem.ctx.handle, problem.beta, C.byref(o), 1, _ptr(rows), _ptr(seeds),
+                                           _ptr(res), _ptr(lv), max_levels))
     else:
         _check(L.lib.expmc_mlmc_driver(problem.ctx.handle, problem.entry, problem.beta, C.byref(o),
                                        C.cast(_ptr(res), C.POINTER(L.ResultC)), _ptr(lv), max_levels))
@@ -457,6 +502,54 @@ def mlmc_driver_rows(ctx: Context, beta: float, rows, row_seeds, options: MlmcOp
     _check(L.lib.expmc_mlmc_driver_rows(ctx.handle, beta, C.byref(o), rows.size, _ptr(rows), _ptr(seeds), _ptr(res),
                                         _ptr(lv), max_levels))
     return res, lv
+
+
+def mlmc_driver_fem(ctx: Context, beta: float, rows, row_seeds, options: MlmcOptions = MlmcOptions(),
+                    max_levels: int = 64, want_levels: bool = True):
+    """fem-mode driver for many entries (lane 2): one reference decision sequence per row,
+    batched; results carry quadrature_bound."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    seeds = np.ascontiguousarray(row_seeds, np.uint64)
+    if seeds.shape != rows.shape:
+        raise InvalidArgument("one seed per row required")
+    res = np.zeros(rows.size, _RESULT_DT)
+    lv = np.zeros((rows.size, max_levels), LEVEL_RECORD_DT) if want_levels else None
+    o = options._c()
+    _check(L.lib.expmc_mlmc_driver_fem(ctx.handle, beta, C.byref(o), rows.size, _ptr(rows), _ptr(seeds), _ptr(res),
+                                       _ptr(lv), max_levels))
+    return res, lv
+
+
+@dataclass
+class FemSystem:
+    """fem.hpp FemSystem: lumped-mass system M u' = -K u + F, u(0) = u0."""
+
+    mass_diag: np.ndarray
+    stiffness: SparseMatrix
+    load: np.ndarray
+    u0: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.stiffness.n
+
+
+def fem_context(sys: FemSystem, device: int = 0) -> Context:
+    """The chain of -M^{-1}K with u0 and the load M^{-1}F bound (fem.cpp:58-64)."""
+    md = np.asarray(sys.mass_diag, np.float64)
+    return Context(sys.stiffness, sys.u0, device, row_scale=-1.0 / md,
+                   load=np.asarray(sys.load, np.float64) / md)
+
+
+def solve_convdiff_point(sys: FemSystem, node: int, t: float, options: MlmcOptions = MlmcOptions(),
+                         device: int = 0) -> MlmcResult:
+    """fem.cpp:51-73: u(node, t) of the inhomogeneous system by fem-mode MLMC."""
+    if not t > 0.0:
+        raise InvalidArgument("time must be positive")
+    if node < 0 or node >= sys.n:
+        raise OutOfRange("node index outside system")
+    with fem_context(sys, device) as ctx:
+        return mlmc_driver(MlmcProblem(ctx, node, t, SampleMode.fem), options)
 
 
 def spectral_scale(ctx: Context) -> float:

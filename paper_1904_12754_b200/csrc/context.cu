@@ -27,6 +27,7 @@ struct expmc_ctx {
     int sampler_grid = 0;       // persistent grid of the active sampler
     int sampler_grid_ref = 0;
     int sampler_grid_ed = 0;
+    int sampler_grid_fem = 0;
     int sampler = EXPMC_SAMPLER_REFERENCE;
     cudaStream_t stream = nullptr;
     int64_t n = 0;
@@ -46,7 +47,7 @@ struct expmc_ctx {
     uint64_t* h_chunk0 = nullptr;
     Partial* h_totals = nullptr;
     size_t cap_h = 0;
-    double* d_pf = nullptr;          // chunk partials window: sum | sum_sq
+    double* d_pf = nullptr;          // chunk partials window: sum | sum_sq | extra
     unsigned long long* d_pu = nullptr;  //                    cost | jumps
     uint64_t cap_partials = 0;
     uint64_t last_window = 0;
@@ -60,6 +61,7 @@ struct expmc_ctx {
     double* d_init_cdf = nullptr;
     double init_total = 0.0;
     bool init_valid = false;
+    double* d_load = nullptr;  // fem: MlmcProblem::load (mlmc.hpp:53), set by expmc_ctx_set_load
     SampleOut* d_dbg = nullptr;
     size_t cap_dbg = 0;
 
@@ -208,6 +210,7 @@ void nccl_allreduce_partials(ncclComm_t comm, const ChunkPartials& p, uint64_t w
     nccl_check(n.group_start(), "ncclGroupStart");
     nccl_check(n.all_reduce(p.sum, p.sum, w, ncclFloat64, ncclSum, comm, s), "ncclAllReduce");
     nccl_check(n.all_reduce(p.sum_sq, p.sum_sq, w, ncclFloat64, ncclSum, comm, s), "ncclAllReduce");
+    nccl_check(n.all_reduce(p.extra, p.extra, w, ncclFloat64, ncclSum, comm, s), "ncclAllReduce");
     nccl_check(n.all_reduce(p.cost, p.cost, w, ncclUint64, ncclSum, comm, s), "ncclAllReduce");
     nccl_check(n.all_reduce(p.jumps, p.jumps, w, ncclUint64, ncclSum, comm, s), "ncclAllReduce");
     nccl_check(n.group_end(), "ncclGroupEnd");
@@ -244,9 +247,11 @@ void ensure_forward_init(expmc_ctx* c) {
     c->init_valid = true;
 }
 
-ForwardInit forward_init(const expmc_ctx* c) {
-    return c->init_valid ? ForwardInit{c->d_init_cdf, c->init_total, static_cast<uint32_t>(c->n)}
-                         : ForwardInit{nullptr, 0.0, 0u};
+LaneData lane_data(const expmc_ctx* c) {
+    LaneData ld = c->init_valid ? LaneData{c->d_init_cdf, c->init_total, static_cast<uint32_t>(c->n), nullptr}
+                                : LaneData{nullptr, 0.0, 0u, nullptr};
+    ld.load = c->d_load;
+    return ld;
 }
 
 DevItem make_item(const expmc_level_req& r, double beta, uint32_t lane) {
@@ -257,7 +262,7 @@ DevItem make_item(const expmc_level_req& r, double beta, uint32_t lane) {
     it.count = r.count;
     it.dt = beta / static_cast<double>(steps);  // mlmc.cpp:81
     it.nsteps = steps;
-    it.entry = lane == EXPMC_LANE_FORWARD ? 0u : static_cast<uint32_t>(r.entry);
+    it.entry = lane == EXPMC_LANE_FORWARD ? 0u : static_cast<uint32_t>(r.entry);  // fem: entry mode's entry
     it.key3 = (static_cast<uint32_t>(r.level) & 0xFFFFFFu) | (lane << 24);  // rng.hpp:29
     it.base = r.base_level ? 1u : 0u;
     it.mode = lane;
@@ -266,12 +271,18 @@ DevItem make_item(const expmc_level_req& r, double beta, uint32_t lane) {
 
 // validate_problem (mlmc.cpp:150-159) + run_level_ex's level check (mlmc.cpp:79) + the
 // coupled even-step check (paths.cpp:119).
-// Forward requests carry no entry (the start state is drawn from u).
+// Forward requests carry no entry (the start state is drawn from u).  fem requests need the
+// load (validate_problem, mlmc.cpp:156-157) and, when coupled, a step count divisible by 4
+// (fem_coupled, paths.cpp:212-213; raised per sample, so only for count > 0).
 void validate_req(const expmc_ctx* c, const expmc_level_req& r, double beta, uint32_t lane) {
     if (lane != EXPMC_LANE_FORWARD) need(r.entry >= 0 && r.entry < c->n, EXPMC_ERANGE, "entry index outside matrix");
+    if (lane == EXPMC_LANE_FEM)
+        need(c->d_load != nullptr, EXPMC_EINVAL, "load length does not match decomposition");
     need(beta > 0.0, EXPMC_EINVAL, "beta must be positive");
     need(r.level >= 0 && r.level <= 62, EXPMC_EINVAL, "level outside [0, 62]");
     need(beta / static_cast<double>(uint64_t{1} << r.level) > 0.0, EXPMC_EINVAL, "step size must be positive");
+    if (lane == EXPMC_LANE_FEM && !r.base_level && r.level < 2 && r.count > 0)
+        throw Status(EXPMC_EINVAL, "coupled quadrature needs a step count divisible by 4");
     if (!r.base_level && r.level == 0 && r.count > 0)
         throw Status(EXPMC_EINVAL, "coupled sampling needs an even step count");
 }
@@ -282,6 +293,8 @@ namespace expmc_b200 {
 
 void set_error(const std::string& m) { g_err = m; }
 
+bool ctx_has_load(const expmc_ctx* c) { return c->d_load != nullptr; }
+
 void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
                      expmc_level_stats* out) {
     bind(c);
@@ -289,7 +302,7 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
     int64_t bad = nreq;
 #pragma omp parallel for schedule(static) reduction(min : bad)
     for (int64_t i = 0; i < nreq; ++i) {
-        out[i] = expmc_level_stats{0.0, 0.0, 0, 0, 0};
+        out[i] = expmc_level_stats{0.0, 0.0, 0, 0, 0, 0.0};
         try {
             validate_req(c, req[i], beta, lane);
         } catch (const Status&) {
@@ -332,11 +345,14 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
     cuda_check(cudaMemsetAsync(c->d_totals, 0, nitems * sizeof(Partial), c->stream), "memset totals");
     if (!c->d_pf) {
         c->cap_partials = kWindowChunks;
-        dev_alloc(&c->d_pf, 2 * c->cap_partials);
+        dev_alloc(&c->d_pf, 3 * c->cap_partials);
         dev_alloc(&c->d_pu, 2 * c->cap_partials);
         dev_alloc(&c->d_counter, 1);
     }
-    const ChunkPartials cp{c->d_pf, c->d_pf + c->cap_partials, c->d_pu, c->d_pu + c->cap_partials};
+    const ChunkPartials cp{c->d_pf, c->d_pf + c->cap_partials, c->d_pf + 2 * c->cap_partials, c->d_pu,
+                           c->d_pu + c->cap_partials};
+    const bool fem = lane == EXPMC_LANE_FEM;
+    const int sampler_grid = fem ? c->sampler_grid_fem : c->sampler_grid;
     const uint32_t world = static_cast<uint32_t>(c->shard_world);
     const int warps_per_block = sampler_threads() / 32;
     size_t nev = 0;
@@ -347,6 +363,7 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         if (world > 1) {  // chunks sampled by the other ranks stay exactly zero here
             cuda_check(cudaMemsetAsync(cp.sum, 0, w * sizeof(double), c->stream), "memset partials");
             cuda_check(cudaMemsetAsync(cp.sum_sq, 0, w * sizeof(double), c->stream), "memset partials");
+            cuda_check(cudaMemsetAsync(cp.extra, 0, w * sizeof(double), c->stream), "memset partials");
             cuda_check(cudaMemsetAsync(cp.cost, 0, w * sizeof(uint64_t), c->stream), "memset partials");
             cuda_check(cudaMemsetAsync(cp.jumps, 0, w * sizeof(uint64_t), c->stream), "memset partials");
         }
@@ -362,24 +379,24 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         a.counter = c->d_counter;
         a.shard_rank = static_cast<uint32_t>(c->shard_rank);
         a.shard_world = world;
-        a.init = forward_init(c);
+        a.init = lane_data(c);
         const uint64_t own = (w + world - 1) / world;
         const uint64_t want_blocks = (own + warps_per_block - 1) / warps_per_block;
-        const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(c->sampler_grid, want_blocks)));
+        const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(sampler_grid, want_blocks)));
         while (c->ev.size() < 2 * (nev + 1)) {
             cudaEvent_t e;
             cuda_check(cudaEventCreate(&e), "cudaEventCreate");
             c->ev.push_back(e);
         }
         cuda_check(cudaEventRecord(c->ev[2 * nev], c->stream), "event");
-        launch_sampler(a, grid, c->sampler, forward, c->stream);
+        launch_sampler(a, grid, c->sampler, lane, c->stream);
         cuda_check(cudaEventRecord(c->ev[2 * nev + 1], c->stream), "event");
         ++nev;
         if (c->nccl) {  // exact cross-GPU sum of the window's chunk partials (one rank non-zero per chunk)
             nccl_allreduce_partials(c->nccl, cp, w, c->cap_partials, c->stream);
-            c->ctr.nccl_bytes += 2 * w * (sizeof(double) + sizeof(uint64_t));
+            c->ctr.nccl_bytes += w * (3 * sizeof(double) + 2 * sizeof(uint64_t));
         }
-        launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, c->d_totals, c->stream);
+        launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, fem, c->d_totals, c->stream);
         c->ctr.kernel_launches += 2;
         c->ctr.sampler_launches += 1;
         c->last_window = w;
@@ -403,6 +420,7 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         o.samples = r.count;
         o.cost = c->h_totals[k].cost;
         o.jumps = c->h_totals[k].jumps;
+        o.integ_sum = c->h_totals[k].extra;
         samples += r.count;
         jumps += o.jumps;
         steps += r.count << r.level;
@@ -410,6 +428,37 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
     c->ctr.samples += samples;
     c->ctr.jumps += jumps;
     c->ctr.fine_steps += steps;
+}
+
+// Per-sample records of any lane (one debug launch): the shared body of expmc_sample_debug[_ex].
+std::vector<SampleOut> sample_debug(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq,
+                                    const expmc_level_req* req) {
+    need(lane <= EXPMC_LANE_FEM, EXPMC_ENOTIMPL, "unknown sampling lane (0 entry, 1 forward, 2 fem)");
+    std::vector<SampleOut> o(static_cast<size_t>(nreq > 0 ? nreq : 0));
+    if (nreq == 0) return o;
+    bind(c);
+    std::vector<DevItem> items(static_cast<size_t>(nreq));
+    for (int64_t i = 0; i < nreq; ++i) {
+        expmc_level_req r = req[i];
+        r.count = 1;
+        validate_req(c, r, beta, lane);
+        items[i] = make_item(r, beta, lane);
+    }
+    if (lane == EXPMC_LANE_FORWARD) ensure_forward_init(c);
+    ensure_items(c, static_cast<size_t>(nreq));
+    if (static_cast<size_t>(nreq) > c->cap_dbg) {
+        dev_alloc(&c->d_dbg, nreq);
+        c->cap_dbg = nreq;
+    }
+    cuda_check(cudaMemcpyAsync(c->d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
+               "H2D");
+    launch_debug(c->rows, c->edges(), c->d_items, static_cast<uint32_t>(nreq), lane_data(c), c->d_dbg, c->sampler,
+                 lane, c->stream);
+    c->ctr.kernel_launches += 1;
+    cuda_check(cudaMemcpyAsync(o.data(), c->d_dbg, nreq * sizeof(SampleOut), cudaMemcpyDeviceToHost, c->stream),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sample debug");
+    return o;
 }
 
 }  // namespace expmc_b200
@@ -452,6 +501,7 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
             cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
             c->sampler_grid_ref = c->num_sms * sampler_blocks_per_sm(EXPMC_SAMPLER_REFERENCE);
             c->sampler_grid_ed = c->num_sms * sampler_blocks_per_sm(EXPMC_SAMPLER_EVENT);
+            c->sampler_grid_fem = c->num_sms * sampler_blocks_per_sm(kSamplerFem);
             c->sampler_grid = c->sampler_grid_ref;
             c->n = n;
             if (n > 0) {
@@ -539,6 +589,7 @@ void expmc_ctx_destroy(expmc_ctx* c) {
     if (c->nccl) nccl().comm_destroy(c->nccl);
     cudaFree(c->d_counter);
     cudaFree(c->d_init_cdf);
+    cudaFree(c->d_load);
     cudaFree(c->d_dbg);
     if (c->cap_h) {  // staging blocks go back to the process-wide pool
         pinned_put(c->h_items, c->cap_h * sizeof(DevItem));
@@ -731,12 +782,20 @@ int expmc_run_level_forward(expmc_ctx* c, double beta, int32_t level, int32_t ba
     });
 }
 
+int expmc_run_level_fem(expmc_ctx* c, int64_t entry, double beta, int32_t level, int32_t base_level,
+                        uint64_t first_index, uint64_t additional, uint64_t seed, expmc_level_stats* out) {
+    return guarded([&] {
+        need(c && out, EXPMC_EINVAL, "null argument");
+        expmc_level_req r{entry, seed, first_index, additional, level, base_level};
+        run_level_batch(c, beta, EXPMC_LANE_FEM, &r, 1, out);
+    });
+}
+
 int expmc_run_level_batch(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, const expmc_level_req* req,
                           expmc_level_stats* out) {
     return guarded([&] {
         need(c && (nreq == 0 || (req && out)), EXPMC_EINVAL, "null argument");
-        need(lane == EXPMC_LANE_ENTRY || lane == EXPMC_LANE_FORWARD, EXPMC_ENOTIMPL,
-             "only entry (lane 0) and forward (lane 1) sampling are built");
+        need(lane <= EXPMC_LANE_FEM, EXPMC_ENOTIMPL, "unknown sampling lane (0 entry, 1 forward, 2 fem)");
         run_level_batch(c, beta, lane, req, nreq, out);
     });
 }
@@ -745,33 +804,7 @@ int expmc_sample_debug(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, c
                        double* eta_fine, double* eta_coarse, uint64_t* cost, uint64_t* jumps, int64_t* end_state) {
     return guarded([&] {
         need(c && (nreq == 0 || req), EXPMC_EINVAL, "null argument");
-        need(lane == EXPMC_LANE_ENTRY || lane == EXPMC_LANE_FORWARD, EXPMC_ENOTIMPL,
-             "only entry (lane 0) and forward (lane 1) sampling are built");
-        if (nreq == 0) return;
-        bind(c);
-        std::vector<DevItem> items(static_cast<size_t>(nreq));
-        for (int64_t i = 0; i < nreq; ++i) {
-            expmc_level_req r = req[i];
-            r.count = 1;
-            validate_req(c, r, beta, lane);
-            items[i] = make_item(r, beta, lane);
-        }
-        const bool forward = lane == EXPMC_LANE_FORWARD;
-        if (forward) ensure_forward_init(c);
-        ensure_items(c, static_cast<size_t>(nreq));
-        if (static_cast<size_t>(nreq) > c->cap_dbg) {
-            dev_alloc(&c->d_dbg, nreq);
-            c->cap_dbg = nreq;
-        }
-        cuda_check(cudaMemcpyAsync(c->d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
-                   "H2D");
-        launch_debug(c->rows, c->edges(), c->d_items, static_cast<uint32_t>(nreq), forward_init(c), c->d_dbg, c->sampler,
-                     forward, c->stream);
-        c->ctr.kernel_launches += 1;
-        std::vector<SampleOut> o(static_cast<size_t>(nreq));
-        cuda_check(cudaMemcpyAsync(o.data(), c->d_dbg, nreq * sizeof(SampleOut), cudaMemcpyDeviceToHost, c->stream),
-                   "D2H");
-        cuda_check(cudaStreamSynchronize(c->stream), "sample debug");
+        const std::vector<SampleOut> o = sample_debug(c, beta, lane, nreq, req);
         for (int64_t i = 0; i < nreq; ++i) {
             if (eta_fine) eta_fine[i] = o[i].fine;
             if (eta_coarse) eta_coarse[i] = o[i].coarse;
@@ -780,6 +813,56 @@ int expmc_sample_debug(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, c
             if (end_state) end_state[i] = o[i].end_state;
         }
     });
+}
+
+int expmc_sample_debug_ex(expmc_ctx* c, double beta, uint32_t lane, int64_t nreq, const expmc_level_req* req,
+                          expmc_sample_record* out) {
+    return guarded([&] {
+        need(c && (nreq == 0 || (req && out)), EXPMC_EINVAL, "null argument");
+        const std::vector<SampleOut> o = sample_debug(c, beta, lane, nreq, req);
+        for (int64_t i = 0; i < nreq; ++i)
+            out[i] = expmc_sample_record{o[i].fine, o[i].coarse, o[i].value, o[i].integ_f, o[i].integ_c,
+                                         o[i].cost, o[i].jumps, o[i].end_state};
+    });
+}
+
+int expmc_ctx_set_load(expmc_ctx* c, const double* load) {
+    return guarded([&] {
+        need(c && (load || c->n == 0), EXPMC_EINVAL, "null argument");
+        if (c->n == 0) return;
+        bind(c);
+        if (!c->d_load) dev_alloc(&c->d_load, c->n);
+        cuda_check(cudaMemcpyAsync(c->d_load, load, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
+        c->ctr.h2d_bytes += c->n * sizeof(double);
+        cuda_check(cudaStreamSynchronize(c->stream), "set load");
+    });
+}
+
+int expmc_ctx_create_scaled(const expmc_csr* A, const double* row_scale, const double* u, int device,
+                            expmc_ctx** out) {
+    int rc = EXPMC_OK;
+    std::vector<double> val;
+    expmc_csr scaled{};
+    rc = guarded([&] {
+        need(A != nullptr && out != nullptr, EXPMC_EINVAL, "null argument");
+        need(A->n >= 0, EXPMC_EINVAL, "matrix dimension must be nonnegative");
+        need(A->n == 0 || (A->row_ptr && row_scale), EXPMC_EINVAL, "null CSR or row scale");
+        need(A->n == 0 || A->nnz == 0 || A->val, EXPMC_EINVAL, "null CSR arrays");
+        // decompose_impl's row loop (chain.cpp:29-38): scale checked first, then each v = s a_ij
+        val.resize(static_cast<size_t>(A->nnz > 0 ? A->nnz : 0));
+        for (int64_t i = 0; i < A->n; ++i) {
+            const double sc = row_scale[i];
+            need(std::isfinite(sc), EXPMC_EINVAL, "row scale is NaN or Inf");
+            for (int64_t k = A->row_ptr[i]; k < A->row_ptr[i + 1] && k < A->nnz; ++k) {
+                val[static_cast<size_t>(k)] = sc * A->val[k];
+                need(std::isfinite(val[static_cast<size_t>(k)]), EXPMC_EINVAL, "matrix entry is NaN or Inf");
+            }
+        }
+        scaled = *A;
+        scaled.val = val.data();
+    });
+    if (rc != EXPMC_OK) return rc;
+    return expmc_ctx_create(&scaled, u, device, out);
 }
 
 }  // extern "C"

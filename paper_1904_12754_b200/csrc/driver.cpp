@@ -26,6 +26,7 @@ namespace {
 
 struct Level {
     double sum = 0.0, sum_sq = 0.0;
+    double integ = 0.0;  // fem: Level::integ_sum (mlmc.cpp:184-198)
     uint64_t samples = 0, cost = 0, jumps = 0;
     double mean() const { return samples ? sum / static_cast<double>(samples) : 0.0; }
     double variance() const {  // LevelStats::variance, mlmc.cpp:13-17
@@ -74,7 +75,7 @@ struct RowState {
     Phase phase = Phase::waiting_warmup;
     std::vector<Level> lv;
     std::vector<std::pair<int, uint64_t>> pending;  // (level index, additional samples)
-    double stat_error = 0.0, bias = 0.0;
+    double stat_error = 0.0, bias = 0.0, quad = 0.0;
     double projected = 0.0;
     bool converged = false;
     bool over_budget = false;
@@ -85,6 +86,7 @@ struct DriverConfig {
     uint64_t warmup;
     int max_iterations;
     double max_cost;
+    bool fem;
 };
 
 // Advance one row whose pending work has completed, up to its next GPU request or the end.
@@ -132,6 +134,12 @@ void advance(RowState& r, const DriverConfig& cfg, std::vector<double>& v, std::
         means.clear();
         for (size_t i = 1; i < r.lv.size(); ++i) means.push_back(r.lv[i].mean());
         r.bias = bias_estimate_impl(means.size(), means.data());
+        if (cfg.fem) {  // quad = bias_estimate(integ_means), mlmc.cpp:226-235
+            means.clear();
+            for (size_t i = 1; i < r.lv.size(); ++i)
+                means.push_back(r.lv[i].integ / static_cast<double>(r.lv[i].samples));
+            r.quad = bias_estimate_impl(means.size(), means.data());
+        }
         if (r.stat_error <= cfg.target && r.bias <= cfg.target) {
             r.converged = true;
             r.phase = Phase::done;
@@ -153,20 +161,25 @@ void advance(RowState& r, const DriverConfig& cfg, std::vector<double>& v, std::
     }
 }
 
-// rows == nullptr: forward mode (lane 1), each "row" an independent run of the functional
+// lane EXPMC_LANE_FORWARD: rows == nullptr, each "row" an independent run of the functional
 // sum(e^{tA} u) with its own seed; validate_problem skips the entry check (mlmc.cpp:154).
-void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t nrows, const int64_t* rows,
-                const uint64_t* row_seed, expmc_result* out, expmc_level_record* levels, int32_t max_levels) {
+// lane EXPMC_LANE_FEM: entry rows plus the load integrals; l0 >= 1 (mlmc.cpp:177).
+void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options& opt, int64_t nrows,
+                const int64_t* rows, const uint64_t* row_seed, expmc_result* out, expmc_level_record* levels,
+                int32_t max_levels) {
     expmc_ctx_info info{};
     if (expmc_ctx_get_info(ctx, &info) != EXPMC_OK) throw Status(EXPMC_EINVAL, "null context");
-    const uint32_t lane = rows ? EXPMC_LANE_ENTRY : EXPMC_LANE_FORWARD;
     for (int64_t r = 0; rows && r < nrows; ++r)  // validate_problem, mlmc.cpp:150-159
         if (rows[r] < 0 || rows[r] >= info.n) throw Status(EXPMC_ERANGE, "entry index outside matrix");
+    if (lane == EXPMC_LANE_FEM && !ctx_has_load(ctx))
+        throw Status(EXPMC_EINVAL, "load length does not match decomposition");
     if (!(beta > 0.0)) throw Status(EXPMC_EINVAL, "beta must be positive");
     if (!(opt.epsilon > 0.0)) throw Status(EXPMC_EINVAL, "epsilon must be positive");
-    const int l0 = opt.l0_override >= 0 ? opt.l0_override : initial_level_impl(beta, info.d_max);
+    int l0 = opt.l0_override >= 0 ? opt.l0_override : initial_level_impl(beta, info.d_max);
+    if (lane == EXPMC_LANE_FEM) l0 = std::max(l0, 1);  // the coarse grid must carry a Simpson rule
     const int cap = l0 + opt.max_levels_above_l0;
-    DriverConfig cfg{opt.epsilon, opt.epsilon / std::sqrt(2.0), opt.warmup, opt.max_iterations, opt.max_cost};
+    DriverConfig cfg{opt.epsilon, opt.epsilon / std::sqrt(2.0), opt.warmup, opt.max_iterations, opt.max_cost,
+                     lane == EXPMC_LANE_FEM};
 
     std::vector<RowState> st(static_cast<size_t>(nrows));
 #pragma omp parallel for schedule(static)
@@ -231,6 +244,7 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
                     l.samples += d.samples;
                     l.cost += d.cost;
                     l.jumps += d.jumps;
+                    l.integ += d.integ_sum;
                 }
                 s.pending.clear();
                 try {
@@ -272,6 +286,7 @@ void drive_rows(expmc_ctx* ctx, double beta, const expmc_options& opt, int64_t n
         o.L = s.top;
         o.statistical_error = s.stat_error;
         o.bias_estimate = s.bias;
+        o.quadrature_bound = s.quad;
         o.converged = s.converged ? 1 : 0;
         o.projected_cost = s.projected;
         o.over_budget = s.over_budget ? 1 : 0;
@@ -319,7 +334,7 @@ int expmc_mlmc_driver_rows(expmc_ctx* ctx, double beta, const expmc_options* opt
     return guarded([&] {
         if (!ctx || !opt || (nrows > 0 && (!rows || !row_seed || !out)))
             throw Status(EXPMC_EINVAL, "null argument");
-        drive_rows(ctx, beta, *opt, nrows, rows, row_seed, out, levels, max_levels);
+        drive_rows(ctx, EXPMC_LANE_ENTRY, beta, *opt, nrows, rows, row_seed, out, levels, max_levels);
     });
 }
 
@@ -328,7 +343,7 @@ int expmc_mlmc_driver(expmc_ctx* ctx, int64_t entry, double beta, const expmc_op
     return guarded([&] {
         if (!ctx || !opt || !out) throw Status(EXPMC_EINVAL, "null argument");
         const uint64_t seed = opt->seed;
-        drive_rows(ctx, beta, *opt, 1, &entry, &seed, out, levels, max_levels);
+        drive_rows(ctx, EXPMC_LANE_ENTRY, beta, *opt, 1, &entry, &seed, out, levels, max_levels);
     });
 }
 
@@ -342,7 +357,17 @@ int expmc_mlmc_driver_forward(expmc_ctx* ctx, double beta, const expmc_options* 
             if (nruns != 1) throw Status(EXPMC_EINVAL, "null argument");
             seeds = &one;
         }
-        drive_rows(ctx, beta, *opt, nruns, nullptr, seeds, out, levels, max_levels);
+        drive_rows(ctx, EXPMC_LANE_FORWARD, beta, *opt, nruns, nullptr, seeds, out, levels, max_levels);
+    });
+}
+
+int expmc_mlmc_driver_fem(expmc_ctx* ctx, double beta, const expmc_options* opt, int64_t nrows, const int64_t* rows,
+                          const uint64_t* row_seed, expmc_result* out, expmc_level_record* levels,
+                          int32_t max_levels) {
+    return guarded([&] {
+        if (!ctx || !opt || (nrows > 0 && (!rows || !row_seed || !out)))
+            throw Status(EXPMC_EINVAL, "null argument");
+        drive_rows(ctx, EXPMC_LANE_FEM, beta, *opt, nrows, rows, row_seed, out, levels, max_levels);
     });
 }
 

@@ -19,6 +19,10 @@
 // driver's allocation (mlmc.cpp:216) sees the same unit costs in expectation.
 #pragma once
 
+#ifndef EXPMC_SAMPLER_MINB
+#define EXPMC_SAMPLER_MINB 4  // resident 256-thread blocks per SM the sampler is register-budgeted for
+#endif
+
 #include "walker.cuh"
 
 namespace expmc_b200 {
@@ -37,7 +41,7 @@ struct EdWalker {
 };
 
 template <bool F>
-__device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
+__device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                          uint64_t sample) {
     stream_init(w.st, ic.seed, sample, ic.key3);
     const uint32_t s0 = draw_start<F>(w.st, ic, fi);
@@ -106,7 +110,7 @@ __device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const
 }
 
 template <bool F>
-__device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
+__device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                           double& fine, double& coarse) {
     const double sg = static_cast<double>(w.sign);
     const double u_end = terminal_factor<F>(ic, fi, rows, w.state);
@@ -125,7 +129,7 @@ __device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic
 }
 
 template <bool F>
-__device__ __forceinline__ double ed_sample(const EdWalker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows) {
+__device__ __forceinline__ double ed_sample(const EdWalker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows) {
     if (!ic.base && w.dconst) return 0.0;
     double fine, coarse;
     ed_finish<F>(w, ic, fi, rows, fine, coarse);
@@ -133,41 +137,61 @@ __device__ __forceinline__ double ed_sample(const EdWalker& w, const ItemConst& 
 }
 
 // ---- policies the chunk kernel is templated on (F: forward mode, lane 1)
+// sample() returns the run_level sample x; kExtra policies also produce the SumAcc side
+// channel (fem).  record() fills the per-sample debug output.
 template <bool F>
 struct RefPolicy {
     using W = Walker;
-    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows, uint64_t s) {
-        walker_start<F>(w, ic, fi, rows, s);
+    static constexpr bool kExtra = false;
+    static constexpr int kMinBlocks = EXPMC_SAMPLER_MINB;
+    static __device__ __forceinline__ void prepare(ItemConst&) {}
+    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
+                                                 uint64_t s) {
+        walker_start<F>(w, ic, ld, rows, s);
     }
-    static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const RowRec* rows, const EdgeTables& e,
-                                                 const LogEntry* lg, unsigned long long& dr, unsigned long long& j) {
+    static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const LaneData&, const RowRec* rows,
+                                                 const EdgeTables& e, const LogEntry* lg, unsigned long long& dr,
+                                                 unsigned long long& j) {
         return walker_event(w, ic, rows, e, lg, dr, j);
     }
-    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows) {
-        return walker_sample<F>(w, ic, fi, rows);
+    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const LaneData& ld,
+                                                    const RowRec* rows, double&) {
+        return walker_sample<F>(w, ic, ld, rows);
     }
-    static __device__ __forceinline__ void finish(const W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows, double& f,
-                                                  double& c) {
-        walker_finish<F>(w, ic, fi, rows, f, c);
+    static __device__ __forceinline__ void record(const W& w, const ItemConst& ic, const LaneData& ld,
+                                                  const RowRec* rows, SampleOut& o) {
+        walker_finish<F>(w, ic, ld, rows, o.fine, o.coarse);
+        o.value = ic.base ? o.fine : __dsub_rn(o.fine, o.coarse);
+        o.integ_f = o.integ_c = 0.0;
+        o.end_state = w.state;
     }
 };
 
 template <bool F>
 struct EdPolicy {
     using W = EdWalker;
-    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows, uint64_t s) {
-        ed_start<F>(w, ic, fi, rows, s);
+    static constexpr bool kExtra = false;
+    static constexpr int kMinBlocks = EXPMC_SAMPLER_MINB;
+    static __device__ __forceinline__ void prepare(ItemConst&) {}
+    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
+                                                 uint64_t s) {
+        ed_start<F>(w, ic, ld, rows, s);
     }
-    static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const RowRec* rows, const EdgeTables& e,
-                                                 const LogEntry* lg, unsigned long long& dr, unsigned long long& j) {
+    static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const LaneData&, const RowRec* rows,
+                                                 const EdgeTables& e, const LogEntry* lg, unsigned long long& dr,
+                                                 unsigned long long& j) {
         return ed_event(w, ic, rows, e, lg, dr, j);
     }
-    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows) {
-        return ed_sample<F>(w, ic, fi, rows);
+    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const LaneData& ld,
+                                                    const RowRec* rows, double&) {
+        return ed_sample<F>(w, ic, ld, rows);
     }
-    static __device__ __forceinline__ void finish(const W& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* rows, double& f,
-                                                  double& c) {
-        ed_finish<F>(w, ic, fi, rows, f, c);
+    static __device__ __forceinline__ void record(const W& w, const ItemConst& ic, const LaneData& ld,
+                                                  const RowRec* rows, SampleOut& o) {
+        ed_finish<F>(w, ic, ld, rows, o.fine, o.coarse);
+        o.value = ic.base ? o.fine : __dsub_rn(o.fine, o.coarse);
+        o.integ_f = o.integ_c = 0.0;
+        o.end_state = w.state;
     }
 };
 

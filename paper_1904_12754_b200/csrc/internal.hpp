@@ -52,14 +52,17 @@ struct alignas(16) DevItem {
     uint32_t entry;
     uint32_t key3;    // (level & 0xFFFFFF) | lane << 24   (rng.hpp:29)
     uint32_t base;
-    uint32_t mode;    // lane: 0 entry, 1 forward (the kernel instantiation is chosen per batch)
+    uint32_t mode;    // lane: 0 entry, 1 forward, 2 fem (the kernel instantiation is chosen per batch)
 };
 
-// Forward-mode initial distribution on the device (InitialDistribution, paths.hpp:310-315).
-struct ForwardInit {
+// Per-context data of the non-entry lanes: forward mode's initial distribution
+// (InitialDistribution, paths.hpp; make_initial_distribution paths.cpp:12-28) and fem mode's
+// load vector (MlmcProblem::load, mlmc.hpp:53).
+struct LaneData {
     const double* cdf;
     double total;
     uint32_t n;
+    const double* load;
 };
 
 // Per-chunk partial and per-item running total (SumAcc, parallel.hpp:57-78, + jumps).
@@ -68,6 +71,7 @@ struct alignas(16) Partial {
     double sum_sq;
     unsigned long long cost;
     unsigned long long jumps;
+    double extra;  // fem: sum of integ_f - integ_c (SumAcc::extra, parallel.hpp:60)
 };
 
 // Chunk partials of one sampler window, structure of arrays so that a sample-sharded run can
@@ -76,14 +80,18 @@ struct alignas(16) Partial {
 struct ChunkPartials {
     double* sum;     // [W]
     double* sum_sq;  // [W]  (contiguous after sum)
+    double* extra;   // [W]  (contiguous after sum_sq; written by fem batches only)
     unsigned long long* cost;   // [W]
     unsigned long long* jumps;  // [W]  (contiguous after cost)
 };
 
 // Per-sample debug output.
 struct SampleOut {
-    double fine;
-    double coarse;
+    double fine;      // single: value; coupled: eta_fine (fem: sign e^{coarse+delta})
+    double coarse;    // coupled: eta_coarse
+    double value;     // the run_level sample x (mlmc.cpp:103-133)
+    double integ_f;   // fem: fine / coarse load integrals
+    double integ_c;
     unsigned long long cost;
     unsigned long long jumps;
     long long end_state;
@@ -107,17 +115,18 @@ struct SamplerArgs {
     uint32_t nitems;
     uint64_t g_begin, g_end;  // global chunk window of this launch
     ChunkPartials partials;   // [g_end - g_begin] each
-    ForwardInit init;
+    LaneData init;
     unsigned int* counter;    // dynamic chunk counter, zeroed before launch
     uint32_t shard_rank;      // sample sharding: this launch samples the chunks g with
     uint32_t shard_world;     //   g % shard_world == shard_rank (the others stay zero)
 };
 
-void launch_sampler(const SamplerArgs& a, int grid, int mode, bool forward, cudaStream_t s);
+void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s);
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
-                    const ChunkPartials& partials, Partial* totals, cudaStream_t s);
+                    const ChunkPartials& partials, bool with_extra, Partial* totals, cudaStream_t s);
 void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n,
-                  const ForwardInit& init, SampleOut* out, int mode, bool forward, cudaStream_t s);
+                  const LaneData& init, SampleOut* out, int mode, uint32_t lane, cudaStream_t s);
+constexpr int kSamplerFem = 2;  // sampler_blocks_per_sm: the fem instantiation
 int sampler_blocks_per_sm(int mode);
 int sampler_threads();
 
@@ -150,4 +159,5 @@ namespace expmc_b200 {
 void run_level_batch(expmc_ctx* ctx, double beta, uint32_t lane, const expmc_level_req* req,
                      int64_t nreq, expmc_level_stats* out);
 void set_error(const std::string& m);
+bool ctx_has_load(const expmc_ctx* c);
 }  // namespace expmc_b200

@@ -18,6 +18,7 @@
 
 #include "internal.hpp"
 #include "ed_walker.cuh"
+#include "fem_walker.cuh"
 #include "walker.cuh"
 
 namespace expmc_b200 {
@@ -55,7 +56,7 @@ __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ chunk
 }
 
 template <class P>
-__global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(SamplerArgs a) {
+__global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned full = 0xFFFFFFFFu;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -78,8 +79,11 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
         const uint32_t item = find_item(a.chunk0, a.nitems, g, hint);
         hint = item;
         {
-            const ItemConst c = load_item(a.items, item);
-            if (lane == 0) ic = c;
+            if (lane == 0) {
+                ItemConst c = load_item(a.items, item);
+                P::prepare(c);
+                ic = c;
+            }
             __syncwarp();
         }
         const DevItem& it = a.items[item];
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
         const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
         const uint32_t cnt = static_cast<uint32_t>(hi - lo);
 
-        double sum = 0.0, sum_sq = 0.0;
+        double sum = 0.0, sum_sq = 0.0, extra = 0.0;
         unsigned long long cost = 0, jumps = 0;
         typename P::W w;
         bool active = false;
@@ -105,10 +109,12 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
             }
             next += __popc(need);
             if (!__any_sync(full, active)) break;
-            if (active && P::event(w, ic, a.rows, a.edges, s_log, cost, jumps)) {
-                const double x = P::sample(w, ic, a.init, a.rows);
+            if (active && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps)) {
+                double ex;
+                const double x = P::sample(w, ic, a.init, a.rows, ex);
                 sum = __dadd_rn(sum, x);
                 sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
+                if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
                 cost += ic.nsteps;
                 active = false;
             }
@@ -117,6 +123,7 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
         for (int o = 16; o > 0; o >>= 1) {
             sum = __dadd_rn(sum, __shfl_xor_sync(full, sum, o));
             sum_sq = __dadd_rn(sum_sq, __shfl_xor_sync(full, sum_sq, o));
+            if constexpr (P::kExtra) extra = __dadd_rn(extra, __shfl_xor_sync(full, extra, o));
             cost += __shfl_xor_sync(full, cost, o);
             jumps += __shfl_xor_sync(full, jumps, o);
         }
@@ -124,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
             const uint64_t k = g - a.g_begin;
             a.partials.sum[k] = sum;
             a.partials.sum_sq[k] = sum_sq;
+            if constexpr (P::kExtra) a.partials.extra[k] = extra;
             a.partials.cost[k] = cost;
             a.partials.jumps[k] = jumps;
         }
@@ -131,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, EXPMC_SAMPLER_MINB) k_sample(Sampler
 }
 
 __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, uint64_t g_begin,
-                          uint64_t g_end, ChunkPartials p, Partial* __restrict__ totals) {
+                          uint64_t g_end, ChunkPartials p, bool with_extra, Partial* __restrict__ totals) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nitems) return;
     const uint64_t c0 = chunk0[i] > g_begin ? chunk0[i] : g_begin;
@@ -142,6 +150,7 @@ __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, 
         const uint64_t k = g - g_begin;
         t.sum = __dadd_rn(t.sum, p.sum[k]);
         t.sum_sq = __dadd_rn(t.sum_sq, p.sum_sq[k]);
+        if (with_extra) t.extra = __dadd_rn(t.extra, p.extra[k]);
         t.cost += p.cost[k];
         t.jumps += p.jumps[k];
     }
@@ -150,23 +159,23 @@ __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, 
 
 template <class P>
 __global__ void k_debug(const RowRec* __restrict__ rows, EdgeTables edges,
-                        const DevItem* __restrict__ items, uint32_t n, ForwardInit init, SampleOut* __restrict__ out) {
+                        const DevItem* __restrict__ items, uint32_t n, LaneData init, SampleOut* __restrict__ out) {
     __shared__ LogEntry s_log[128];
     load_log_table(s_log);
     __syncthreads();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const ItemConst ic = load_item(items, i);
+    ItemConst ic = load_item(items, i);
+    P::prepare(ic);
     typename P::W w;
     P::start(w, ic, init, rows, items[i].first);
     unsigned long long draws = 0, jumps = 0;
-    while (!P::event(w, ic, rows, edges, s_log, draws, jumps)) {
+    while (!P::event(w, ic, init, rows, edges, s_log, draws, jumps)) {
     }
     SampleOut o;
-    P::finish(w, ic, init, rows, o.fine, o.coarse);
+    P::record(w, ic, init, rows, o);
     o.cost = draws + ic.nsteps;
     o.jumps = jumps;
-    o.end_state = w.state;
     out[i] = o;
 }
 
@@ -347,7 +356,9 @@ int sampler_threads() { return kThreads; }
 
 int sampler_blocks_per_sm(int mode) {
     int b = 0;
-    if (mode == EXPMC_SAMPLER_EVENT)
+    if (mode == kSamplerFem)
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<FemPolicy>, kThreads, 0), "occupancy");
+    else if (mode == EXPMC_SAMPLER_EVENT)
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<EdPolicy<false>>, kThreads, 0), "occupancy");
     else
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<RefPolicy<false>>, kThreads, 0), "occupancy");
@@ -356,31 +367,35 @@ int sampler_blocks_per_sm(int mode) {
 
 // Entry and forward mode are separate instantiations: a batch is one lane, and the entry-mode
 // kernel (the hot path) carries no trace of the forward start draw.
-void launch_sampler(const SamplerArgs& a, int grid, int mode, bool forward, cudaStream_t s) {
-    if (mode == EXPMC_SAMPLER_EVENT) {
-        if (forward) k_sample<EdPolicy<true>><<<grid, kThreads, 0, s>>>(a);
+void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s) {
+    if (lane == EXPMC_LANE_FEM) {
+        k_sample<FemPolicy><<<grid, kThreads, 0, s>>>(a);
+    } else if (mode == EXPMC_SAMPLER_EVENT) {
+        if (lane == EXPMC_LANE_FORWARD) k_sample<EdPolicy<true>><<<grid, kThreads, 0, s>>>(a);
         else k_sample<EdPolicy<false>><<<grid, kThreads, 0, s>>>(a);
     } else {
-        if (forward) k_sample<RefPolicy<true>><<<grid, kThreads, 0, s>>>(a);
+        if (lane == EXPMC_LANE_FORWARD) k_sample<RefPolicy<true>><<<grid, kThreads, 0, s>>>(a);
         else k_sample<RefPolicy<false>><<<grid, kThreads, 0, s>>>(a);
     }
     cuda_check(cudaGetLastError(), "k_sample launch");
 }
 
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
-                    const ChunkPartials& partials, Partial* totals, cudaStream_t s) {
-    k_combine<<<grid_for(nitems, 256), 256, 0, s>>>(chunk0, nitems, g_begin, g_end, partials, totals);
+                    const ChunkPartials& partials, bool with_extra, Partial* totals, cudaStream_t s) {
+    k_combine<<<grid_for(nitems, 256), 256, 0, s>>>(chunk0, nitems, g_begin, g_end, partials, with_extra, totals);
     cuda_check(cudaGetLastError(), "k_combine launch");
 }
 
-void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n, const ForwardInit& init,
-                  SampleOut* out, int mode, bool forward, cudaStream_t s) {
+void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n, const LaneData& init,
+                  SampleOut* out, int mode, uint32_t lane, cudaStream_t s) {
     const int g = grid_for(n, 128);
-    if (mode == EXPMC_SAMPLER_EVENT) {
-        if (forward) k_debug<EdPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+    if (lane == EXPMC_LANE_FEM) {
+        k_debug<FemPolicy><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+    } else if (mode == EXPMC_SAMPLER_EVENT) {
+        if (lane == EXPMC_LANE_FORWARD) k_debug<EdPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
         else k_debug<EdPolicy<false>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
     } else {
-        if (forward) k_debug<RefPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+        if (lane == EXPMC_LANE_FORWARD) k_debug<RefPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
         else k_debug<RefPolicy<false>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
     }
     cuda_check(cudaGetLastError(), "k_debug launch");

@@ -200,6 +200,8 @@ struct ItemConst {
     double half_dt;  // dt_ * 0.5, the left factor of paths.cpp:110
     double tend;     // N * dt (= beta), event-driven walker
     double inv_dt;   // 1 / dt, event-driven walker
+    double h_fine;   // fem: dt / 3, the fine Simpson scale (mlmc.cpp:68, 90)
+    double h_coarse; // fem: (2 dt) / 3, the coarse Simpson scale (mlmc.cpp:68, 91)
     uint32_t entry;
     uint32_t key3;
     uint32_t base;
@@ -208,7 +210,7 @@ struct ItemConst {
 // sample_initial (paths.cpp:32-36): the path's first draw picks the start state by
 // upper_bound over the CDF of u -- an exact binary search over the same fp64 CDF.
 template <bool F>
-__device__ __forceinline__ uint32_t draw_start(Stream& st, const ItemConst& ic, const ForwardInit& fi) {
+__device__ __forceinline__ uint32_t draw_start(Stream& st, const ItemConst& ic, const LaneData& fi) {
     if (!F) return ic.entry;
     stream_reserve2(st);
     const double v = stream_pop(st);
@@ -228,7 +230,7 @@ __device__ __forceinline__ uint32_t draw_start(Stream& st, const ItemConst& ic, 
 
 // The terminal factor: u[end] (entry mode, paths.cpp:112,138) or sum(u) (forward, 156,178).
 template <bool F>
-__device__ __forceinline__ double terminal_factor(const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
+__device__ __forceinline__ double terminal_factor(const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                                   uint32_t state) {
     return F ? fi.total : __ldg(&rows[state].u);
 }
@@ -246,7 +248,7 @@ struct Walker {
 };
 
 template <bool F>
-__device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
+__device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                              uint64_t sample) {
     stream_init(w.st, ic.seed, sample, ic.key3);
     const uint32_t s0 = draw_start<F>(w.st, ic, fi);
@@ -261,14 +263,13 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
     w.step = 0;
 }
 
-// One event of the path: one pass of evolve_common's for(;;) body, plus the step
-// bookkeeping of single/coupled when the holding interval ends the fine step.
-// Returns true when the sample's last fine step has completed.  Exponential draws and jumps
-// are counted straight into the caller's accumulators (cost = draws + fine steps,
-// paths.hpp:22-23; the fine steps are added by the caller when the sample ends).
-__device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
-                                             const EdgeTables& edges, const LogEntry* s_log,
-                                             unsigned long long& draws, unsigned long long& jumps) {
+// One pass of evolve_common's for(;;) body (paths.cpp:48-69): the holding-interval test and,
+// on a jump, the neighbour draw.  Returns true when the holding interval ends the fine step.
+// Exponential draws and jumps are counted straight into the caller's accumulators (cost =
+// draws + fine steps, paths.hpp:22-23; the fine steps are added when the sample ends).
+__device__ __forceinline__ bool walker_hold(Walker& w, const RowRec* __restrict__ rows, const EdgeTables& edges,
+                                            const LogEntry* s_log, unsigned long long& draws,
+                                            unsigned long long& jumps) {
     stream_reserve2(w.st);  // the event's only Philox call site
     bool step_done = true;
     if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
@@ -288,7 +289,16 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
             step_done = !(w.remaining > 0.0);
         }
     }
-    if (!step_done) return false;
+    return step_done;
+}
+
+// One event of the path: walker_hold plus the step bookkeeping of single / coupled
+// (paths.cpp:108-110, 130-136) when the holding interval ends the fine step.  Returns true
+// when the sample's last fine step has completed.
+__device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+                                             const EdgeTables& edges, const LogEntry* s_log,
+                                             unsigned long long& draws, unsigned long long& jumps) {
+    if (!walker_hold(w, rows, edges, s_log, draws, jumps)) return false;
     // ---- the fine step ended in w.state
     const double dn = w.cur.d;
     if (ic.base) {
@@ -319,7 +329,7 @@ __device__ __forceinline__ double exp_or_one(double x) { return x == 0.0 ? 1.0 :
 // Terminal values: single -> (sign * e^expo) * u[end] (paths.cpp:112);
 // coupled -> uf = sign * u[end]; (uf e^{coarse+delta}, uf e^{coarse}) (paths.cpp:138-140).
 template <bool F>
-__device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows,
+__device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                               double& fine, double& coarse) {
     const double sg = static_cast<double>(w.sign);
     const double u_end = terminal_factor<F>(ic, fi, rows, w.state);  // same sector as the last row record read
@@ -336,7 +346,7 @@ __device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& 
 // The level-statistics sample x = P_l (base) or P_l - P_{l-1} (coupled), as run_level_ex adds
 // it (mlmc.cpp:103-108).  delta == 0 makes fine and coarse bitwise equal, so x = 0 exactly.
 template <bool F>
-__device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst& ic, const ForwardInit& fi, const RowRec* __restrict__ rows) {
+__device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows) {
     if (!ic.base && w.acc_b == 0.0) return 0.0;
     // same values as walker_finish, with one exp call site shared by both modes
     const double sg = static_cast<double>(w.sign);
@@ -356,6 +366,8 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.half_dt = __dmul_rn(it.dt, 0.5);
     ic.tend = __dmul_rn(it.dt, static_cast<double>(it.nsteps));
     ic.inv_dt = __ddiv_rn(1.0, it.dt);
+    ic.h_fine = 0.0;  // fem only: FemPolicy::prepare
+    ic.h_coarse = 0.0;
     ic.entry = it.entry;
     ic.key3 = it.key3;
     ic.base = it.base;

@@ -16,6 +16,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.json")
 GOLDEN_FORWARD = os.path.join(ROOT, "tests", "golden", "golden_forward.json")
+GOLDEN_FEM = os.path.join(ROOT, "tests", "golden", "golden_fem.json")
 
 
 def pytest_configure(config):
@@ -39,6 +40,12 @@ def golden():
 @pytest.fixture(scope="session")
 def golden_forward():
     with open(GOLDEN_FORWARD) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def golden_fem():
+    with open(GOLDEN_FEM) as f:
         return json.load(f)
 
 

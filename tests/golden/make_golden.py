@@ -189,7 +189,82 @@ def forward():
     print(path, os.path.getsize(path), "bytes")
 
 
+def fem():
+    """golden_fem.json: SampleMode::fem (paths.cpp:183-245; mlmc.cpp:66-148, 170-260) and
+    solve_convdiff_point (fem.cpp:51-73) through the reference.  The toy system is read from the
+    reference's own test fixture by the reference's load_fem_system at generation time."""
+    ref = Reference()
+    out = {"generator": "tests/golden/make_golden.py fem() (reference: /root/reference/proj/core via oracle/_ref)"}
+    data = "/root/reference/proj/tests/data"
+    toy = ref.load_fem_system(f"{data}/toy_mass.mtx", f"{data}/toy_stiffness.mtx", f"{data}/toy_load.txt",
+                              f"{data}/toy_u0.txt")
+    systems = {
+        "toy3": dict(mass_diag=toy["mass_diag"], stiffness=toy["stiffness"], load=toy["load"], u0=toy["u0"], t=0.9),
+        # test_apps.cpp:154-171: m = 2, k = 2.6, F = 1.4, u0 = 2
+        "scalar": dict(mass_diag=np.array([2.0]), stiffness=CSR.from_dense([[2.6]]), load=np.array([1.4]),
+                       u0=np.array([2.0]), t=1.0),
+    }
+    # a small world as a "stiffness" with unit mass: wide and signed rows, seeded load
+    sw = ref.smallw(60, 2, 0.2, 31)
+    n = sw.n
+    rng = np.random.default_rng(3)
+    systems["smallw60"] = dict(mass_diag=np.round(rng.uniform(0.5, 2.0, n), 6), stiffness=sw.a,
+                               load=np.round(rng.uniform(-1.0, 1.0, n), 6),
+                               u0=1.0 + 0.01 * np.arange(n, dtype=np.float64), t=0.2)
+    out["systems"] = {}
+    for name, sy in systems.items():
+        a, md = sy["stiffness"], sy["mass_diag"]
+        scale = -1.0 / md
+        g = sy["load"] / md
+        ch = ref.chain_scaled(a, scale)
+        t = sy["t"]
+        nn = a.n
+        entries = sorted(set([0, nn - 1, nn // 2]))
+        samples = []
+        for entry in entries:
+            for level in range(0, 6):
+                for b in ([1, 0] if level >= 2 else [1]):
+                    seed = 300 + entry + 13 * level + b
+                    idx = np.array(list(range(20)) + [511, 512, 2 ** 33 + 3], np.uint64)
+                    r = ch.fem_samples(sy["u0"], g, entry, t, level, b, seed, idx)
+                    samples.append(dict(entry=entry, level=level, base=b, seed=seed, idx=[int(x) for x in idx],
+                                        **{k: hx(r[k]) for k in ("value", "eta_f", "eta_c", "integ_f", "integ_c")},
+                                        end_state=[int(x) for x in r["end_state"]], cost=[int(c) for c in r["cost"]]))
+        runs = []
+        for entry in entries[:2]:
+            for (level, b, first, count) in [(0, 1, 0, 1000), (1, 1, 5, 700), (2, 0, 37, 2500), (4, 0, 1000, 600)]:
+                seed = 61 + entry
+                r = ch.fem_run_level(sy["u0"], g, entry, t, level, b, first, count, seed, threads=4)
+                runs.append(dict(entry=entry, level=level, base=b, first=first, count=count, seed=seed,
+                                 sum=float(r["sum"]).hex(), sum_sq=float(r["sum_sq"]).hex(),
+                                 samples=int(r["samples"]), cost=int(r["cost"])))
+        drivers = []
+        eps = {"toy3": 5e-3, "scalar": 1e-5, "smallw60": 2e-2}[name]
+        for node in entries:
+            seed = 31 + node
+            r = ref.solve_convdiff_point(md, a, sy["load"], sy["u0"], node, t, epsilon=eps, seed=seed, threads=4)
+            drivers.append(dict(node=node, seed=seed, epsilon=eps, estimate=float(r["estimate"]).hex(),
+                                statistical_error=float(r["statistical_error"]).hex(),
+                                bias_estimate=float(r["bias_estimate"]).hex(),
+                                quadrature_bound=float(r["quadrature_bound"]).hex(), l0=r["l0"], L=r["L"],
+                                total_cost=int(r["total_cost"]), converged=r["converged"],
+                                levels=[dict(level=int(x["level"]), sum=float(x["sum"]).hex(),
+                                             sum_sq=float(x["sum_sq"]).hex(), samples=int(x["samples"]),
+                                             cost=int(x["cost"])) for x in r["levels"]]))
+        out["systems"][name] = dict(csr=csr_json(a), mass_diag=hx(md), load=hx(sy["load"]), u0=hx(sy["u0"]),
+                                    t=float(t).hex(), d=hx(ch.decomposition()["d"]), samples=samples, run_level=runs,
+                                    drivers=drivers)
+    path = os.path.join(HERE, "golden_fem.json")
+    with open(path, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print(path, os.path.getsize(path), "bytes")
+
+
 if __name__ == "__main__":
+    if "--fem-only" in sys.argv:
+        fem()
+        sys.exit(0)
     if "--forward-only" not in sys.argv:
         main()
     forward()
+    fem()

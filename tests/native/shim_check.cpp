@@ -139,6 +139,30 @@ static void gpu_checks() {
         Context zmat(dense(2, {0.0, 0.0, 0.0, 0.0}), {1.0, 1.0});
         CHECK(throws<std::domain_error>([&] { spectral_scale(zmat); }));
     }
+    // fem mode: test_apps.cpp:154-171, the scalar convection-diffusion closed form
+    {
+        FemSystem sys;
+        sys.mass_diag = {2.0};
+        sys.stiffness = dense(1, {2.6});
+        sys.load = {1.4};
+        sys.u0 = {2.0};
+        MlmcOptions o;
+        o.epsilon = 1e-5;
+        o.seed = 2;
+        const MlmcResult r = solve_convdiff_point(sys, 0, 1.0, o);
+        const double a = 1.3, g = 0.7;
+        const double expect = 2.0 * std::exp(-a) + g / a * (1.0 - std::exp(-a));
+        // the reference asserts statistical_error == 0 (an absorbing chain: every sample equal);
+        // its sequential sums happen to cancel exactly, the GPU's tree-ordered sums leave the
+        // variance formula sum_sq/n - mean^2 at rounding level (ulp(x^2) ~ 1e-16, so se ~ 1e-10)
+        CHECK(r.converged && r.statistical_error <= 1e-8 * std::abs(r.estimate) && r.l0 >= 1);
+        CHECK(std::abs(r.estimate - expect) < 3.0 * r.statistical_error + r.bias_estimate + r.quadrature_bound + 1e-6);
+        CHECK(throws<std::out_of_range>([&] { solve_convdiff_point(sys, 1, 1.0, o); }));
+        CHECK(throws<std::invalid_argument>([&] { solve_convdiff_point(sys, 0, 0.0, o); }));
+        Context nol(dense(1, {2.6}), std::vector<double>{-0.5}, {2.0}, 0);  // no load bound
+        CHECK(throws<std::invalid_argument>(
+            [&] { run_level(MlmcProblem{&nol, 0, 1.0, SampleMode::fem}, 2, true, 0, 10, 1); }));
+    }
 }
 
 int main(int argc, char** argv) {

@@ -229,7 +229,8 @@ def test_gpu_forward_small_world_strang(gpu, golden_forward):
 
 @pytest.mark.gpu
 def test_gpu_forward_errors(gpu):
-    """Reference errors: negative u / zero sum (paths.cpp:17-22), unknown lane -> ENOTIMPL,
+    """Reference errors: negative u / zero sum (paths.cpp:17-22), unknown lane -> ENOTIMPL, fem
+    without a load -> invalid_argument (mlmc.cpp:156-157),
     entry is not validated in forward mode (mlmc.cpp:154)."""
     import paper_1904_12754_b200 as P
 
@@ -246,10 +247,10 @@ def test_gpu_forward_errors(gpu):
         ctx.set_vector(np.ones(2))  # set_vector rebuilds the start distribution
         st = P.run_level(P.MlmcProblem(ctx, 12345, 1.0, P.SampleMode.forward), 2, True, 0, 100, 1)
         assert st.sum / st.samples == pytest.approx(2.0 * math.e, rel=1e-13)
-        with pytest.raises(P.NotImplementedMode):
+        with pytest.raises(P.InvalidArgument, match="load length"):  # fem without a load
             P.run_level(P.MlmcProblem(ctx, 0, 1.0, P.SampleMode.fem), 2, True, 0, 10, 1)
         with pytest.raises(P.NotImplementedMode):
-            ctx.run_level_batch(1.0, 0, 2, 1, 0, 10, 1, lane=2)
+            ctx.run_level_batch(1.0, 0, 2, 1, 0, 10, 1, lane=3)
 
 
 @pytest.mark.gpu

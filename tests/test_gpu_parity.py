@@ -130,7 +130,7 @@ def test_run_level_batch_equals_singles_and_is_deterministic(gpu):
         for k in range(len(entries)):
             s = P.run_level(P.MlmcProblem(ctx, int(entries[k]), cfg.beta), int(levels[k]), bool(base[k]),
                             int(first[k]), int(count[k]), int(seeds[k]))
-            assert (s.sum, s.sum_sq, s.samples, s.cost, s.jumps) == tuple(b1[k].tolist())
+            assert (s.sum, s.sum_sq, s.samples, s.cost, s.jumps) == tuple(b1[k].tolist())[:5]
 
 
 def test_run_level_extension_is_additive(gpu):  # test_mlmc.cpp:128-143
