@@ -29,7 +29,8 @@ extern "C" {
 #define EXPMC_ERANGE 2    /* std::out_of_range     */
 #define EXPMC_EDOMAIN 3   /* std::domain_error     */
 #define EXPMC_ECUDA 4     /* CUDA runtime failure (no CPU fallback exists) */
-#define EXPMC_ENOTIMPL 5  /* mode not built yet (forward / fem sampling)   */
+#define EXPMC_ENOTIMPL 5  /* unknown sampling lane                          */
+#define EXPMC_EIO 6       /* std::runtime_error: file / parse errors (io.cpp), "path:line: what" */
 #define EXPMC_EINTERNAL 9
 
 /* Path samplers.  REFERENCE: draw-for-draw the reference's evolve_common / single / coupled
@@ -287,6 +288,17 @@ int expmc_bench_gather(int device, uint64_t bytes, int32_t loads_per_thread, int
 /* Host input generators for the BASELINE configs (no GPU needed; csrc/gen.cpp).
  * Results are canonical CSR matrices owned by the library until expmc_matrix_destroy. */
 typedef struct expmc_matrix expmc_matrix;
+
+/* Host input pipeline (multi-threaded, bit-identical results and the same messages):
+ *   expmc_read_matrix_market  read_matrix_market (io.cpp:69-128): coordinate real
+ *                             general|symmetric; errors EXPMC_EIO "path:line: what"
+ *   expmc_read_vector         read_vector (io.cpp:154-167): *n = entries; copies min(cap, n)
+ *   expmc_csr_from_triplets   SparseMatrix::from_triplets (sparse.cpp:12-49): sorted,
+ *                             duplicates summed, zero sums dropped; EXPMC_ERANGE / EXPMC_EINVAL */
+int expmc_read_matrix_market(const char* path, expmc_matrix** out);
+int expmc_read_vector(const char* path, int64_t cap, double* out, int64_t* n);
+int expmc_csr_from_triplets(int64_t n, int64_t count, const int64_t* rows, const int64_t* cols,
+                            const double* vals, expmc_matrix** out);
 /* Barabasi-Albert, the reference's pref(n, d, seed) algorithm (netgen.cpp:61-107). */
 int expmc_gen_ba(int64_t n, int64_t d, uint64_t seed, expmc_matrix** out);
 /* R-MAT: 2^scale nodes, edge_factor * 2^scale directed draws, symmetrised, unit weights. */

@@ -404,6 +404,14 @@ class Reference(_Backend):
         self._check(self.lib.ref_read_matrix_market(os.fsencode(path), C.byref(h)))
         return RefChain(self, None, handle=h)
 
+    def from_triplets(self, n, rows, cols, vals) -> "RefChain":
+        r = np.ascontiguousarray(rows, np.int64)
+        c = np.ascontiguousarray(cols, np.int64)
+        v = np.ascontiguousarray(vals, np.float64)
+        h = C.c_void_p()
+        self._check(self.lib.ref_from_triplets(_I64(n), _I64(r.size), _ptr(r), _ptr(c), _ptr(v), C.byref(h)))
+        return RefChain(self, None, handle=h)
+
     def read_vector(self, path):
         n = _I64()
         self._check(self.lib.ref_read_vector(os.fsencode(path), _I64(0), None, C.byref(n)))

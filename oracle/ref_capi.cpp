@@ -592,6 +592,25 @@ int ref_read_matrix_market(const char* path, void** out) {
     });
 }
 
+// SparseMatrix::from_triplets (sparse.cpp:12-49) on a triplet list, in list order.
+int ref_from_triplets(int64_t n, int64_t count, const int64_t* rows, const int64_t* cols, const double* vals,
+                      void** out) {
+    return guarded([&] {
+        std::vector<Triplet> t;
+        t.reserve(static_cast<std::size_t>(count));
+        for (int64_t k = 0; k < count; ++k) t.push_back({rows[k], cols[k], vals[k]});
+        auto* m = new RefMatrix;
+        try {
+            m->a = SparseMatrix::from_triplets(n, std::move(t));
+            m->dec = decompose(m->a);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
 int ref_read_vector(const char* path, int64_t cap, double* out, int64_t* n) {
     return guarded([&] {
         const std::vector<double> v = read_vector(path);

@@ -11,6 +11,7 @@ from .api import (  # noqa: F401
     DomainError,
     ExpmcError,
     InvalidArgument,
+    IoError,
     LANE_ENTRY,
     LANE_FEM,
     LANE_FORWARD,
@@ -27,6 +28,9 @@ from .api import (  # noqa: F401
     bias_estimate,
     device_count,
     initial_level,
+    load_fem_system,
+    read_matrix_market,
+    read_vector,
     mlmc_driver,
     FemSystem,
     fem_context,

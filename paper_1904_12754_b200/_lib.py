@@ -12,7 +12,8 @@ LIB_PATH = os.environ.get("EXPMC_LIB") or os.path.join(_HERE, "_lib", "libexpmc_
 
 _I32, _I64, _U32, _U64, _D = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 
-EXPMC_OK, EXPMC_EINVAL, EXPMC_ERANGE, EXPMC_EDOMAIN, EXPMC_ECUDA, EXPMC_ENOTIMPL, EXPMC_EINTERNAL = 0, 1, 2, 3, 4, 5, 9
+EXPMC_OK, EXPMC_EINVAL, EXPMC_ERANGE, EXPMC_EDOMAIN, EXPMC_ECUDA, EXPMC_ENOTIMPL, EXPMC_EIO, EXPMC_EINTERNAL = (
+    0, 1, 2, 3, 4, 5, 6, 9)
 LANE_ENTRY, LANE_FORWARD, LANE_FEM = 0, 1, 2
 SAMPLER_REFERENCE, SAMPLER_EVENT = 0, 1
 
@@ -98,6 +99,9 @@ SYMBOLS = [
     ("expmc_gen_ba", C.c_int, [_I64, _I64, _U64, C.POINTER(_P)]),
     ("expmc_gen_rmat", C.c_int, [_I32, _I64, _D, _D, _D, _U64, C.POINTER(_P)]),
     ("expmc_gen_convdiff3d", C.c_int, [_I64, _D, _I32, C.POINTER(_P)]),
+    ("expmc_read_matrix_market", C.c_int, [C.c_char_p, C.POINTER(_P)]),
+    ("expmc_read_vector", C.c_int, [C.c_char_p, _I64, _P, C.POINTER(_I64)]),
+    ("expmc_csr_from_triplets", C.c_int, [_I64, _I64, _P, _P, _P, C.POINTER(_P)]),
     ("expmc_matrix_info", C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
     ("expmc_matrix_copy", C.c_int, [_P, _P, _P, _P]),
     ("expmc_matrix_destroy", None, [_P]),

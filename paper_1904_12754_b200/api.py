@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -57,8 +58,12 @@ class NotImplementedMode(ExpmcError, NotImplementedError):
     pass
 
 
+class IoError(ExpmcError):
+    """std::runtime_error of the readers: "path:line: what" (io.cpp)."""
+
+
 _ERR = {L.EXPMC_EINVAL: InvalidArgument, L.EXPMC_ERANGE: OutOfRange, L.EXPMC_EDOMAIN: DomainError,
-        L.EXPMC_ECUDA: CudaError, L.EXPMC_ENOTIMPL: NotImplementedMode}
+        L.EXPMC_ECUDA: CudaError, L.EXPMC_ENOTIMPL: NotImplementedMode, L.EXPMC_EIO: IoError}
 
 
 def _check(rc: int) -> None:
@@ -96,35 +101,17 @@ class SparseMatrix:
 
     @staticmethod
     def from_triplets(n: int, rows, cols, vals) -> "SparseMatrix":
-        """sparse.cpp:12-49: indices checked (out_of_range), values finite (invalid_argument),
-        sorted by (row, col), duplicates summed in input order, zero sums dropped."""
-        if n < 0:
-            raise InvalidArgument("matrix dimension must be nonnegative")
-        r = np.asarray(rows, np.int64)
-        c = np.asarray(cols, np.int64)
-        v = np.asarray(vals, np.float64)
-        if r.size and (r.min() < 0 or r.max() >= n or c.min() < 0 or c.max() >= n):
-            raise OutOfRange("triplet index outside [0, n)")
-        if v.size and not np.isfinite(v).all():
-            raise InvalidArgument("matrix entry is NaN or Inf")
-        order = np.lexsort((c, r))  # stable: duplicates keep input order
-        r, c, v = r[order], c[order], v[order]
-        if r.size:
-            key = r * n + c
-            start = np.flatnonzero(np.r_[True, key[1:] != key[:-1]])
-            # sequential summation of each duplicate run, left to right (sparse.cpp:33-37)
-            sums = v[start].copy()
-            dup = np.flatnonzero(np.diff(np.r_[start, key.size]) > 1)
-            for g in dup:
-                s = v[start[g]]
-                for k in range(start[g] + 1, (start[g + 1] if g + 1 < start.size else key.size)):
-                    s = s + v[k]
-                sums[g] = s
-            keep = sums != 0.0
-            r, c, v = r[start][keep], c[start][keep], sums[keep]
-        rp = np.zeros(n + 1, np.int64)
-        np.add.at(rp, r + 1, 1)
-        return SparseMatrix(n, np.cumsum(rp).astype(np.int64), c.astype(np.int64), v.astype(np.float64))
+        """sparse.cpp:12-49 in the native builder (csrc/io.cpp): indices checked (out_of_range),
+        values finite (invalid_argument), sorted by (row, col), duplicates summed exactly as the
+        reference sums them, zero sums dropped."""
+        r = np.ascontiguousarray(rows, np.int64).ravel()
+        c = np.ascontiguousarray(cols, np.int64).ravel()
+        v = np.ascontiguousarray(vals, np.float64).ravel()
+        if not (r.size == c.size == v.size):
+            raise InvalidArgument("triplet arrays differ in length")
+        h = C.c_void_p()
+        _check(L.lib.expmc_csr_from_triplets(int(n), r.size, _ptr(r), _ptr(c), _ptr(v), C.byref(h)))
+        return _take_matrix(h)
 
     @staticmethod
     def from_dense(d) -> "SparseMatrix":
@@ -147,6 +134,36 @@ class SparseMatrix:
         y = np.zeros(self.n)
         np.add.at(y, r, self.val * x[self.col])
         return y
+
+
+def _take_matrix(h) -> SparseMatrix:
+    """Copy a library-owned expmc_matrix into a SparseMatrix and free it."""
+    n, nnz = C.c_int64(), C.c_int64()
+    try:
+        _check(L.lib.expmc_matrix_info(h, C.byref(n), C.byref(nnz)))
+        rp = np.empty(n.value + 1, np.int64)
+        col = np.empty(nnz.value, np.int64)
+        val = np.empty(nnz.value, np.float64)
+        _check(L.lib.expmc_matrix_copy(h, _ptr(rp), _ptr(col), _ptr(val)))
+    finally:
+        L.lib.expmc_matrix_destroy(h)
+    return SparseMatrix(n.value, rp, col, val)
+
+
+def read_matrix_market(path) -> SparseMatrix:
+    """io.cpp:69-128 (native, multi-threaded): coordinate real general|symmetric."""
+    h = C.c_void_p()
+    _check(L.lib.expmc_read_matrix_market(os.fsencode(path), C.byref(h)))
+    return _take_matrix(h)
+
+
+def read_vector(path) -> np.ndarray:
+    """io.cpp:154-167: every whitespace-separated real of every non-comment line."""
+    n = C.c_int64()
+    _check(L.lib.expmc_read_vector(os.fsencode(path), 0, None, C.byref(n)))
+    out = np.empty(n.value)
+    _check(L.lib.expmc_read_vector(os.fsencode(path), out.size, _ptr(out), C.byref(n)))
+    return out
 
 
 # --------------------------------------------------------------------------------- stats
@@ -532,6 +549,27 @@ class FemSystem:
     @property
     def n(self) -> int:
         return self.stiffness.n
+
+
+def load_fem_system(mass_path, stiffness_path, load_path, u0_path) -> FemSystem:
+    """fem.cpp:12-37: mass (Matrix Market, lumped: diagonal and positive), stiffness, load and
+    initial vectors, with the reference's checks and messages."""
+    mass = read_matrix_market(mass_path)
+    stiffness = read_matrix_market(stiffness_path)
+    load = read_vector(load_path)
+    u0 = read_vector(u0_path)
+    n = stiffness.n
+    if mass.n != n or load.size != n or u0.size != n:
+        raise InvalidArgument("FEM system dimensions disagree")
+    md = np.zeros(n)
+    for i in range(n):
+        for k in range(int(mass.row_ptr[i]), int(mass.row_ptr[i + 1])):
+            if mass.col[k] != i:
+                raise InvalidArgument("mass matrix is not lumped (off-diagonal entry)")
+            md[i] = mass.val[k]
+        if not md[i] > 0.0:
+            raise InvalidArgument("lumped mass must be positive on the diagonal")
+    return FemSystem(md, stiffness, load, u0)
 
 
 def fem_context(sys: FemSystem, device: int = 0) -> Context:

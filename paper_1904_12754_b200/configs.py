@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib as L
-from .api import SparseMatrix, _check, _ptr
+from .api import SparseMatrix, _check, _ptr, _take_matrix
 
 _M0, _M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
 _W0, _W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
@@ -85,14 +85,7 @@ GRAPH_SEED = 1       # BA / R-MAT seed (SURVEY §8d probes used seed 1 for C3)
 
 # ---------------------------------------------------------------- native generators (csrc/gen.cpp)
 def _take(h) -> SparseMatrix:
-    n, nnz = C.c_int64(), C.c_int64()
-    _check(L.lib.expmc_matrix_info(h, C.byref(n), C.byref(nnz)))
-    rp = np.empty(n.value + 1, np.int64)
-    col = np.empty(nnz.value, np.int64)
-    val = np.empty(nnz.value, np.float64)
-    _check(L.lib.expmc_matrix_copy(h, _ptr(rp), _ptr(col), _ptr(val)))
-    L.lib.expmc_matrix_destroy(h)
-    return SparseMatrix(n.value, rp, col, val)
+    return _take_matrix(h)
 
 
 def gen_ba(n: int, d: int, seed: int) -> SparseMatrix:

@@ -30,12 +30,6 @@
 
 using namespace expmc_b200;
 
-struct expmc_matrix {
-    int64_t n = 0;
-    std::vector<int64_t> row_ptr{0};
-    std::vector<int64_t> col;
-    std::vector<double> val;
-};
 
 namespace {
 

@@ -10,6 +10,14 @@
 
 #include "expmc_b200.h"
 
+// Host canonical CSR owned by the library (generators, readers; expmc_matrix_* accessors).
+struct expmc_matrix {
+    int64_t n = 0;
+    std::vector<int64_t> row_ptr{0};
+    std::vector<int64_t> col;
+    std::vector<double> val;
+};
+
 namespace expmc_b200 {
 
 // ----------------------------------------------------------------------------- HBM layout
