@@ -31,6 +31,7 @@ extern "C" {
 #define EXPMC_ECUDA 4     /* CUDA runtime failure (no CPU fallback exists) */
 #define EXPMC_ENOTIMPL 5  /* unknown sampling lane                          */
 #define EXPMC_EIO 6       /* std::runtime_error: file / parse errors (io.cpp), "path:line: what" */
+#define EXPMC_EOVERFLOW 7 /* std::overflow_error (mc_auto: step count beyond 64 bits)            */
 #define EXPMC_EINTERNAL 9
 
 /* Path samplers.  REFERENCE: draw-for-draw the reference's evolve_common / single / coupled
@@ -279,6 +280,41 @@ int expmc_mlmc_driver_rows(expmc_ctx* ctx, double beta, const expmc_options* opt
 int expmc_mlmc_driver_forward(expmc_ctx* ctx, double beta, const expmc_options* options, int64_t nruns,
                               const uint64_t* seeds, expmc_result* out, expmc_level_record* levels,
                               int32_t max_levels);
+
+/* Classical (single-level) Monte Carlo on the same sampler (mc.hpp, mc.cpp:42-113): samples
+ * [0, samples) of one step size dt = beta / steps, steps = round(beta / dt) (must be a positive
+ * integer, 1e-9 relative), stream_for(seed, bit_width(steps), s, lane) and the reference's
+ * Welford accumulator per 512-sample chunk merged in chunk order (parallel.hpp:80-104). */
+typedef struct {
+    double estimate;
+    double std_error;
+    uint64_t samples;
+    double dt;
+    int64_t steps;
+    uint64_t wall_cost; /* model units: exponential draws + fine steps */
+    uint64_t jumps;
+} expmc_mc_result;
+
+typedef struct {
+    int64_t entry;    /* ignored on the forward lane */
+    uint64_t seed;
+    uint64_t samples; /* >= 2 */
+    double beta;
+    double dt;
+} expmc_mc_req;
+
+/* mc_single_entry (mc.cpp:42-58): lane 0 on the context of A. */
+int expmc_mc_single_entry(expmc_ctx* ctx, int64_t entry, double beta, double dt, uint64_t samples, uint64_t seed,
+                          expmc_mc_result* out);
+/* mc_forward_scalar (mc.cpp:60-76): lane 1 on the context of A^T (u: the start weights). */
+int expmc_mc_forward_scalar(expmc_ctx* ctx, double beta, double dt, uint64_t samples, uint64_t seed,
+                            expmc_mc_result* out);
+/* nreq independent classical-MC runs in one GPU pass (lane 0 or 1). */
+int expmc_mc_batch(expmc_ctx* ctx, uint32_t lane, int64_t nreq, const expmc_mc_req* req, expmc_mc_result* out);
+/* mc_auto (mc.cpp:78-113): two 1000-sample pilots at dt_a = beta / 2^max(2, l0) and dt_a / 2
+ * (seeds seed+1, seed+2; one batched pass), the Richardson bias constant, the step count and the
+ * sample count of the final run; wall_cost includes the pilots. */
+int expmc_mc_auto(expmc_ctx* ctx, int64_t entry, double beta, double epsilon, uint64_t seed, expmc_mc_result* out);
 
 /* Roofline denominator: random 32-B-sector gather throughput of `device` over a buffer of
  * `bytes` (L2-resident or HBM-sized), `loads_per_thread` independent sector loads per thread,

@@ -131,6 +131,21 @@ class _RefResult(C.Structure):
                 ("L", C.c_int32), ("total_cost", _U64), ("converged", C.c_int32), ("nlevels", C.c_int32)]
 
 
+class _Mc(C.Structure):
+    _fields_ = [("estimate", _D), ("std_error", _D), ("samples", _U64), ("dt", _D), ("steps", _I64),
+                ("wall_cost", _U64)]
+
+
+class _OrcMc(C.Structure):
+    _fields_ = [("estimate", _D), ("std_error", _D), ("samples", _U64), ("dt", _D), ("steps", _I64),
+                ("wall_cost", _U64), ("jumps", _U64)]
+
+
+def _mc_dict(r):
+    return dict(estimate=r.estimate, std_error=r.std_error, samples=r.samples, dt=r.dt, steps=r.steps,
+                wall_cost=r.wall_cost)
+
+
 class _OrcStats(C.Structure):
     _fields_ = [("sum", _D), ("sum_sq", _D), ("samples", _U64), ("cost", _U64), ("jumps", _U64)]
 
@@ -361,6 +376,22 @@ class OracleChain(_Chain):
                      converged=bool(r.converged), nlevels=r.nlevels, total_jumps=r.total_jumps,
                      total_samples=r.total_samples, levels=lv[i, :r.nlevels].copy())
                 for i, r in enumerate(res)]
+
+    # ---- classical MC (mc.cpp:42-76)
+    def mc_single_entry(self, u, entry, beta, dt, samples, seed, threads=4):
+        return self._mc(u, entry, beta, dt, samples, seed, 0, threads)
+
+    def mc_forward_scalar(self, u, beta, dt, samples, seed, threads=4):
+        return self._mc(u, 0, beta, dt, samples, seed, 1, threads)
+
+    def _mc(self, u, entry, beta, dt, samples, seed, lane, threads):
+        u = np.ascontiguousarray(u, np.float64)
+        r = _OrcMc()
+        self.be._check(self.be.lib.orc_mc(self.h, _ptr(u), _I64(entry), _D(beta), _D(dt), _U64(samples), _U64(seed),
+                                          _U32(lane), _INT(threads), C.byref(r)))
+        d = _mc_dict(r)
+        d["jumps"] = r.jumps
+        return d
 
     def transposed(self) -> "OracleChain":
         return OracleChain(self.be, self.a.transpose())
@@ -616,6 +647,28 @@ class RefChain(_Chain):
                                                       C.byref(q)))
             out.append(_ref_result(res, lv, quadrature_bound=q.value))
         return out
+
+    # ---- classical MC (mc.cpp:42-113)
+    def mc_single_entry(self, u, entry, beta, dt, samples, seed, threads=4):
+        u = np.ascontiguousarray(u, np.float64)
+        r = _Mc()
+        self.be._check(self.be.lib.ref_mc_single_entry(self.h, _ptr(u), _I64(entry), _D(beta), _D(dt), _U64(samples),
+                                                       _U64(seed), _INT(threads), C.byref(r)))
+        return _mc_dict(r)
+
+    def mc_forward_scalar(self, u, beta, dt, samples, seed, threads=4):
+        u = np.ascontiguousarray(u, np.float64)
+        r = _Mc()
+        self.be._check(self.be.lib.ref_mc_forward_scalar(self.h, _ptr(u), _D(beta), _D(dt), _U64(samples),
+                                                         _U64(seed), _INT(threads), C.byref(r)))
+        return _mc_dict(r)
+
+    def mc_auto(self, u, entry, beta, epsilon, seed, threads=4):
+        u = np.ascontiguousarray(u, np.float64)
+        r = _Mc()
+        self.be._check(self.be.lib.ref_mc_auto(self.h, _ptr(u), _I64(entry), _D(beta), _D(epsilon), _U64(seed),
+                                               _INT(threads), C.byref(r)))
+        return _mc_dict(r)
 
     def dense_expmv(self, u, beta):
         u = np.ascontiguousarray(u, np.float64)

@@ -569,6 +569,83 @@ int orc_fem_run_level(const orc_chain* c, const double* u, const double* load, i
     return 0;
 }
 
+/* ---------------------------------------------------------------- classical MC
+ * mc_single_entry / mc_forward_scalar (mc.cpp:42-76): samples [0, m) at dt with
+ * steps = round(beta / dt), key level = bit_width(steps); WelfordAcc per 512-sample chunk
+ * (parallel.hpp:80-92), chunks merged in order by Chan's formula (parallel.hpp:93-104). */
+typedef struct {
+    uint64_t n;
+    double mean, m2;
+    uint64_t cost, jumps;
+} orc_welford;
+
+static void welford_merge(orc_welford* a, const orc_welford* o) {
+    if (o->n == 0) return;
+    if (a->n == 0) {
+        *a = *o;
+        return;
+    }
+    const double delta = o->mean - a->mean;
+    const double total = (double)(a->n + o->n);
+    a->mean += delta * ((double)o->n / total);
+    a->m2 += o->m2 + delta * delta * ((double)a->n * (double)o->n / total);
+    a->n += o->n;
+    a->cost += o->cost;
+    a->jumps += o->jumps;
+}
+
+int orc_mc(const orc_chain* c, const double* u, int64_t entry, double beta, double dt, uint64_t samples,
+           uint64_t seed, uint32_t lane, int threads, orc_mc_result* out) {
+    if (samples < 2) return fail(1, "at least 2 samples required");
+    const int forward = lane == ORC_LANE_FORWARD;
+    if (!forward && (entry < 0 || entry >= c->n)) return fail(2, "entry index outside matrix");
+    if (!(dt > 0.0) || !(beta > 0.0)) return fail(1, "beta and dt must be positive");
+    const double ratio = beta / dt;
+    const double rounded = round(ratio);
+    if (fabs(ratio - rounded) > 1e-9 * ratio || rounded < 1.0)
+        return fail(1, "beta/dt must be a positive integer step count");
+    const int64_t steps = (int64_t)rounded;
+    const uint32_t key = (uint32_t)(64 - __builtin_clzll((unsigned long long)steps));
+    orc_init init = {NULL, 0, 0.0};
+    int rc;
+    if (forward && (rc = init_build(u, c->n, &init))) return rc;
+    const orc_init* ip = forward ? &init : NULL;
+    const int64_t nch = (int64_t)((samples - 1) / ORC_CHUNK + 1);
+    orc_welford* part = (orc_welford*)calloc((size_t)nch, sizeof *part);
+    if (threads <= 0) threads = 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+    for (int64_t ci = 0; ci < nch; ++ci) {
+        const uint64_t lo = (uint64_t)ci * ORC_CHUNK;
+        const uint64_t hi = samples < lo + ORC_CHUNK ? samples : lo + ORC_CHUNK;
+        orc_welford a = {0, 0.0, 0.0, 0, 0};
+        for (uint64_t smp = lo; smp < hi; ++smp) {
+            orc_stream s;
+            orc_stream_init(&s, seed, key, smp, lane);
+            const orc_sample r = sample_single(c, u, entry, dt, steps, &s, ip);
+            ++a.n; /* WelfordAcc::add */
+            const double delta = r.fine - a.mean;
+            a.mean += delta / (double)a.n;
+            a.m2 += delta * (r.fine - a.mean);
+            a.cost += r.cost;
+            a.jumps += r.jumps;
+        }
+        part[ci] = a;
+    }
+    orc_welford t = {0, 0.0, 0.0, 0, 0};
+    for (int64_t ci = 0; ci < nch; ++ci) welford_merge(&t, &part[ci]);
+    free(part);
+    free(init.cdf);
+    out->estimate = t.mean;
+    const double var = t.n > 1 ? (t.m2 / (double)(t.n - 1) > 0.0 ? t.m2 / (double)(t.n - 1) : 0.0) : 0.0;
+    out->std_error = t.n > 1 ? sqrt(var / (double)t.n) : 0.0;
+    out->samples = t.n;
+    out->dt = dt;
+    out->steps = steps;
+    out->wall_cost = t.cost;
+    out->jumps = t.jumps;
+    return 0;
+}
+
 /* ---------------------------------------------------------------- driver helpers */
 
 int orc_initial_level(double beta, double d_max, int* out) { /* mlmc.cpp:19-23 */

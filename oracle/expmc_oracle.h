@@ -135,6 +135,17 @@ int orc_mlmc_driver_fem(const orc_chain* c, const double* u, const double* load,
                         const orc_options* o, int64_t nrows, const int64_t* rows, const uint64_t* row_seed,
                         orc_result* out, double* quad, orc_level_record* levels, int32_t max_levels);
 
+/* classical MC (mc.cpp:42-76): lane 0 = mc_single_entry, lane 1 = mc_forward_scalar. */
+typedef struct {
+    double estimate, std_error;
+    uint64_t samples;
+    double dt;
+    int64_t steps;
+    uint64_t wall_cost, jumps;
+} orc_mc_result;
+int orc_mc(const orc_chain* c, const double* u, int64_t entry, double beta, double dt, uint64_t samples,
+           uint64_t seed, uint32_t lane, int threads, orc_mc_result* out);
+
 int orc_initial_level(double beta, double d_max, int* out);
 int orc_optimal_allocation(int64_t n, const double* v, const double* c, double eps, uint64_t* out);
 int orc_bias_estimate(int64_t n, const double* means, double* out);

@@ -27,6 +27,7 @@
 #include "expmc/communicability.hpp"
 #include "expmc/fem.hpp"
 #include "expmc/io.hpp"
+#include "expmc/mc.hpp"
 #include "expmc/mlmc.hpp"
 #include "expmc/netgen.hpp"
 #include "expmc/oracle.hpp"
@@ -608,6 +609,49 @@ int ref_from_triplets(int64_t n, int64_t count, const int64_t* rows, const int64
             throw;
         }
         *out = m;
+    });
+}
+
+// Classical MC (mc.cpp:42-113).  out = {estimate, std_error, samples, dt, steps, wall_cost}.
+struct RefMc {
+    double estimate, std_error;
+    uint64_t samples;
+    double dt;
+    int64_t steps;
+    uint64_t wall_cost;
+};
+
+static void put_mc(const McResult& r, RefMc* out) {
+    *out = RefMc{r.estimate, r.std_error, r.samples, r.dt, r.steps, r.wall_cost};
+}
+
+int ref_mc_single_entry(void* h, const double* u, int64_t entry, double beta, double dt, uint64_t samples,
+                        uint64_t seed, int threads, RefMc* out) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        put_mc(mc_single_entry(m->dec, std::span<const double>(u, static_cast<std::size_t>(m->dec.n)), entry, beta,
+                               dt, samples, seed, threads),
+               out);
+    });
+}
+
+int ref_mc_forward_scalar(void* h, const double* u, double beta, double dt, uint64_t samples, uint64_t seed,
+                          int threads, RefMc* out) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        put_mc(mc_forward_scalar(m->dec, std::span<const double>(u, static_cast<std::size_t>(m->dec.n)), beta, dt,
+                                 samples, seed, threads),
+               out);
+    });
+}
+
+int ref_mc_auto(void* h, const double* u, int64_t entry, double beta, double epsilon, uint64_t seed, int threads,
+                RefMc* out) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        put_mc(mc_auto(m->dec, std::span<const double>(u, static_cast<std::size_t>(m->dec.n)), entry, beta, epsilon,
+                       seed, threads),
+               out);
     });
 }
 

@@ -28,6 +28,11 @@ from .api import (  # noqa: F401
     bias_estimate,
     device_count,
     initial_level,
+    McResult,
+    mc_auto,
+    mc_batch,
+    mc_forward_scalar,
+    mc_single_entry,
     load_fem_system,
     read_matrix_market,
     read_vector,

@@ -12,8 +12,9 @@ LIB_PATH = os.environ.get("EXPMC_LIB") or os.path.join(_HERE, "_lib", "libexpmc_
 
 _I32, _I64, _U32, _U64, _D = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 
-EXPMC_OK, EXPMC_EINVAL, EXPMC_ERANGE, EXPMC_EDOMAIN, EXPMC_ECUDA, EXPMC_ENOTIMPL, EXPMC_EIO, EXPMC_EINTERNAL = (
-    0, 1, 2, 3, 4, 5, 6, 9)
+EXPMC_OK, EXPMC_EINVAL, EXPMC_ERANGE, EXPMC_EDOMAIN, EXPMC_ECUDA, EXPMC_ENOTIMPL, EXPMC_EIO, EXPMC_EOVERFLOW = (
+    0, 1, 2, 3, 4, 5, 6, 7)
+EXPMC_EINTERNAL = 9
 LANE_ENTRY, LANE_FORWARD, LANE_FEM = 0, 1, 2
 SAMPLER_REFERENCE, SAMPLER_EVENT = 0, 1
 
@@ -51,6 +52,15 @@ class ResultC(C.Structure):
 class SampleRecordC(C.Structure):
     _fields_ = [("eta_fine", _D), ("eta_coarse", _D), ("value", _D), ("integ_fine", _D), ("integ_coarse", _D),
                 ("cost", _U64), ("jumps", _U64), ("end_state", _I64)]
+
+
+class McResultC(C.Structure):
+    _fields_ = [("estimate", _D), ("std_error", _D), ("samples", _U64), ("dt", _D), ("steps", _I64),
+                ("wall_cost", _U64), ("jumps", _U64)]
+
+
+class McReqC(C.Structure):
+    _fields_ = [("entry", _I64), ("seed", _U64), ("samples", _U64), ("beta", _D), ("dt", _D)]
 
 
 class LevelRecordC(C.Structure):
@@ -99,6 +109,10 @@ SYMBOLS = [
     ("expmc_gen_ba", C.c_int, [_I64, _I64, _U64, C.POINTER(_P)]),
     ("expmc_gen_rmat", C.c_int, [_I32, _I64, _D, _D, _D, _U64, C.POINTER(_P)]),
     ("expmc_gen_convdiff3d", C.c_int, [_I64, _D, _I32, C.POINTER(_P)]),
+    ("expmc_mc_single_entry", C.c_int, [_P, _I64, _D, _D, _U64, _U64, C.POINTER(McResultC)]),
+    ("expmc_mc_forward_scalar", C.c_int, [_P, _D, _D, _U64, _U64, C.POINTER(McResultC)]),
+    ("expmc_mc_batch", C.c_int, [_P, _U32, _I64, _P, _P]),
+    ("expmc_mc_auto", C.c_int, [_P, _I64, _D, _D, _U64, C.POINTER(McResultC)]),
     ("expmc_read_matrix_market", C.c_int, [C.c_char_p, C.POINTER(_P)]),
     ("expmc_read_vector", C.c_int, [C.c_char_p, _I64, _P, C.POINTER(_I64)]),
     ("expmc_csr_from_triplets", C.c_int, [_I64, _I64, _P, _P, _P, C.POINTER(_P)]),

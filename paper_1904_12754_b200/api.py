@@ -62,8 +62,13 @@ class IoError(ExpmcError):
     """std::runtime_error of the readers: "path:line: what" (io.cpp)."""
 
 
+class OverflowError_(ExpmcError, OverflowError):
+    """std::overflow_error (mc_auto)."""
+
+
 _ERR = {L.EXPMC_EINVAL: InvalidArgument, L.EXPMC_ERANGE: OutOfRange, L.EXPMC_EDOMAIN: DomainError,
-        L.EXPMC_ECUDA: CudaError, L.EXPMC_ENOTIMPL: NotImplementedMode, L.EXPMC_EIO: IoError}
+        L.EXPMC_ECUDA: CudaError, L.EXPMC_ENOTIMPL: NotImplementedMode, L.EXPMC_EIO: IoError,
+        L.EXPMC_EOVERFLOW: OverflowError_}
 
 
 def _check(rc: int) -> None:
@@ -588,6 +593,60 @@ def solve_convdiff_point(sys: FemSystem, node: int, t: float, options: MlmcOptio
         raise OutOfRange("node index outside system")
     with fem_context(sys, device) as ctx:
         return mlmc_driver(MlmcProblem(ctx, node, t, SampleMode.fem), options)
+
+
+# --------------------------------------------------------------------------------- classical MC
+@dataclass
+class McResult:
+    """mc.hpp McResult (+ jumps)."""
+
+    estimate: float = 0.0
+    std_error: float = 0.0
+    samples: int = 0
+    dt: float = 0.0
+    steps: int = 0
+    wall_cost: int = 0
+    jumps: int = 0
+
+
+def _mc(r) -> McResult:
+    return McResult(r.estimate, r.std_error, r.samples, r.dt, r.steps, r.wall_cost, r.jumps)
+
+
+def mc_single_entry(ctx: Context, entry: int, beta: float, dt: float, samples: int, seed: int,
+                    threads: int = 0) -> McResult:
+    """mc.cpp:42-58: plain MC of (e^{beta A} u)_entry at one step size, Welford statistics."""
+    r = L.McResultC()
+    _check(L.lib.expmc_mc_single_entry(ctx.handle, entry, beta, dt, samples, seed, C.byref(r)))
+    return _mc(r)
+
+
+def mc_forward_scalar(ctx_t: Context, beta: float, dt: float, samples: int, seed: int,
+                      threads: int = 0) -> McResult:
+    """mc.cpp:60-76: plain MC of sum(e^{beta A} u) on Context(A^T, u)."""
+    r = L.McResultC()
+    _check(L.lib.expmc_mc_forward_scalar(ctx_t.handle, beta, dt, samples, seed, C.byref(r)))
+    return _mc(r)
+
+
+def mc_auto(ctx: Context, entry: int, beta: float, epsilon: float, seed: int, threads: int = 0) -> McResult:
+    """mc.cpp:78-113: pilot-sized plain MC to tolerance epsilon."""
+    r = L.McResultC()
+    _check(L.lib.expmc_mc_auto(ctx.handle, entry, beta, epsilon, seed, C.byref(r)))
+    return _mc(r)
+
+
+def mc_batch(ctx: Context, entries, seeds, samples, beta: float, dt: float, lane: int = L.LANE_ENTRY) -> list:
+    """Many classical-MC runs (one per entry / seed) in one GPU pass."""
+    e, sd, m = np.broadcast_arrays(np.asarray(entries, np.int64), np.asarray(seeds, np.uint64),
+                                   np.asarray(samples, np.uint64))
+    k = e.size
+    req = (L.McReqC * k)()
+    for i in range(k):
+        req[i] = L.McReqC(int(e.ravel()[i]), int(sd.ravel()[i]), int(m.ravel()[i]), beta, dt)
+    out = (L.McResultC * k)()
+    _check(L.lib.expmc_mc_batch(ctx.handle, lane, k, C.cast(req, C.c_void_p), C.cast(out, C.c_void_p)))
+    return [_mc(out[i]) for i in range(k)]
 
 
 def spectral_scale(ctx: Context) -> float:

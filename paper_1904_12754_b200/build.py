@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libexpmc_b200.so")
-SOURCES = ["kernels.cu", "context.cu", "driver.cpp", "gen.cpp", "io.cpp"]
+SOURCES = ["kernels.cu", "context.cu", "driver.cpp", "gen.cpp", "io.cpp", "mc.cpp"]
 HEADERS = ["internal.hpp", "walker.cuh", "ed_walker.cuh", "fem_walker.cuh", "fastmath.cuh", "log_table.inc"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

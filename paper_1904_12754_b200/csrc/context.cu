@@ -295,40 +295,10 @@ void set_error(const std::string& m) { g_err = m; }
 
 bool ctx_has_load(const expmc_ctx* c) { return c->d_load != nullptr; }
 
-void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
-                     expmc_level_stats* out) {
-    bind(c);
-    // validate (first failing request wins, as a sequential loop would report it)
-    int64_t bad = nreq;
-#pragma omp parallel for schedule(static) reduction(min : bad)
-    for (int64_t i = 0; i < nreq; ++i) {
-        out[i] = expmc_level_stats{0.0, 0.0, 0, 0, 0, 0.0};
-        try {
-            validate_req(c, req[i], beta, lane);
-        } catch (const Status&) {
-            bad = std::min(bad, i);
-        }
-    }
-    if (bad < nreq) validate_req(c, req[bad], beta, lane);  // rethrows with the right code
-    std::vector<int64_t> slot;  // request index of each item (count > 0)
-    slot.reserve(static_cast<size_t>(nreq));
-    for (int64_t i = 0; i < nreq; ++i)
-        if (req[i].count > 0) slot.push_back(i);
-    const size_t nitems = slot.size();
-    if (nitems == 0) return;
-    const bool forward = lane == EXPMC_LANE_FORWARD;
-    if (forward) ensure_forward_init(c);  // run_level builds it before sampling (mlmc.cpp)
-    c->ctr.rounds += 1;
-    need(nitems < (size_t{1} << 31), EXPMC_EINVAL, "too many run_level requests in one batch");
-    ensure_items(c, nitems);
-#pragma omp parallel for schedule(static)
-    for (size_t k = 0; k < nitems; ++k) {
-        const expmc_level_req& r = req[slot[k]];
-        c->h_items[k] = make_item(r, beta, lane);
-        const uint64_t first_chunk = r.first_index / kChunk;
-        const uint64_t last_chunk = (r.first_index + r.count - 1) / kChunk;  // parallel.hpp:36-38
-        c->h_chunk0[k] = last_chunk - first_chunk + 1;
-    }
+// The device pass over prepared items (c->h_items, c->h_chunk0 = per-item chunk counts):
+// upload, sampler windows of up to kWindowChunks chunks (+ the NCCL exchange when sample-
+// sharded), ordered combine, totals back to c->h_totals.  welford: the classical-MC reduction.
+void sample_items(expmc_ctx* c, size_t nitems, uint32_t lane, bool welford) {
     uint64_t total = 0;
     for (size_t k = 0; k < nitems; ++k) {  // exclusive prefix of the chunk counts
         const uint64_t n = c->h_chunk0[k];
@@ -351,7 +321,7 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
     }
     const ChunkPartials cp{c->d_pf, c->d_pf + c->cap_partials, c->d_pf + 2 * c->cap_partials, c->d_pu,
                            c->d_pu + c->cap_partials};
-    const bool fem = lane == EXPMC_LANE_FEM;
+    const bool fem = lane == EXPMC_LANE_FEM && !welford;
     const int sampler_grid = fem ? c->sampler_grid_fem : c->sampler_grid;
     const uint32_t world = static_cast<uint32_t>(c->shard_world);
     const int warps_per_block = sampler_threads() / 32;
@@ -389,14 +359,19 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
             c->ev.push_back(e);
         }
         cuda_check(cudaEventRecord(c->ev[2 * nev], c->stream), "event");
-        launch_sampler(a, grid, c->sampler, lane, c->stream);
+        if (welford) launch_sampler_welford(a, grid, c->sampler, lane, c->stream);
+        else launch_sampler(a, grid, c->sampler, lane, c->stream);
         cuda_check(cudaEventRecord(c->ev[2 * nev + 1], c->stream), "event");
         ++nev;
         if (c->nccl) {  // exact cross-GPU sum of the window's chunk partials (one rank non-zero per chunk)
             nccl_allreduce_partials(c->nccl, cp, w, c->cap_partials, c->stream);
             c->ctr.nccl_bytes += w * (3 * sizeof(double) + 2 * sizeof(uint64_t));
         }
-        launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, fem, c->d_totals, c->stream);
+        if (welford)
+            launch_combine_welford(c->d_chunk0, c->d_items, static_cast<uint32_t>(nitems), g0, g1, cp, c->d_totals,
+                                   c->stream);
+        else
+            launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, fem, c->d_totals, c->stream);
         c->ctr.kernel_launches += 2;
         c->ctr.sampler_launches += 1;
         c->last_window = w;
@@ -410,6 +385,106 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         cuda_check(cudaEventElapsedTime(&ms, c->ev[2 * k], c->ev[2 * k + 1]), "event time");
         c->ctr.sampler_ms += ms;
     }
+}
+
+// checked_steps (mc.cpp:16-23) and level_key = bit_width(steps) (mc.cpp:25-27).
+int64_t mc_steps(double beta, double dt) {
+    need(dt > 0.0 && beta > 0.0, EXPMC_EINVAL, "beta and dt must be positive");
+    const double ratio = beta / dt;
+    const double rounded = std::round(ratio);
+    need(!(std::abs(ratio - rounded) > 1e-9 * ratio || rounded < 1.0), EXPMC_EINVAL,
+         "beta/dt must be a positive integer step count");
+    return static_cast<int64_t>(rounded);
+}
+
+void mc_batch(expmc_ctx* c, uint32_t lane, const expmc_mc_req* req, int64_t nreq, expmc_mc_result* out) {
+    need(lane == EXPMC_LANE_ENTRY || lane == EXPMC_LANE_FORWARD, EXPMC_ENOTIMPL,
+         "classical MC runs on the entry (0) or forward (1) lane");
+    bind(c);
+    std::vector<int64_t> steps(static_cast<size_t>(nreq));
+    for (int64_t i = 0; i < nreq; ++i) {  // mc_single_entry / mc_forward_scalar checks, in order
+        need(req[i].samples >= 2, EXPMC_EINVAL, "at least 2 samples required");
+        if (lane == EXPMC_LANE_ENTRY)
+            need(req[i].entry >= 0 && req[i].entry < c->n, EXPMC_ERANGE, "entry index outside matrix");
+        steps[static_cast<size_t>(i)] = mc_steps(req[i].beta, req[i].dt);
+    }
+    if (nreq == 0) return;
+    if (lane == EXPMC_LANE_FORWARD) ensure_forward_init(c);
+    need(static_cast<uint64_t>(nreq) < (uint64_t{1} << 31), EXPMC_EINVAL, "too many MC requests in one batch");
+    const size_t nitems = static_cast<size_t>(nreq);
+    ensure_items(c, nitems);
+    for (size_t k = 0; k < nitems; ++k) {
+        const expmc_mc_req& r = req[k];
+        DevItem it{};
+        const uint64_t st = static_cast<uint64_t>(steps[k]);
+        it.seed = r.seed;
+        it.first = 0;
+        it.count = r.samples;
+        it.dt = r.dt;  // LevelSampler(dec, dt, steps): the given dt, not beta / steps
+        it.nsteps = st;
+        it.entry = lane == EXPMC_LANE_FORWARD ? 0u : static_cast<uint32_t>(r.entry);
+        const uint32_t key = static_cast<uint32_t>(64 - __builtin_clzll(st));  // std::bit_width
+        it.key3 = (key & 0xFFFFFFu) | (lane << 24);
+        it.base = 1u;
+        it.mode = lane;
+        c->h_items[k] = it;
+        c->h_chunk0[k] = (r.samples - 1) / kChunk + 1;
+    }
+    c->ctr.rounds += 1;
+    sample_items(c, nitems, lane, true);
+    for (size_t k = 0; k < nitems; ++k) {  // finish (mc.cpp:29-38)
+        const Partial& t = c->h_totals[k];
+        const uint64_t n = static_cast<uint64_t>(t.extra);
+        expmc_mc_result& o = out[k];
+        o.samples = n;
+        o.estimate = t.sum;
+        const double var = n > 1 ? std::max(0.0, t.sum_sq / static_cast<double>(n - 1)) : 0.0;
+        o.std_error = n > 1 ? std::sqrt(var / static_cast<double>(n)) : 0.0;
+        o.dt = req[k].dt;
+        o.steps = steps[k];
+        o.wall_cost = t.cost;
+        o.jumps = t.jumps;
+        c->ctr.samples += n;
+        c->ctr.jumps += t.jumps;
+        c->ctr.fine_steps += n * static_cast<uint64_t>(steps[k]);
+    }
+}
+
+void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
+                     expmc_level_stats* out) {
+    bind(c);
+    // validate (first failing request wins, as a sequential loop would report it)
+    int64_t bad = nreq;
+#pragma omp parallel for schedule(static) reduction(min : bad)
+    for (int64_t i = 0; i < nreq; ++i) {
+        out[i] = expmc_level_stats{0.0, 0.0, 0, 0, 0, 0.0};
+        try {
+            validate_req(c, req[i], beta, lane);
+        } catch (const Status&) {
+            bad = std::min(bad, i);
+        }
+    }
+    if (bad < nreq) validate_req(c, req[bad], beta, lane);  // rethrows with the right code
+    std::vector<int64_t> slot;  // request index of each item (count > 0)
+    slot.reserve(static_cast<size_t>(nreq));
+    for (int64_t i = 0; i < nreq; ++i)
+        if (req[i].count > 0) slot.push_back(i);
+    const size_t nitems = slot.size();
+    if (nitems == 0) return;
+    const bool forward = lane == EXPMC_LANE_FORWARD;
+    if (forward) ensure_forward_init(c);  // run_level builds it before sampling (mlmc.cpp)
+    c->ctr.rounds += 1;
+    need(nitems < (size_t{1} << 31), EXPMC_EINVAL, "too many run_level requests in one batch");
+    ensure_items(c, nitems);
+#pragma omp parallel for schedule(static)
+    for (size_t k = 0; k < nitems; ++k) {
+        const expmc_level_req& r = req[slot[k]];
+        c->h_items[k] = make_item(r, beta, lane);
+        const uint64_t first_chunk = r.first_index / kChunk;
+        const uint64_t last_chunk = (r.first_index + r.count - 1) / kChunk;  // parallel.hpp:36-38
+        c->h_chunk0[k] = last_chunk - first_chunk + 1;
+    }
+    sample_items(c, nitems, lane, false);
     uint64_t samples = 0, jumps = 0, steps = 0;
 #pragma omp parallel for schedule(static) reduction(+ : samples, jumps, steps)
     for (size_t k = 0; k < nitems; ++k) {

@@ -130,6 +130,9 @@ struct SamplerArgs {
 };
 
 void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s);
+void launch_sampler_welford(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s);
+void launch_combine_welford(const uint64_t* chunk0, const DevItem* items, uint32_t nitems, uint64_t g_begin,
+                            uint64_t g_end, const ChunkPartials& partials, Partial* totals, cudaStream_t s);
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
                     const ChunkPartials& partials, bool with_extra, Partial* totals, cudaStream_t s);
 void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n,
@@ -168,4 +171,6 @@ void run_level_batch(expmc_ctx* ctx, double beta, uint32_t lane, const expmc_lev
                      int64_t nreq, expmc_level_stats* out);
 void set_error(const std::string& m);
 bool ctx_has_load(const expmc_ctx* c);
+// Classical MC batch (csrc/mc.cpp front end): validated requests, Welford reduction.
+void mc_batch(expmc_ctx* c, uint32_t lane, const expmc_mc_req* req, int64_t nreq, expmc_mc_result* out);
 }  // namespace expmc_b200

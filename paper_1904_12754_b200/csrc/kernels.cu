@@ -55,11 +55,37 @@ __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ chunk
     return lo;
 }
 
-template <class P>
+// Chan's pairwise merge of Welford accumulators (WelfordAcc::combine, parallel.hpp:92-104),
+// in the reference's evaluation order.
+__device__ __forceinline__ void welford_merge(double& mean, double& m2, uint64_t& n, double omean, double om2,
+                                              uint64_t on) {
+    if (on == 0) return;
+    if (n == 0) {
+        mean = omean;
+        m2 = om2;
+        n = on;
+        return;
+    }
+    const double delta = __dsub_rn(omean, mean);
+    const double total = static_cast<double>(n + on);
+    mean = __dadd_rn(mean, __dmul_rn(delta, __ddiv_rn(static_cast<double>(on), total)));
+    m2 = __dadd_rn(m2, __dadd_rn(om2, __dmul_rn(__dmul_rn(delta, delta),
+                                                 __ddiv_rn(__dmul_rn(static_cast<double>(n), static_cast<double>(on)),
+                                                           total))));
+    n += on;
+}
+
+// The path sampler.  Sums (W = false): per-chunk (sum x, sum x^2, cost, jumps) for run_level
+// (SumAcc).  Welford (W = true): the classical-MC accumulator (WelfordAcc, parallel.hpp:80-104):
+// every sample's value is parked in its chunk slot in shared memory and lane 0 folds the chunk
+// in sample order -- the reference's sequential Welford, so mc_* results match it.
+template <class P, bool W>
 __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned full = 0xFFFFFFFFu;
     const unsigned lt_mask = (1u << lane) - 1u;
+    __shared__ double s_x[W ? kWarps * kChunk : 1];
+    double* const wx = s_x + (W ? (threadIdx.x >> 5) * kChunk : 0);
     __shared__ LogEntry s_log[128];
     load_log_table(s_log);
     __syncthreads();
@@ -98,6 +124,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
         typename P::W w;
         bool active = false;
         uint32_t next = 0;
+        uint32_t my = 0;  // Welford: the running sample's slot in the chunk
         for (;;) {
             const unsigned need = __ballot_sync(full, !active);
             if (!active) {
@@ -105,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
                 if (mine < cnt) {
                     P::start(w, ic, a.init, a.rows, lo + mine);
                     active = true;
+                    if constexpr (W) my = mine;
                 }
             }
             next += __popc(need);
@@ -112,17 +140,36 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
             if (active && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps)) {
                 double ex;
                 const double x = P::sample(w, ic, a.init, a.rows, ex);
-                sum = __dadd_rn(sum, x);
-                sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
-                if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
+                if constexpr (W) {
+                    wx[my] = x;
+                } else {
+                    sum = __dadd_rn(sum, x);
+                    sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
+                    if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
+                }
                 cost += ic.nsteps;
                 active = false;
             }
         }
+        if constexpr (W) {  // WelfordAcc::add over the chunk in sample order (parallel.hpp:86-92)
+            __syncwarp();
+            if (lane == 0) {
+                double mean = 0.0, m2 = 0.0;
+                for (uint32_t k = 0; k < cnt; ++k) {
+                    const double x = wx[k];
+                    const double delta = __dsub_rn(x, mean);
+                    mean = __dadd_rn(mean, __ddiv_rn(delta, static_cast<double>(k + 1)));
+                    m2 = __dadd_rn(m2, __dmul_rn(delta, __dsub_rn(x, mean)));
+                }
+                sum = mean;
+                sum_sq = m2;
+            }
+            __syncwarp();
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            sum = __dadd_rn(sum, __shfl_xor_sync(full, sum, o));
-            sum_sq = __dadd_rn(sum_sq, __shfl_xor_sync(full, sum_sq, o));
+            if constexpr (!W) sum = __dadd_rn(sum, __shfl_xor_sync(full, sum, o));
+            if constexpr (!W) sum_sq = __dadd_rn(sum_sq, __shfl_xor_sync(full, sum_sq, o));
             if constexpr (P::kExtra) extra = __dadd_rn(extra, __shfl_xor_sync(full, extra, o));
             cost += __shfl_xor_sync(full, cost, o);
             jumps += __shfl_xor_sync(full, jumps, o);
@@ -154,6 +201,32 @@ __global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, 
         t.cost += p.cost[k];
         t.jumps += p.jumps[k];
     }
+    totals[i] = t;
+}
+
+// Welford combine: per item, Chan-merge its chunks' (mean, m2, n) in ascending chunk order
+// (parallel_samples' ordered combine, parallel.hpp:52).  n of a chunk is its sample count.
+__global__ void k_combine_welford(const uint64_t* __restrict__ chunk0, const DevItem* __restrict__ items,
+                                  uint32_t nitems, uint64_t g_begin, uint64_t g_end, ChunkPartials p,
+                                  Partial* __restrict__ totals) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nitems) return;
+    const uint64_t c0 = chunk0[i] > g_begin ? chunk0[i] : g_begin;
+    const uint64_t c1 = chunk0[i + 1] < g_end ? chunk0[i + 1] : g_end;
+    if (c0 >= c1) return;
+    Partial t = totals[i];  // sum = mean, sum_sq = m2, extra = n (exact below 2^53)
+    uint64_t n = static_cast<uint64_t>(t.extra);
+    const uint64_t first = items[i].first, end = first + items[i].count;
+    for (uint64_t g = c0; g < c1; ++g) {
+        const uint64_t k = g - g_begin;
+        const uint64_t chunk = first / kChunk + (g - chunk0[i]);
+        const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
+        const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
+        welford_merge(t.sum, t.sum_sq, n, p.sum[k], p.sum_sq[k], hi - lo);
+        t.cost += p.cost[k];
+        t.jumps += p.jumps[k];
+    }
+    t.extra = static_cast<double>(n);
     totals[i] = t;
 }
 
@@ -357,27 +430,50 @@ int sampler_threads() { return kThreads; }
 int sampler_blocks_per_sm(int mode) {
     int b = 0;
     if (mode == kSamplerFem)
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<FemPolicy>, kThreads, 0), "occupancy");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<FemPolicy, false>, kThreads, 0), "occupancy");
     else if (mode == EXPMC_SAMPLER_EVENT)
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<EdPolicy<false>>, kThreads, 0), "occupancy");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<EdPolicy<false>, false>, kThreads, 0),
+                   "occupancy");
     else
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<RefPolicy<false>>, kThreads, 0), "occupancy");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<RefPolicy<false>, false>, kThreads, 0),
+                   "occupancy");
     return b > 0 ? b : 1;
 }
 
 // Entry and forward mode are separate instantiations: a batch is one lane, and the entry-mode
 // kernel (the hot path) carries no trace of the forward start draw.
-void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s) {
-    if (lane == EXPMC_LANE_FEM) {
-        k_sample<FemPolicy><<<grid, kThreads, 0, s>>>(a);
-    } else if (mode == EXPMC_SAMPLER_EVENT) {
-        if (lane == EXPMC_LANE_FORWARD) k_sample<EdPolicy<true>><<<grid, kThreads, 0, s>>>(a);
-        else k_sample<EdPolicy<false>><<<grid, kThreads, 0, s>>>(a);
+template <bool W>
+void launch_sampler_t(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s) {
+    if constexpr (!W) {
+        if (lane == EXPMC_LANE_FEM) {
+            k_sample<FemPolicy, false><<<grid, kThreads, 0, s>>>(a);
+            cuda_check(cudaGetLastError(), "k_sample launch");
+            return;
+        }
+    }
+    if (mode == EXPMC_SAMPLER_EVENT) {
+        if (lane == EXPMC_LANE_FORWARD) k_sample<EdPolicy<true>, W><<<grid, kThreads, 0, s>>>(a);
+        else k_sample<EdPolicy<false>, W><<<grid, kThreads, 0, s>>>(a);
     } else {
-        if (lane == EXPMC_LANE_FORWARD) k_sample<RefPolicy<true>><<<grid, kThreads, 0, s>>>(a);
-        else k_sample<RefPolicy<false>><<<grid, kThreads, 0, s>>>(a);
+        if (lane == EXPMC_LANE_FORWARD) k_sample<RefPolicy<true>, W><<<grid, kThreads, 0, s>>>(a);
+        else k_sample<RefPolicy<false>, W><<<grid, kThreads, 0, s>>>(a);
     }
     cuda_check(cudaGetLastError(), "k_sample launch");
+}
+
+void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s) {
+    launch_sampler_t<false>(a, grid, mode, lane, s);
+}
+
+void launch_sampler_welford(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s) {
+    if (lane == EXPMC_LANE_FEM) throw Status(EXPMC_ENOTIMPL, "classical MC has no fem lane");
+    launch_sampler_t<true>(a, grid, mode, lane, s);
+}
+
+void launch_combine_welford(const uint64_t* chunk0, const DevItem* items, uint32_t nitems, uint64_t g_begin,
+                            uint64_t g_end, const ChunkPartials& partials, Partial* totals, cudaStream_t s) {
+    k_combine_welford<<<grid_for(nitems, 256), 256, 0, s>>>(chunk0, items, nitems, g_begin, g_end, partials, totals);
+    cuda_check(cudaGetLastError(), "k_combine_welford launch");
 }
 
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,

@@ -17,6 +17,7 @@ if ROOT not in sys.path:
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.json")
 GOLDEN_FORWARD = os.path.join(ROOT, "tests", "golden", "golden_forward.json")
 GOLDEN_FEM = os.path.join(ROOT, "tests", "golden", "golden_fem.json")
+GOLDEN_MC = os.path.join(ROOT, "tests", "golden", "golden_mc.json")
 
 
 def pytest_configure(config):
@@ -46,6 +47,12 @@ def golden_forward():
 @pytest.fixture(scope="session")
 def golden_fem():
     with open(GOLDEN_FEM) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def golden_mc():
+    with open(GOLDEN_MC) as f:
         return json.load(f)
 
 

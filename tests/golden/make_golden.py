@@ -260,7 +260,49 @@ def fem():
     print(path, os.path.getsize(path), "bytes")
 
 
+def mc():
+    """golden_mc.json: classical MC (mc.cpp:42-113) through the reference."""
+    ref = Reference()
+    out = {"generator": "tests/golden/make_golden.py mc() (reference: /root/reference/proj/core via oracle/_ref)"}
+    rng = np.random.default_rng(4)
+    cases = {"grid8": ref.chain(grid(8)), "smallw100": ref.smallw(100, 2, 0.1, 5), "pref300": ref.pref(300, 3, 7)}
+    out["matrices"] = {}
+    for name, ch in cases.items():
+        n = ch.n
+        u = np.round(rng.uniform(0.0, 2.0, n), 6)
+        beta = 1.0 if name == "grid8" else 1.0 / ch.decomposition()["d_max"]
+        single = []
+        for (entry, steps, samples, seed) in [(0, 4, 3000, 1), (n // 2, 12, 1537, 2), (n - 1, 1, 2, 3),
+                                              (7, 33, 5000, 4)]:
+            dt = beta / steps
+            r = ch.mc_single_entry(u, entry, beta, dt, samples, seed)
+            single.append(dict(entry=entry, seed=seed, req_samples=samples,
+                               **{k: (float(v).hex() if isinstance(v, float) else int(v)) for k, v in r.items()}))
+        t = ch.transposed()
+        forward = []
+        for (steps, samples, seed) in [(8, 4000, 5), (5, 1025, 6)]:
+            dt = beta / steps
+            r = t.mc_forward_scalar(u, beta, dt, samples, seed)
+            forward.append(dict(seed=seed, req_samples=samples,
+                                **{k: (float(v).hex() if isinstance(v, float) else int(v)) for k, v in r.items()}))
+        auto = []
+        eps = {"grid8": 1e-2, "smallw100": 5e-2, "pref300": 1e-2}[name]
+        for (entry, seed) in [(1, 10), (n // 3, 11)]:
+            r = ch.mc_auto(u, entry, beta, eps, seed)
+            auto.append(dict(entry=entry, epsilon=eps, seed=seed,
+                             **{k: (float(v).hex() if isinstance(v, float) else int(v)) for k, v in r.items()}))
+        out["matrices"][name] = dict(csr=csr_json(ch.a), csr_t=csr_json(t.a), u=hx(u), beta=float(beta).hex(),
+                                     single=single, forward=forward, auto=auto)
+    path = os.path.join(HERE, "golden_mc.json")
+    with open(path, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print(path, os.path.getsize(path), "bytes")
+
+
 if __name__ == "__main__":
+    if "--mc-only" in sys.argv:
+        mc()
+        sys.exit(0)
     if "--fem-only" in sys.argv:
         fem()
         sys.exit(0)
@@ -268,3 +310,4 @@ if __name__ == "__main__":
         main()
     forward()
     fem()
+    mc()
