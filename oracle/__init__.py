@@ -443,6 +443,13 @@ class Reference(_Backend):
         self._check(self.lib.ref_from_triplets(_I64(n), _I64(r.size), _ptr(r), _ptr(c), _ptr(v), C.byref(h)))
         return RefChain(self, None, handle=h)
 
+    def fit_slope(self, x, y, loglog=False):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        out = _D()
+        self._check(self.lib.ref_fit_slope(_INT(int(loglog)), _I64(x.size), _ptr(x), _ptr(y), C.byref(out)))
+        return out.value
+
     def read_vector(self, path):
         n = _I64()
         self._check(self.lib.ref_read_vector(os.fsencode(path), _I64(0), None, C.byref(n)))
@@ -669,6 +676,34 @@ class RefChain(_Chain):
         self.be._check(self.be.lib.ref_mc_auto(self.h, _ptr(u), _I64(entry), _D(beta), _D(epsilon), _U64(seed),
                                                _INT(threads), C.byref(r)))
         return _mc_dict(r)
+
+    # ---- paper-figure harness (harness.cpp:61-144)
+    def bench_levels(self, u, entry, beta, l0, count, samples, seed, threads=4):
+        u = np.ascontiguousarray(u, np.float64)
+        rows = np.zeros((count, 5))
+        slopes = np.zeros(3)
+        self.be._check(self.be.lib.ref_bench_levels(self.h, _ptr(u), _I64(entry), _D(beta), _INT(l0), _INT(count),
+                                                    _U64(samples), _U64(seed), _INT(threads), _ptr(rows),
+                                                    _ptr(slopes)))
+        return rows, slopes
+
+    def bench_l0(self, u, entry, beta, l0_min, l0_max, epsilon, seed, threads=4):
+        u = np.ascontiguousarray(u, np.float64)
+        costs = np.zeros(l0_max - l0_min + 1)
+        best, heur = C.c_int(), C.c_int()
+        self.be._check(self.be.lib.ref_bench_l0(self.h, _ptr(u), _I64(entry), _D(beta), _INT(l0_min), _INT(l0_max),
+                                                _D(epsilon), _U64(seed), _INT(threads), _ptr(costs), C.byref(best),
+                                                C.byref(heur)))
+        return costs, best.value, heur.value
+
+    def bench_complexity(self, u, entry, beta, epsilons, seed, threads=4):
+        u = np.ascontiguousarray(u, np.float64)
+        eps = np.ascontiguousarray(epsilons, np.float64)
+        ml, mc, sl = np.zeros(eps.size), np.zeros(eps.size), np.zeros(2)
+        self.be._check(self.be.lib.ref_bench_complexity(self.h, _ptr(u), _I64(entry), _D(beta), _I64(eps.size),
+                                                        _ptr(eps), _U64(seed), _INT(threads), _ptr(ml), _ptr(mc),
+                                                        _ptr(sl)))
+        return ml, mc, sl
 
     def dense_expmv(self, u, beta):
         u = np.ascontiguousarray(u, np.float64)

@@ -27,6 +27,7 @@
 #include "expmc/communicability.hpp"
 #include "expmc/fem.hpp"
 #include "expmc/io.hpp"
+#include "expmc/harness.hpp"
 #include "expmc/mc.hpp"
 #include "expmc/mlmc.hpp"
 #include "expmc/netgen.hpp"
@@ -652,6 +653,73 @@ int ref_mc_auto(void* h, const double* u, int64_t entry, double beta, double eps
         put_mc(mc_auto(m->dec, std::span<const double>(u, static_cast<std::size_t>(m->dec.n)), entry, beta, epsilon,
                        seed, threads),
                out);
+    });
+}
+
+// Paper-figure harness (harness.cpp:41-144), entry mode.
+int ref_fit_slope(int loglog, int64_t n, const double* x, const double* y, double* out) {
+    return guarded([&] {
+        const std::span<const double> xs(x, static_cast<std::size_t>(n)), ys(y, static_cast<std::size_t>(n));
+        *out = loglog ? fit_loglog_slope(xs, ys) : fit_log2_slope(xs, ys);
+    });
+}
+
+int ref_bench_levels(void* h, const double* u, int64_t entry, double beta, int l0, int count, uint64_t samples,
+                     uint64_t seed, int threads, double* rows /* count x 5 */, double* slopes /* 3 */) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.entry = entry;
+        p.beta = beta;
+        const LevelDecayReport r = bench_levels(p, l0, count, samples, seed, threads);
+        for (std::size_t i = 0; i < r.rows.size(); ++i) {
+            rows[5 * i + 0] = r.rows[i].level;
+            rows[5 * i + 1] = r.rows[i].dt;
+            rows[5 * i + 2] = r.rows[i].mean;
+            rows[5 * i + 3] = r.rows[i].variance;
+            rows[5 * i + 4] = r.rows[i].cost_per_sample;
+        }
+        slopes[0] = r.slope_mean;
+        slopes[1] = r.slope_variance;
+        slopes[2] = r.slope_cost_tail;
+    });
+}
+
+int ref_bench_l0(void* h, const double* u, int64_t entry, double beta, int l0_min, int l0_max, double epsilon,
+                 uint64_t seed, int threads, double* costs, int* best, int* heuristic) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.entry = entry;
+        p.beta = beta;
+        const L0Report r = bench_l0(p, l0_min, l0_max, epsilon, seed, threads);
+        for (std::size_t i = 0; i < r.points.size(); ++i) costs[i] = r.points[i].cost;
+        *best = r.best_l0;
+        *heuristic = r.heuristic_l0;
+    });
+}
+
+int ref_bench_complexity(void* h, const double* u, int64_t entry, double beta, int64_t neps, const double* eps,
+                         uint64_t seed, int threads, double* mlmc_cost, double* mc_cost, double* slopes) {
+    return guarded([&] {
+        auto* m = static_cast<RefMatrix*>(h);
+        MlmcProblem p;
+        p.dec = &m->dec;
+        p.u = std::span<const double>(u, static_cast<std::size_t>(m->dec.n));
+        p.entry = entry;
+        p.beta = beta;
+        const ComplexityReport r =
+            bench_complexity(p, std::span<const double>(eps, static_cast<std::size_t>(neps)), seed, threads);
+        for (std::size_t i = 0; i < r.mlmc.size(); ++i) {
+            mlmc_cost[i] = r.mlmc[i].cost;
+            mc_cost[i] = r.mc[i].cost;
+        }
+        slopes[0] = r.slope_mlmc;
+        slopes[1] = r.slope_mc;
     });
 }
 
