@@ -172,11 +172,13 @@ def load_peaks():
 
 
 def load_traffic():
-    """DRAM bytes per k_sample launch from the committed ncu capture (profiles/ncu_traffic.json)."""
+    """DRAM bytes per ms of k_sample time from the committed ncu capture (profiles/ncu_traffic.json:
+    dram__bytes_read.sum + dram__bytes_write.sum of one C2 main-round launch / its duration)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
         with open(path) as f:
-            return json.load(f).get("bytes_per_launch")
+            t = json.load(f)
+        return t["dram_bytes"] / t["launch_ms"]
     return None
 
 
@@ -351,7 +353,10 @@ def main():
     achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
     peaks, peak_src = load_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = load_traffic()
+    traffic_rate = load_traffic()
+    launches = max(1, ctr["sampler_launches"])
+    # per launch, like `achieved`: the capture's DRAM bytes per kernel-ms x this run's mean launch length
+    traffic = traffic_rate * ctr["sampler_ms"] / launches if traffic_rate else None
     gather_l2 = gather_hbm = None
     if rank == 0:
         try:
@@ -432,7 +437,8 @@ def main():
                          "kernel": "k_sample", "sampler_launches": ctr["sampler_launches"],
                          "kernel_ms": ctr["sampler_ms"], "step_share": ctr["sampler_ms"] / ms_local,
                          "alg_bytes_per_launch": alg_bytes / max(1, ctr["sampler_launches"]),
-                         "traffic_source": "profiles/ncu_traffic.json (C2 main-round launch, ncu --set full)",
+                         "traffic_source": "profiles/ncu_traffic.json (C2 main-round launch, ncu --set full): "
+                                           "DRAM bytes per kernel-ms x this run's mean launch ms",
                          "alg_bytes": f"{ALG_BYTES_PER_JUMP} B/transition + {ALG_BYTES_PER_SAMPLE} B/sample",
                          "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
                          "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},

@@ -25,6 +25,10 @@ namespace expmc_b200 {
 
 namespace {
 
+#ifndef EXPMC_MERGED_RESTART
+#define EXPMC_MERGED_RESTART 1
+#endif
+
 #ifndef EXPMC_SAMPLER_MINB
 #define EXPMC_SAMPLER_MINB 4  // resident 256-thread blocks per SM the sampler is register-budgeted for
 #endif
@@ -123,8 +127,42 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
         unsigned long long cost = 0, jumps = 0;
         typename P::W w;
         bool active = false;
-        uint32_t next = 0;
         uint32_t my = 0;  // Welford: the running sample's slot in the chunk
+#if EXPMC_MERGED_RESTART
+        // Lanes start samples lo + lane; a lane whose sample ends takes the next unstarted
+        // index in the same divergent section as its finish (one ballot per trip).
+        if (lane < cnt) {
+            P::start(w, ic, a.init, a.rows, lo + lane);
+            active = true;
+            if constexpr (W) my = lane;
+        }
+        uint32_t next = cnt < 32u ? cnt : 32u;
+        while (__any_sync(full, active)) {
+            const bool done = active && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps);
+            const unsigned fin = __ballot_sync(full, done);
+            if (done) {
+                double ex;
+                const double x = P::sample(w, ic, a.init, a.rows, ex);
+                if constexpr (W) {
+                    wx[my] = x;
+                } else {
+                    sum = __dadd_rn(sum, x);
+                    sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
+                    if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
+                }
+                cost += ic.nsteps;
+                const uint32_t mine = next + __popc(fin & lt_mask);
+                if (mine < cnt) {
+                    P::start(w, ic, a.init, a.rows, lo + mine);
+                    if constexpr (W) my = mine;
+                } else {
+                    active = false;
+                }
+            }
+            next += __popc(fin);
+        }
+#else
+        uint32_t next = 0;
         for (;;) {
             const unsigned need = __ballot_sync(full, !active);
             if (!active) {
@@ -151,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
                 active = false;
             }
         }
+#endif
         if constexpr (W) {  // WelfordAcc::add over the chunk in sample order (parallel.hpp:86-92)
             __syncwarp();
             if (lane == 0) {
