@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -65,6 +66,26 @@ double bias_estimate_impl(size_t n, const double* means) {  // mlmc.cpp:45-51
     const double prev = std::abs(means[n - 2]);
     return std::max(last, prev / 4.0) / 3.0;
 }
+
+// A growable array of trivially copyable T whose new elements are left uninitialised.
+template <class T>
+struct RawArray {
+    std::unique_ptr<T[]> p;
+    size_t n = 0, cap = 0;
+    void resize(size_t m) {
+        if (m > cap) {
+            std::unique_ptr<T[]> q(new T[m]);  // default-init: no zeroing pass
+            if (n) std::memcpy(q.get(), p.get(), n * sizeof(T));
+            p = std::move(q);
+            cap = m;
+        }
+        n = m;
+    }
+    size_t size() const { return n; }
+    T* data() { return p.get(); }
+    T& operator[](size_t i) { return p[i]; }
+    const T& operator[](size_t i) const { return p[i]; }
+};
 
 enum class Phase { waiting_warmup, waiting_extend, waiting_added, done };
 
@@ -190,6 +211,8 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
         s.l0 = l0;
         s.cap = cap;
         s.top = std::min(l0 + 4, cap);  // mlmc.cpp:201-205
+        s.lv.reserve(8);  // one allocation each for the common L - l0 < 8
+        s.pending.reserve(8);
         s.lv.resize(static_cast<size_t>(s.top - l0 + 1));
         for (int i = 0; i <= s.top - l0; ++i) s.pending.emplace_back(i, opt.warmup);
     }
@@ -197,8 +220,10 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
     // Per round: (1) every active row's pending extensions become one contiguous slice of the
     // batch, (2) one batched GPU pass, (3) each row applies its slice (extend(), mlmc.cpp:188-199)
     // and advances its state machine.  Rows are independent, so (1) and (3) run in parallel.
-    std::vector<expmc_level_req> req;
-    std::vector<expmc_level_stats> res;
+    // request / result arrays: grown without value-initialisation, first touched by the parallel
+    // fill (round 0 stages ~5 requests per row: hundreds of MB at n = 2^20)
+    RawArray<expmc_level_req> req;
+    RawArray<expmc_level_stats> res;
     std::vector<size_t> off;
     std::vector<unsigned char> keep;
     std::vector<int64_t> active(static_cast<size_t>(nrows));
@@ -212,7 +237,7 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
         off.assign(na + 1, 0);
         for (size_t i = 0; i < na; ++i) off[i + 1] = off[i] + st[static_cast<size_t>(active[i])].pending.size();
         req.resize(off[na]);
-        res.resize(off[na]);
+        res.resize(off[na]);  // run_level_batch writes every element
 #pragma omp parallel for schedule(static)
         for (size_t i = 0; i < na; ++i) {
             const RowState& s = st[static_cast<size_t>(active[i])];
@@ -266,7 +291,7 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
             if (keep[i]) active[m++] = active[i];
         if (trace) {
             uint64_t smp = 0;
-            for (const auto& q : req) smp += q.count;
+            for (size_t q = 0; q < req.size(); ++q) smp += req[q].count;
             const auto t3 = clk::now();
             auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
             std::fprintf(stderr, "[expmc] round %d rows %zu reqs %zu samples %llu | build %.2f ms gpu %.2f ms advance %.2f ms\n",
