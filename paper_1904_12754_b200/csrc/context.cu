@@ -59,6 +59,8 @@ struct expmc_ctx {
     // forward mode: CDF of u and sum(u) (make_initial_distribution, paths.cpp:12-28), built on
     // the first forward request and dropped by set_vector
     double* d_init_cdf = nullptr;
+    uint32_t* d_init_guide = nullptr;  // bucket guide over the CDF (exact upper_bound ranges)
+    uint32_t guide_bits = 0;
     double init_total = 0.0;
     bool init_valid = false;
     double* d_load = nullptr;  // fem: MlmcProblem::load (mlmc.hpp:53), set by expmc_ctx_set_load
@@ -238,6 +240,24 @@ void ensure_forward_init(expmc_ctx* c) {
     need(total > 0.0, EXPMC_EINVAL, "forward sampling requires sum(u) > 0");
     for (double& x : cdf) x /= total;
     cdf.back() = 1.0;
+    // Guide table: 2^b buckets (b = ceil(log2 n), 4..24), guide[k] = upper_bound(cdf, k 2^-b).
+    // A draw v = K 2^-53 lies in bucket k = K >> (53 - b), i.e. k 2^-b <= v < (k+1) 2^-b exactly,
+    // so upper_bound(v) lies in [guide[k], guide[k+1]]: the device searches that range only.
+    uint32_t bits = 4;
+    while (bits < 24 && (size_t{1} << bits) < n) ++bits;
+    const size_t nb = (size_t{1} << bits) + 1;
+    std::vector<uint32_t> guide(nb);
+#pragma omp parallel for schedule(static)
+    for (size_t k = 0; k < nb; ++k) {
+        const double edge = std::ldexp(static_cast<double>(k), -static_cast<int>(bits));
+        guide[k] = static_cast<uint32_t>(std::upper_bound(cdf.begin(), cdf.end(), edge) - cdf.begin());
+    }
+    if (!c->d_init_guide || bits != c->guide_bits) dev_alloc(&c->d_init_guide, nb);
+    c->guide_bits = bits;
+    cuda_check(cudaMemcpyAsync(c->d_init_guide, guide.data(), nb * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               c->stream),
+               "H2D guide");
+    c->ctr.h2d_bytes += nb * sizeof(uint32_t);
     if (!c->d_init_cdf) dev_alloc(&c->d_init_cdf, n);
     cuda_check(cudaMemcpyAsync(c->d_init_cdf, cdf.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream),
                "H2D initial CDF");
@@ -248,8 +268,9 @@ void ensure_forward_init(expmc_ctx* c) {
 }
 
 LaneData lane_data(const expmc_ctx* c) {
-    LaneData ld = c->init_valid ? LaneData{c->d_init_cdf, c->init_total, static_cast<uint32_t>(c->n), nullptr}
-                                : LaneData{nullptr, 0.0, 0u, nullptr};
+    LaneData ld = c->init_valid ? LaneData{c->d_init_cdf, c->init_total, static_cast<uint32_t>(c->n), nullptr,
+                                           c->d_init_guide, c->guide_bits}
+                                : LaneData{nullptr, 0.0, 0u, nullptr, nullptr, 0u};
     ld.load = c->d_load;
     return ld;
 }
@@ -664,6 +685,7 @@ void expmc_ctx_destroy(expmc_ctx* c) {
     if (c->nccl) nccl().comm_destroy(c->nccl);
     cudaFree(c->d_counter);
     cudaFree(c->d_init_cdf);
+    cudaFree(c->d_init_guide);
     cudaFree(c->d_load);
     cudaFree(c->d_dbg);
     if (c->cap_h) {  // staging blocks go back to the process-wide pool

@@ -40,7 +40,7 @@ __device__ __forceinline__ double simpson_weight(uint64_t j, uint64_t panels, do
 
 __device__ __forceinline__ void fem_start(FemWalker& f, const ItemConst& ic, const double* __restrict__ load,
                                           const RowRec* __restrict__ rows, uint64_t sample) {
-    walker_start<false>(f.w, ic, LaneData{nullptr, 0.0, 0u, nullptr}, rows, sample);
+    walker_start<false>(f.w, ic, LaneData{nullptr, 0.0, 0u, nullptr, nullptr, 0u}, rows, sample);
     const double g0 = __ldg(load + ic.entry);
     f.integ_f = __dmul_rn(ic.h_fine, g0);    // fine_w[0] * load[entry]            paths.cpp:195, 223
     f.integ_c = __dmul_rn(ic.h_coarse, g0);  // coarse_w[0] * load[entry]          paths.cpp:224

@@ -71,6 +71,8 @@ struct LaneData {
     double total;
     uint32_t n;
     const double* load;
+    const uint32_t* guide;  // forward: guide[k] = upper_bound(cdf, k / 2^gbits), k = 0..2^gbits
+    uint32_t gbits;
 };
 
 // Per-chunk partial and per-item running total (SumAcc, parallel.hpp:57-78, + jumps).

@@ -213,8 +213,12 @@ template <bool F>
 __device__ __forceinline__ uint32_t draw_start(Stream& st, const ItemConst& ic, const LaneData& fi) {
     if (!F) return ic.entry;
     stream_reserve2(st);
-    const double v = stream_pop(st);
-    uint32_t lo = 0, count = fi.n;
+    const uint64_t k53 = stream_pop_bits(st);
+    const double v = to_uniform(k53);
+    // the draw's guide bucket bounds the search (context.cu: ensure_forward_init)
+    const uint32_t b = static_cast<uint32_t>(k53 >> (53u - fi.gbits));
+    uint32_t lo = __ldg(fi.guide + b);
+    uint32_t count = __ldg(fi.guide + b + 1) - lo;
     while (count > 0u) {
         const uint32_t step = count >> 1;
         const uint32_t it = lo + step;
