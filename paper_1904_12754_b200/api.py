@@ -62,13 +62,13 @@ class IoError(ExpmcError):
     """std::runtime_error of the readers: "path:line: what" (io.cpp)."""
 
 
-class OverflowError_(ExpmcError, OverflowError):
+class StepOverflowError(ExpmcError, OverflowError):
     """std::overflow_error (mc_auto)."""
 
 
 _ERR = {L.EXPMC_EINVAL: InvalidArgument, L.EXPMC_ERANGE: OutOfRange, L.EXPMC_EDOMAIN: DomainError,
         L.EXPMC_ECUDA: CudaError, L.EXPMC_ENOTIMPL: NotImplementedMode, L.EXPMC_EIO: IoError,
-        L.EXPMC_EOVERFLOW: OverflowError_}
+        L.EXPMC_EOVERFLOW: StepOverflowError}
 
 
 def _check(rc: int) -> None:
