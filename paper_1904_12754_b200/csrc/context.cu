@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -275,6 +276,16 @@ LaneData lane_data(const expmc_ctx* c) {
     return ld;
 }
 
+// Samples parallel_samples actually draws for [first, first + count) (parallel.hpp:39-50): all
+// of them, except that a chunk whose end (chunk + 1) * 512 wraps to 0 at 2^64 contributes none.
+uint64_t sampled_count(uint64_t first, uint64_t count) {
+    if (count == 0) return 0;
+    const uint64_t last_chunk = (first + count - 1) / kChunk;
+    if ((last_chunk + 1) * kChunk != 0) return count;
+    const uint64_t lo = first > last_chunk * kChunk ? first : last_chunk * kChunk;
+    return count - ((first + count) - lo);
+}
+
 DevItem make_item(const expmc_level_req& r, double beta, uint32_t lane) {
     DevItem it{};
     const uint64_t steps = uint64_t{1} << r.level;
@@ -335,7 +346,10 @@ void sample_items(expmc_ctx* c, size_t nitems, uint32_t lane, bool welford) {
     c->ctr.h2d_bytes += nitems * sizeof(DevItem) + (nitems + 1) * sizeof(uint64_t);
     cuda_check(cudaMemsetAsync(c->d_totals, 0, nitems * sizeof(Partial), c->stream), "memset totals");
     if (!c->d_pf) {
-        c->cap_partials = kWindowChunks;
+        // EXPMC_WINDOW_CHUNKS (tests): a small window exercises the multi-launch path
+        const char* wenv = std::getenv("EXPMC_WINDOW_CHUNKS");
+        const uint64_t wreq = wenv ? std::strtoull(wenv, nullptr, 10) : 0;
+        c->cap_partials = wreq > 0 && wreq < kWindowChunks ? wreq : kWindowChunks;
         dev_alloc(&c->d_pf, 3 * c->cap_partials);
         dev_alloc(&c->d_pu, 2 * c->cap_partials);
         dev_alloc(&c->d_counter, 1);
@@ -513,13 +527,13 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         expmc_level_stats& o = out[slot[k]];
         o.sum = c->h_totals[k].sum;
         o.sum_sq = c->h_totals[k].sum_sq;
-        o.samples = r.count;
+        o.samples = sampled_count(r.first_index, r.count);
         o.cost = c->h_totals[k].cost;
         o.jumps = c->h_totals[k].jumps;
         o.integ_sum = c->h_totals[k].extra;
-        samples += r.count;
+        samples += o.samples;
         jumps += o.jumps;
-        steps += r.count << r.level;
+        steps += o.samples << r.level;
     }
     c->ctr.samples += samples;
     c->ctr.jumps += jumps;

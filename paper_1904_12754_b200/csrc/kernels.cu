@@ -121,7 +121,9 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
         const uint64_t chunk = first / kChunk + (g - a.chunk0[item]);
         const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
         const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
-        const uint32_t cnt = static_cast<uint32_t>(hi - lo);
+        // parallel.hpp:46-49 in uint64: for the chunk ending at 2^64 the reference's bound
+        // (chunk + 1) * kChunk wraps to 0 and its sample loop runs zero times -- so does this one
+        const uint32_t cnt = hi > lo ? static_cast<uint32_t>(hi - lo) : 0u;
 
         double sum = 0.0, sum_sq = 0.0, extra = 0.0;
         unsigned long long cost = 0, jumps = 0;
@@ -261,7 +263,7 @@ __global__ void k_combine_welford(const uint64_t* __restrict__ chunk0, const Dev
         const uint64_t chunk = first / kChunk + (g - chunk0[i]);
         const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
         const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
-        welford_merge(t.sum, t.sum_sq, n, p.sum[k], p.sum_sq[k], hi - lo);
+        welford_merge(t.sum, t.sum_sq, n, p.sum[k], p.sum_sq[k], hi > lo ? hi - lo : 0);
         t.cost += p.cost[k];
         t.jumps += p.jumps[k];
     }

@@ -1,0 +1,125 @@
+"""Edge cases of the CUDA path (through the C-ABI): empty and degenerate inputs, extreme seeds
+and sample indices, isolated / absorbing rows, the multi-launch sampler window, and batches
+mixing every lane-independent request shape.  Each is checked against the oracle (bit-exact
+integer work, <= 4 ulp values, 1e-12 sums) or against a closed form."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_1904_12754_b200 as P
+from oracle import CSR
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ulp_diff(a, b):
+    ia = np.asarray(a, np.float64).view(np.int64)
+    ib = np.asarray(b, np.float64).view(np.int64)
+    ia = np.where(ia < 0, np.int64(-(2 ** 63)) - ia, ia)
+    ib = np.where(ib < 0, np.int64(-(2 ** 63)) - ib, ib)
+    return np.abs(ia - ib)
+
+
+def test_empty_matrix_and_empty_batches(gpu):
+    e = P.SparseMatrix.from_triplets(0, [], [], [])
+    with P.Context(e, np.zeros(0)) as ctx:
+        assert ctx.n == 0 and ctx.n_edges == 0
+        assert ctx.run_level_batch(1.0, [], [], [], [], [], []).size == 0
+        with pytest.raises(P.OutOfRange):
+            P.run_level(P.MlmcProblem(ctx, 0, 1.0), 0, True, 0, 10, 1)
+    z = P.SparseMatrix.from_triplets(3, [], [], [])  # zero matrix: every row absorbing, e^{0} = I
+    with P.Context(z, [1.0, -2.0, 3.0]) as ctx:
+        st = P.run_level(P.MlmcProblem(ctx, 1, 1.0), 3, True, 0, 1000, 5)
+        assert st.sum == -2000.0 and st.sum_sq == 4000.0 and st.cost == 1000 * 8 and st.jumps == 0
+        # count = 0 requests (any level, even 62) do nothing and raise nothing
+        out = ctx.run_level_batch(1.0, [0, 1, 2], [62, 0, 5], [0, 1, 0], [0, 0, 0], [0, 0, 0], [1, 2, 3])
+        assert np.all(out["samples"] == 0) and np.all(out["sum"] == 0.0)
+
+
+def test_extreme_seeds_and_indices(gpu, oracle_lib):
+    a = P.SparseMatrix.from_dense([[0.1, -1.0, 0.5], [0.7, -0.2, -0.2], [-0.4, 0.0, 0.3]])
+    u = np.array([0.3, -1.1, 2.0])
+    och = oracle_lib.chain(CSR(a.n, a.row_ptr, a.col, a.val))
+    idx = np.array([0, 2 ** 32 - 1, 2 ** 32, 2 ** 63, 2 ** 64 - 2, 2 ** 64 - 1], np.uint64)
+    with P.Context(a, u) as ctx:
+        for seed in (0, 1, 2 ** 32 - 1, 2 ** 63 + 11, 2 ** 64 - 1):
+            for level, base in ((0, 1), (4, 0), (9, 0)):
+                got = ctx.sample_debug(0.9, 2, level, base, seed, idx)
+                exp = och.samples(u, 2, 0.9, level, base, seed, idx)
+                assert np.array_equal(got["cost"], exp["cost"]) and np.array_equal(got["end_state"], exp["end_state"])
+                assert ulp_diff(got["fine"], exp["fine"]).max() <= 4
+                assert ulp_diff(got["coarse"], exp["coarse"]).max() <= 4
+        # run_level ranges near the top of the index space.  The reference's chunk bound
+        # (chunk + 1) * 512 wraps to 0 for the last chunk before 2^64 and that chunk draws no
+        # samples (parallel.hpp:46-49); the GPU path reproduces it, sample count included.
+        for first, count in ((2 ** 64 - 1 - 700, 700), (2 ** 64 - 2 ** 20, 1000), (2 ** 64 - 600, 100)):
+            st = P.run_level(P.MlmcProblem(ctx, 0, 0.9), 3, False, first, count, 2 ** 64 - 1)
+            o = och.run_level(u, 0, 0.9, 3, 0, first, count, 2 ** 64 - 1)
+            assert (st.samples, st.cost, st.jumps) == (o["samples"], o["cost"], o["jumps"])
+            assert st.sum == pytest.approx(o["sum"], rel=1e-12, abs=1e-13)
+
+
+def test_isolated_and_absorbing_rows(gpu, oracle_lib):
+    # row 1 isolated (no entries), row 3 with only a diagonal, row 0 pointing into both
+    a = P.SparseMatrix.from_triplets(4, [0, 0, 0, 2, 2, 3], [1, 3, 2, 0, 2, 3], [0.5, -0.25, 1.0, 0.3, -1.0, -0.7])
+    u = np.array([1.0, 2.0, -3.0, 0.5])
+    och = oracle_lib.chain(CSR(a.n, a.row_ptr, a.col, a.val))
+    with P.Context(a, u) as ctx:
+        dec = ctx.decomposition()
+        assert dec["rate"][1] == 0.0 and dec["rate"][3] == 0.0
+        for entry in range(4):
+            for level, base in ((0, 1), (3, 0), (6, 0)):
+                idx = np.arange(300, dtype=np.uint64)
+                got = ctx.sample_debug(1.3, entry, level, base, 77 + entry, idx)
+                exp = och.samples(u, entry, 1.3, level, base, 77 + entry, idx)
+                assert np.array_equal(got["cost"], exp["cost"]) and np.array_equal(got["jumps"], exp["jumps"])
+                assert ulp_diff(got["fine"], exp["fine"]).max() <= 4
+
+
+def test_multi_window_launches_are_bitwise_identical(gpu, tmp_path):
+    """The sampler's chunk-partial window (4M chunks per launch by default) set to 7 chunks in a
+    child process: every request spans windows, the per-item combine continues across launches
+    -- the results must equal the single-window run bit for bit."""
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1904_12754_b200 as P
+from paper_1904_12754_b200 import configs
+cfg = configs.make_config("c1")
+with P.Context(cfg.a, cfg.u) as ctx:
+    e = np.arange(40) * 97 % cfg.a.n
+    out = ctx.run_level_batch(cfg.beta, e, np.arange(40) % 5, (np.arange(40) % 5 == 0).astype(np.int32),
+                              np.arange(40) * 311, 3000 + np.arange(40) * 17, 1000 + e)
+    fw = ctx.run_level_batch(cfg.beta, 0, 2, 0, 0, 50000, 9, lane=P.LANE_FORWARD)
+    np.save(sys.argv[2], np.concatenate([out, fw]))
+'''
+    res = {}
+    for w in ("", "7"):
+        env = dict(os.environ)
+        if w:
+            env["EXPMC_WINDOW_CHUNKS"] = w
+        path = str(tmp_path / f"w{w or 'default'}.npy")
+        subprocess.run([sys.executable, "-c", code, ROOT, path], check=True, env=env)
+        res[w] = np.load(path)
+    assert res[""].tobytes() == res["7"].tobytes()
+
+
+def test_long_paths_and_mixed_batch(gpu, oracle_lib):
+    """Levels up to 12 (4096 fine steps per sample) next to level-0 requests in one batch."""
+    from paper_1904_12754_b200 import configs
+
+    cfg = configs.make_config("c1")
+    och = oracle_lib.chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
+    with P.Context(cfg.a, cfg.u) as ctx:
+        reqs = [(5, 12, 0, 0, 40), (9, 0, 1, 3, 5000), (4095, 7, 0, 600, 513), (2048, 1, 0, 0, 1)]
+        out = ctx.run_level_batch(cfg.beta, [r[0] for r in reqs], [r[1] for r in reqs], [r[2] for r in reqs],
+                                  [r[3] for r in reqs], [r[4] for r in reqs], [1000 + r[0] for r in reqs])
+        for k, (e, l, b, f, c) in enumerate(reqs):
+            o = och.run_level(cfg.u, e, cfg.beta, l, b, f, c, 1000 + e)
+            assert int(out[k]["cost"]) == o["cost"] and int(out[k]["jumps"]) == o["jumps"]
+            assert float(out[k]["sum"]) == pytest.approx(o["sum"], rel=1e-12, abs=1e-13)
