@@ -182,6 +182,16 @@ def load_traffic():
     return None
 
 
+def load_issue_active():
+    """Issue-slot utilisation of k_sample from the committed ncu capture (the kernel's real bound)."""
+    path = os.path.join(ROOT, "profiles", "r01", "k_sample_r1c_key_metrics.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["smsp__issue_active.avg.pct_of_peak_sustained_active"]["value"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 # ------------------------------------------------------------------------------ reference arm
 def reference_rows(ref_chain, cfg, rows, seconds, threads, max_rows):
     """Reference mlmc_driver on rows one at a time, in a worker thread, for at most `seconds`.
@@ -441,6 +451,9 @@ def main():
                                            "DRAM bytes per kernel-ms x this run's mean launch ms",
                          "alg_bytes": f"{ALG_BYTES_PER_JUMP} B/transition + {ALG_BYTES_PER_SAMPLE} B/sample",
                          "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
+                         "issue_active_pct": load_issue_active(),
+                         "binding_resource": "instruction issue (ncu smsp__issue_active, "
+                                             "profiles/r01/k_sample_r1c_key_metrics.json)",
                          "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches), "clocks": clk,
         }
