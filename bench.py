@@ -182,6 +182,28 @@ def load_traffic():
     return None
 
 
+def sampler_only_rate(ref_chain, cfg, threads, seconds=4.0):
+    """The reference's sampler without the driver: one large run_level per level
+    (its LevelSampler table is built once per call, so the O(n) construction is amortised),
+    OpenMP on all cores.  transitions = cost - 2 M 2^l (every fine step of a non-absorbing row
+    ends with one draw).  Level 0 (base) and level 2 (coupled), each sized to ~seconds/2."""
+    out = {}
+    row = cfg.a.n // 2 + 7
+    for level, base in ((0, True), (2, False)):
+        m = 1 << 16
+        t0 = time.perf_counter()
+        ref_chain.run_level(cfg.u, row, cfg.beta, level, base, 0, m, 99, threads=threads)
+        probe = time.perf_counter() - t0
+        m = max(m, int(m * (seconds / 2) / max(probe, 1e-3)))
+        t0 = time.perf_counter()
+        r = ref_chain.run_level(cfg.u, row, cfg.beta, level, base, 1 << 40, m, 99, threads=threads)
+        dt = time.perf_counter() - t0
+        jumps = r["cost"] - 2 * m * (1 << level)
+        out[f"level{level}"] = {"transitions_per_s": jumps / dt, "samples_per_s": m / dt, "samples": m,
+                                "seconds": dt}
+    return out
+
+
 def load_issue_active():
     """Issue-slot utilisation of k_sample from the committed ncu capture (the kernel's real bound)."""
     path = os.path.join(ROOT, "profiles", "r01", "k_sample_r1c_key_metrics.json")
@@ -421,7 +443,8 @@ def main():
                                                   args.ref_seconds, threads, 1 << 30)
                 cpu = {"value": j / dt if done else None, "unit": UNIT, "cores": threads, "kind": "reference",
                        "sample": f"{done} randomly chosen {cfg.name.upper()} components through the as-shipped reference "
-                                 f"mlmc_driver (OpenMP, {dt:.1f} s)", "rows_per_s": done / dt if done else None}
+                                 f"mlmc_driver (OpenMP, {dt:.1f} s)", "rows_per_s": done / dt if done else None,
+                       "sampler_only": sampler_only_rate(ref, cfg, threads)}
         except Exception as exc:  # baseline failure must not hide the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
 
