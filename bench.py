@@ -191,13 +191,13 @@ def sampler_only_rate(ref_chain, cfg, threads, seconds=4.0):
     row = cfg.a.n // 2 + 7
     for level, base in ((0, True), (2, False)):
         m = 1 << 16
-        t0 = time.perf_counter()
-        ref_chain.run_level(cfg.u, row, cfg.beta, level, base, 0, m, 99, threads=threads)
-        probe = time.perf_counter() - t0
-        m = max(m, int(m * (seconds / 2) / max(probe, 1e-3)))
-        t0 = time.perf_counter()
-        r = ref_chain.run_level(cfg.u, row, cfg.beta, level, base, 1 << 40, m, 99, threads=threads)
-        dt = time.perf_counter() - t0
+        while True:  # grow the sample until one call takes ~seconds / 2
+            t0 = time.perf_counter()
+            r = ref_chain.run_level(cfg.u, row, cfg.beta, level, base, 1 << 40, m, 99, threads=threads)
+            dt = time.perf_counter() - t0
+            if dt >= seconds / 4 or m >= (1 << 34):
+                break
+            m = int(m * min(16.0, max(2.0, (seconds / 2) / max(dt, 1e-3))))
         jumps = r["cost"] - 2 * m * (1 << level)
         out[f"level{level}"] = {"transitions_per_s": jumps / dt, "samples_per_s": m / dt, "samples": m,
                                 "seconds": dt}
