@@ -83,6 +83,13 @@ __device__ __forceinline__ void welford_merge(double& mean, double& m2, uint64_t
 // (SumAcc).  Welford (W = true): the classical-MC accumulator (WelfordAcc, parallel.hpp:80-104):
 // every sample's value is parked in its chunk slot in shared memory and lane 0 folds the chunk
 // in sample order -- the reference's sequential Welford, so mc_* results match it.
+// %lanemask_lt read where it is used (one S2R) instead of a value kept live across the loop.
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
 template <class P, bool W>
 __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
                     if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
                 }
                 cost += ic.nsteps;
-                const uint32_t mine = next + __popc(fin & lt_mask);
+                const uint32_t mine = next + __popc(fin & lanemask_lt());
                 if (mine < cnt) {
                     P::start(w, ic, a.init, a.rows, lo + mine);
                     if constexpr (W) my = mine;
