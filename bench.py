@@ -373,6 +373,7 @@ def main():
     agg = (lambda x: x) if sample_shard else sum_over_ranks
     jumps = agg(ctr["jumps"])
     samples = agg(ctr["samples"])
+    fine_steps = agg(ctr["fine_steps"])
     rows_done = agg(len(res))
     conv = agg(int(res["converged"].sum()))
     over = agg(int(res["over_budget"].sum()))
@@ -463,6 +464,8 @@ def main():
                                        if sample_shard else
                                        f"rows sharded over {world} rank(s), no data-path collective")},
             "rows_per_s": rows_done / (ms * 1e-3), "samples_per_s": samples / (ms * 1e-3),
+            "path_steps_per_s": fine_steps / (ms * 1e-3),
+            "cost_units_per_s": agg(int(res["total_cost"].sum())) / (ms * 1e-3),
             "converged_rows": int(conv), "rows": int(rows_done), "sampler": sampler,
             "over_budget_rows": int(over), "max_cost": max_cost, "max_projected_cost_over_budget": proj_over,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
