@@ -349,7 +349,7 @@ void sample_items(expmc_ctx* c, size_t nitems, uint32_t lane, bool welford) {
         // EXPMC_WINDOW_CHUNKS (tests): a small window exercises the multi-launch path
         const char* wenv = std::getenv("EXPMC_WINDOW_CHUNKS");
         const uint64_t wreq = wenv ? std::strtoull(wenv, nullptr, 10) : 0;
-        c->cap_partials = wreq > 0 && wreq < kWindowChunks ? wreq : kWindowChunks;
+        c->cap_partials = wreq > 0 && wreq <= (kWindowChunks << 4) ? wreq : kWindowChunks;
         dev_alloc(&c->d_pf, 3 * c->cap_partials);
         dev_alloc(&c->d_pu, 2 * c->cap_partials);
         dev_alloc(&c->d_counter, 1);
