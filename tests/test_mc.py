@@ -133,3 +133,22 @@ def test_gpu_mc_matches_oracle_on_c1_rows(gpu, oracle_lib):
                                                                           exp["wall_cost"], exp["jumps"])
             assert got.estimate == pytest.approx(exp["estimate"], rel=1e-13)
             assert got.std_error == pytest.approx(exp["std_error"], rel=1e-9, abs=1e-15)
+
+
+@pytest.mark.gpu
+def test_gpu_mc_event_sampler_statistical(gpu, golden_mc):
+    """Classical MC on the event-driven sampler (same law, different draws): its estimates agree
+    with the reference-order sampler's within combined standard errors; costs follow the same
+    cost model (jumps + non-absorbing step ends + steps)."""
+    import paper_1904_12754_b200 as P
+
+    m = golden_mc["matrices"]["smallw100"]
+    beta = float.fromhex(m["beta"])
+    res = {}
+    for sampler in ("reference", "event"):
+        c = csr(m)
+        with P.Context(P.SparseMatrix(c.n, c.row_ptr, c.col, c.val), unhex(m["u"]), sampler=sampler) as ctx:
+            res[sampler] = [P.mc_single_entry(ctx, e, beta, beta / 8, 200000, 21 + e) for e in (0, 50, 99)]
+    for a, b in zip(res["reference"], res["event"]):
+        assert abs(a.estimate - b.estimate) < 4 * math.sqrt(a.std_error ** 2 + b.std_error ** 2)
+        assert a.steps == b.steps == 8
