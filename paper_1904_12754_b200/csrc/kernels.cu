@@ -25,10 +25,6 @@ namespace expmc_b200 {
 
 namespace {
 
-#ifndef EXPMC_MERGED_RESTART
-#define EXPMC_MERGED_RESTART 1
-#endif
-
 #ifndef EXPMC_SAMPLER_MINB
 #define EXPMC_SAMPLER_MINB 4  // resident 256-thread blocks per SM the sampler is register-budgeted for
 #endif
@@ -94,7 +90,6 @@ template <class P, bool W>
 __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned full = 0xFFFFFFFFu;
-    const unsigned lt_mask = (1u << lane) - 1u;
     __shared__ double s_x[W ? kWarps * kChunk : 1];
     double* const wx = s_x + (W ? (threadIdx.x >> 5) * kChunk : 0);
     __shared__ LogEntry s_log[128];
@@ -137,7 +132,6 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
         typename P::W w;
         bool active = false;
         uint32_t my = 0;  // Welford: the running sample's slot in the chunk
-#if EXPMC_MERGED_RESTART
         // Lanes start samples lo + lane; a lane whose sample ends takes the next unstarted
         // index in the same divergent section as its finish (one ballot per trip).
         if (lane < cnt) {
@@ -170,35 +164,6 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
             }
             next += __popc(fin);
         }
-#else
-        uint32_t next = 0;
-        for (;;) {
-            const unsigned need = __ballot_sync(full, !active);
-            if (!active) {
-                const uint32_t mine = next + __popc(need & lt_mask);
-                if (mine < cnt) {
-                    P::start(w, ic, a.init, a.rows, lo + mine);
-                    active = true;
-                    if constexpr (W) my = mine;
-                }
-            }
-            next += __popc(need);
-            if (!__any_sync(full, active)) break;
-            if (active && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps)) {
-                double ex;
-                const double x = P::sample(w, ic, a.init, a.rows, ex);
-                if constexpr (W) {
-                    wx[my] = x;
-                } else {
-                    sum = __dadd_rn(sum, x);
-                    sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
-                    if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
-                }
-                cost += ic.nsteps;
-                active = false;
-            }
-        }
-#endif
         if constexpr (W) {  // WelfordAcc::add over the chunk in sample order (parallel.hpp:86-92)
             __syncwarp();
             if (lane == 0) {
