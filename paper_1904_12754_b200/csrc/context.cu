@@ -22,6 +22,25 @@
 
 using namespace expmc_b200;
 
+// One batch's staging: pinned host arrays and their device twins (grown on demand), the request
+// -> item map of the batch in flight, and its events.
+struct Staging {
+    DevItem* d_items = nullptr;
+    uint64_t* d_chunk0 = nullptr;
+    Partial* d_totals = nullptr;
+    size_t cap_items = 0;
+    DevItem* h_items = nullptr;  // pinned
+    uint64_t* h_chunk0 = nullptr;
+    Partial* h_totals = nullptr;
+    size_t cap_h = 0;
+    std::vector<int64_t> slot;        // request index of each item (count > 0)
+    size_t nitems = 0;
+    bool inflight = false;
+    std::vector<cudaEvent_t> ev;      // sampler launch brackets (timing)
+    size_t nev = 0;
+    cudaEvent_t done = nullptr;       // totals are on the host
+};
+
 struct expmc_ctx {
     int device = 0;
     int num_sms = 0;
@@ -39,15 +58,9 @@ struct expmc_ctx {
     uint32_t* tgt = nullptr;   // per edge: target | sign bit
     EdgeTables edges() const { return EdgeTables{cdf, tgt}; }
 
-    // batch buffers (grown on demand)
-    DevItem* d_items = nullptr;
-    uint64_t* d_chunk0 = nullptr;
-    Partial* d_totals = nullptr;
-    size_t cap_items = 0;
-    DevItem* h_items = nullptr;  // pinned
-    uint64_t* h_chunk0 = nullptr;
-    Partial* h_totals = nullptr;
-    size_t cap_h = 0;
+    // batch staging, two slots so that one batch can be prepared / consumed on the host while
+    // the other samples (expmc_b200::batch_launch / batch_finish; the driver's row cohorts)
+    Staging stage[2];
     double* d_pf = nullptr;          // chunk partials window: sum | sum_sq | extra
     unsigned long long* d_pu = nullptr;  //                    cost | jumps
     uint64_t cap_partials = 0;
@@ -68,7 +81,6 @@ struct expmc_ctx {
     SampleOut* d_dbg = nullptr;
     size_t cap_dbg = 0;
 
-    std::vector<cudaEvent_t> ev;
     expmc_counters ctr{};
 };
 
@@ -148,20 +160,20 @@ void host_alloc(T** p, size_t count, size_t old_count) {
     *p = static_cast<T*>(pinned_get(std::max<size_t>(count, 1) * sizeof(T)));
 }
 
-void ensure_items(expmc_ctx* c, size_t nitems) {
-    if (nitems + 1 > c->cap_items) {
-        const size_t cap = std::max<size_t>(nitems + 1, c->cap_items * 2);
-        dev_alloc(&c->d_items, cap);
-        dev_alloc(&c->d_chunk0, cap);
-        dev_alloc(&c->d_totals, cap);
-        c->cap_items = cap;
+void ensure_items(Staging& S, size_t nitems) {
+    if (nitems + 1 > S.cap_items) {
+        const size_t cap = std::max<size_t>(nitems + 1, S.cap_items * 2);
+        dev_alloc(&S.d_items, cap);
+        dev_alloc(&S.d_chunk0, cap);
+        dev_alloc(&S.d_totals, cap);
+        S.cap_items = cap;
     }
-    if (nitems + 1 > c->cap_h) {
-        const size_t cap = std::max<size_t>(nitems + 1, c->cap_h * 2);
-        host_alloc(&c->h_items, cap, c->cap_h);
-        host_alloc(&c->h_chunk0, cap, c->cap_h);
-        host_alloc(&c->h_totals, cap, c->cap_h);
-        c->cap_h = cap;
+    if (nitems + 1 > S.cap_h) {
+        const size_t cap = std::max<size_t>(nitems + 1, S.cap_h * 2);
+        host_alloc(&S.h_items, cap, S.cap_h);
+        host_alloc(&S.h_chunk0, cap, S.cap_h);
+        host_alloc(&S.h_totals, cap, S.cap_h);
+        S.cap_h = cap;
     }
 }
 
@@ -327,24 +339,25 @@ void set_error(const std::string& m) { g_err = m; }
 
 bool ctx_has_load(const expmc_ctx* c) { return c->d_load != nullptr; }
 
-// The device pass over prepared items (c->h_items, c->h_chunk0 = per-item chunk counts):
+// The device pass over prepared items (S.h_items, S.h_chunk0 = per-item chunk counts):
 // upload, sampler windows of up to kWindowChunks chunks (+ the NCCL exchange when sample-
-// sharded), ordered combine, totals back to c->h_totals.  welford: the classical-MC reduction.
-void sample_items(expmc_ctx* c, size_t nitems, uint32_t lane, bool welford) {
+// sharded), ordered combine, totals back to S.h_totals -- all queued on the context's stream;
+// sample_wait collects them.  welford: the classical-MC reduction.
+void sample_launch(expmc_ctx* c, Staging& S, size_t nitems, uint32_t lane, bool welford) {
     uint64_t total = 0;
     for (size_t k = 0; k < nitems; ++k) {  // exclusive prefix of the chunk counts
-        const uint64_t n = c->h_chunk0[k];
-        c->h_chunk0[k] = total;
+        const uint64_t n = S.h_chunk0[k];
+        S.h_chunk0[k] = total;
         total += n;
     }
-    c->h_chunk0[nitems] = total;
-    cuda_check(cudaMemcpyAsync(c->d_items, c->h_items, nitems * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
+    S.h_chunk0[nitems] = total;
+    cuda_check(cudaMemcpyAsync(S.d_items, S.h_items, nitems * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
                "H2D items");
-    cuda_check(cudaMemcpyAsync(c->d_chunk0, c->h_chunk0, (nitems + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+    cuda_check(cudaMemcpyAsync(S.d_chunk0, S.h_chunk0, (nitems + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
                                c->stream),
                "H2D chunk0");
     c->ctr.h2d_bytes += nitems * sizeof(DevItem) + (nitems + 1) * sizeof(uint64_t);
-    cuda_check(cudaMemsetAsync(c->d_totals, 0, nitems * sizeof(Partial), c->stream), "memset totals");
+    cuda_check(cudaMemsetAsync(S.d_totals, 0, nitems * sizeof(Partial), c->stream), "memset totals");
     if (!c->d_pf) {
         // EXPMC_WINDOW_CHUNKS (tests): a small window exercises the multi-launch path
         const char* wenv = std::getenv("EXPMC_WINDOW_CHUNKS");
@@ -375,8 +388,8 @@ void sample_items(expmc_ctx* c, size_t nitems, uint32_t lane, bool welford) {
         SamplerArgs a;
         a.rows = c->rows;
         a.edges = c->edges();
-        a.items = c->d_items;
-        a.chunk0 = c->d_chunk0;
+        a.items = S.d_items;
+        a.chunk0 = S.d_chunk0;
         a.nitems = static_cast<uint32_t>(nitems);
         a.g_begin = g0;
         a.g_end = g1;
@@ -388,36 +401,47 @@ void sample_items(expmc_ctx* c, size_t nitems, uint32_t lane, bool welford) {
         const uint64_t own = (w + world - 1) / world;
         const uint64_t want_blocks = (own + warps_per_block - 1) / warps_per_block;
         const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(sampler_grid, want_blocks)));
-        while (c->ev.size() < 2 * (nev + 1)) {
+        while (S.ev.size() < 2 * (nev + 1)) {
             cudaEvent_t e;
             cuda_check(cudaEventCreate(&e), "cudaEventCreate");
-            c->ev.push_back(e);
+            S.ev.push_back(e);
         }
-        cuda_check(cudaEventRecord(c->ev[2 * nev], c->stream), "event");
+        cuda_check(cudaEventRecord(S.ev[2 * nev], c->stream), "event");
         if (welford) launch_sampler_welford(a, grid, c->sampler, lane, c->stream);
         else launch_sampler(a, grid, c->sampler, lane, c->stream);
-        cuda_check(cudaEventRecord(c->ev[2 * nev + 1], c->stream), "event");
+        cuda_check(cudaEventRecord(S.ev[2 * nev + 1], c->stream), "event");
         ++nev;
         if (c->nccl) {  // exact cross-GPU sum of the window's chunk partials (one rank non-zero per chunk)
             nccl_allreduce_partials(c->nccl, cp, w, c->cap_partials, c->stream);
             c->ctr.nccl_bytes += w * (3 * sizeof(double) + 2 * sizeof(uint64_t));
         }
         if (welford)
-            launch_combine_welford(c->d_chunk0, c->d_items, static_cast<uint32_t>(nitems), g0, g1, cp, c->d_totals,
+            launch_combine_welford(S.d_chunk0, S.d_items, static_cast<uint32_t>(nitems), g0, g1, cp, S.d_totals,
                                    c->stream);
         else
-            launch_combine(c->d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, fem, c->d_totals, c->stream);
+            launch_combine(S.d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, fem, S.d_totals, c->stream);
         c->ctr.kernel_launches += 2;
         c->ctr.sampler_launches += 1;
         c->last_window = w;
     }
-    cuda_check(cudaMemcpyAsync(c->h_totals, c->d_totals, nitems * sizeof(Partial), cudaMemcpyDeviceToHost, c->stream),
+    cuda_check(cudaMemcpyAsync(S.h_totals, S.d_totals, nitems * sizeof(Partial), cudaMemcpyDeviceToHost, c->stream),
                "D2H totals");
     c->ctr.d2h_bytes += nitems * sizeof(Partial);
-    cuda_check(cudaStreamSynchronize(c->stream), "sampler");
-    for (size_t k = 0; k < nev; ++k) {
+    if (!S.done) cuda_check(cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventRecord(S.done, c->stream), "event");
+    S.nev = nev;
+    S.nitems = nitems;
+    S.inflight = true;
+}
+
+// Wait for a launched batch's totals and account its sampler time.
+void sample_wait(expmc_ctx* c, Staging& S) {
+    if (!S.inflight) return;
+    S.inflight = false;
+    cuda_check(cudaEventSynchronize(S.done), "sampler");
+    for (size_t k = 0; k < S.nev; ++k) {
         float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, c->ev[2 * k], c->ev[2 * k + 1]), "event time");
+        cuda_check(cudaEventElapsedTime(&ms, S.ev[2 * k], S.ev[2 * k + 1]), "event time");
         c->ctr.sampler_ms += ms;
     }
 }
@@ -447,7 +471,9 @@ void mc_batch(expmc_ctx* c, uint32_t lane, const expmc_mc_req* req, int64_t nreq
     if (lane == EXPMC_LANE_FORWARD) ensure_forward_init(c);
     need(static_cast<uint64_t>(nreq) < (uint64_t{1} << 31), EXPMC_EINVAL, "too many MC requests in one batch");
     const size_t nitems = static_cast<size_t>(nreq);
-    ensure_items(c, nitems);
+    Staging& S = c->stage[0];
+    sample_wait(c, S);
+    ensure_items(S, nitems);
     for (size_t k = 0; k < nitems; ++k) {
         const expmc_mc_req& r = req[k];
         DevItem it{};
@@ -462,13 +488,14 @@ void mc_batch(expmc_ctx* c, uint32_t lane, const expmc_mc_req* req, int64_t nreq
         it.key3 = (key & 0xFFFFFFu) | (lane << 24);
         it.base = 1u;
         it.mode = lane;
-        c->h_items[k] = it;
-        c->h_chunk0[k] = (r.samples - 1) / kChunk + 1;
+        S.h_items[k] = it;
+        S.h_chunk0[k] = (r.samples - 1) / kChunk + 1;
     }
     c->ctr.rounds += 1;
-    sample_items(c, nitems, lane, true);
+    sample_launch(c, S, nitems, lane, true);
+    sample_wait(c, S);
     for (size_t k = 0; k < nitems; ++k) {  // finish (mc.cpp:29-38)
-        const Partial& t = c->h_totals[k];
+        const Partial& t = S.h_totals[k];
         const uint64_t n = static_cast<uint64_t>(t.extra);
         expmc_mc_result& o = out[k];
         o.samples = n;
@@ -485,9 +512,15 @@ void mc_batch(expmc_ctx* c, uint32_t lane, const expmc_mc_req* req, int64_t nreq
     }
 }
 
-void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
-                     expmc_level_stats* out) {
+// Validate a batch, stage its items in slot `s` and queue the device pass; out[] gets zeros for
+// every request now and its totals from batch_finish.  The slot's previous batch, if any, must
+// have been finished.
+void batch_launch(expmc_ctx* c, int s, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
+                  expmc_level_stats* out) {
     bind(c);
+    Staging& S = c->stage[s];
+    need(!S.inflight, EXPMC_EINTERNAL, "staging slot busy");
+    S.nitems = 0;
     // validate (first failing request wins, as a sequential loop would report it)
     int64_t bad = nreq;
 #pragma omp parallel for schedule(static) reduction(min : bad)
@@ -500,37 +533,46 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
         }
     }
     if (bad < nreq) validate_req(c, req[bad], beta, lane);  // rethrows with the right code
-    std::vector<int64_t> slot;  // request index of each item (count > 0)
-    slot.reserve(static_cast<size_t>(nreq));
+    S.slot.clear();
+    S.slot.reserve(static_cast<size_t>(nreq));
     for (int64_t i = 0; i < nreq; ++i)
-        if (req[i].count > 0) slot.push_back(i);
-    const size_t nitems = slot.size();
+        if (req[i].count > 0) S.slot.push_back(i);
+    const size_t nitems = S.slot.size();
     if (nitems == 0) return;
     const bool forward = lane == EXPMC_LANE_FORWARD;
     if (forward) ensure_forward_init(c);  // run_level builds it before sampling (mlmc.cpp)
     c->ctr.rounds += 1;
     need(nitems < (size_t{1} << 31), EXPMC_EINVAL, "too many run_level requests in one batch");
-    ensure_items(c, nitems);
+    ensure_items(S, nitems);
 #pragma omp parallel for schedule(static)
     for (size_t k = 0; k < nitems; ++k) {
-        const expmc_level_req& r = req[slot[k]];
-        c->h_items[k] = make_item(r, beta, lane);
+        const expmc_level_req& r = req[S.slot[k]];
+        S.h_items[k] = make_item(r, beta, lane);
         const uint64_t first_chunk = r.first_index / kChunk;
         const uint64_t last_chunk = (r.first_index + r.count - 1) / kChunk;  // parallel.hpp:36-38
-        c->h_chunk0[k] = last_chunk - first_chunk + 1;
+        S.h_chunk0[k] = last_chunk - first_chunk + 1;
     }
-    sample_items(c, nitems, lane, false);
+    sample_launch(c, S, nitems, lane, false);
+}
+
+// Wait for slot `s`'s batch and write its per-request totals (the same req / out as the launch).
+void batch_finish(expmc_ctx* c, int s, const expmc_level_req* req, expmc_level_stats* out) {
+    Staging& S = c->stage[s];
+    if (!S.inflight) return;  // nothing was queued (all counts 0)
+    bind(c);
+    sample_wait(c, S);
+    const size_t nitems = S.nitems;
     uint64_t samples = 0, jumps = 0, steps = 0;
 #pragma omp parallel for schedule(static) reduction(+ : samples, jumps, steps)
     for (size_t k = 0; k < nitems; ++k) {
-        const expmc_level_req& r = req[slot[k]];
-        expmc_level_stats& o = out[slot[k]];
-        o.sum = c->h_totals[k].sum;
-        o.sum_sq = c->h_totals[k].sum_sq;
+        const expmc_level_req& r = req[S.slot[k]];
+        expmc_level_stats& o = out[S.slot[k]];
+        o.sum = S.h_totals[k].sum;
+        o.sum_sq = S.h_totals[k].sum_sq;
         o.samples = sampled_count(r.first_index, r.count);
-        o.cost = c->h_totals[k].cost;
-        o.jumps = c->h_totals[k].jumps;
-        o.integ_sum = c->h_totals[k].extra;
+        o.cost = S.h_totals[k].cost;
+        o.jumps = S.h_totals[k].jumps;
+        o.integ_sum = S.h_totals[k].extra;
         samples += o.samples;
         jumps += o.jumps;
         steps += o.samples << r.level;
@@ -538,6 +580,20 @@ void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level
     c->ctr.samples += samples;
     c->ctr.jumps += jumps;
     c->ctr.fine_steps += steps;
+}
+
+// Drain every staging slot (error paths of pipelined callers).
+void batch_drain(expmc_ctx* c) {
+    bind(c);
+    cudaStreamSynchronize(c->stream);
+    for (Staging& S : c->stage) S.inflight = false;
+}
+
+void run_level_batch(expmc_ctx* c, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
+                     expmc_level_stats* out) {
+    sample_wait(c, c->stage[0]);  // a previous pipelined caller may have left slot 0 queued
+    batch_launch(c, 0, beta, lane, req, nreq, out);
+    batch_finish(c, 0, req, out);
 }
 
 // Per-sample records of any lane (one debug launch): the shared body of expmc_sample_debug[_ex].
@@ -555,14 +611,16 @@ std::vector<SampleOut> sample_debug(expmc_ctx* c, double beta, uint32_t lane, in
         items[i] = make_item(r, beta, lane);
     }
     if (lane == EXPMC_LANE_FORWARD) ensure_forward_init(c);
-    ensure_items(c, static_cast<size_t>(nreq));
+    Staging& S = c->stage[0];
+    sample_wait(c, S);
+    ensure_items(S, static_cast<size_t>(nreq));
     if (static_cast<size_t>(nreq) > c->cap_dbg) {
         dev_alloc(&c->d_dbg, nreq);
         c->cap_dbg = nreq;
     }
-    cuda_check(cudaMemcpyAsync(c->d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
+    cuda_check(cudaMemcpyAsync(S.d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
                "H2D");
-    launch_debug(c->rows, c->edges(), c->d_items, static_cast<uint32_t>(nreq), lane_data(c), c->d_dbg, c->sampler,
+    launch_debug(c->rows, c->edges(), S.d_items, static_cast<uint32_t>(nreq), lane_data(c), c->d_dbg, c->sampler,
                  lane, c->stream);
     c->ctr.kernel_launches += 1;
     cuda_check(cudaMemcpyAsync(o.data(), c->d_dbg, nreq * sizeof(SampleOut), cudaMemcpyDeviceToHost, c->stream),
@@ -691,9 +749,18 @@ void expmc_ctx_destroy(expmc_ctx* c) {
     cudaFree(c->rows);
     cudaFree(c->cdf);
     cudaFree(c->tgt);
-    cudaFree(c->d_items);
-    cudaFree(c->d_chunk0);
-    cudaFree(c->d_totals);
+    for (Staging& S : c->stage) {
+        cudaFree(S.d_items);
+        cudaFree(S.d_chunk0);
+        cudaFree(S.d_totals);
+        if (S.cap_h) {  // staging blocks go back to the process-wide pool
+            pinned_put(S.h_items, S.cap_h * sizeof(DevItem));
+            pinned_put(S.h_chunk0, S.cap_h * sizeof(uint64_t));
+            pinned_put(S.h_totals, S.cap_h * sizeof(Partial));
+        }
+        for (cudaEvent_t e : S.ev) cudaEventDestroy(e);
+        if (S.done) cudaEventDestroy(S.done);
+    }
     cudaFree(c->d_pf);
     cudaFree(c->d_pu);
     if (c->nccl) nccl().comm_destroy(c->nccl);
@@ -702,12 +769,6 @@ void expmc_ctx_destroy(expmc_ctx* c) {
     cudaFree(c->d_init_guide);
     cudaFree(c->d_load);
     cudaFree(c->d_dbg);
-    if (c->cap_h) {  // staging blocks go back to the process-wide pool
-        pinned_put(c->h_items, c->cap_h * sizeof(DevItem));
-        pinned_put(c->h_chunk0, c->cap_h * sizeof(uint64_t));
-        pinned_put(c->h_totals, c->cap_h * sizeof(Partial));
-    }
-    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

@@ -217,41 +217,62 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
         for (int i = 0; i <= s.top - l0; ++i) s.pending.emplace_back(i, opt.warmup);
     }
 
-    // Per round: (1) every active row's pending extensions become one contiguous slice of the
+    // Per round: (1) every active row's pending extensions become one contiguous slice of a
     // batch, (2) one batched GPU pass, (3) each row applies its slice (extend(), mlmc.cpp:188-199)
-    // and advances its state machine.  Rows are independent, so (1) and (3) run in parallel.
-    // request / result arrays: grown without value-initialisation, first touched by the parallel
-    // fill (round 0 stages ~5 requests per row: hundreds of MB at n = 2^20)
-    RawArray<expmc_level_req> req;
-    RawArray<expmc_level_stats> res;
-    std::vector<size_t> off;
-    std::vector<unsigned char> keep;
-    std::vector<int64_t> active(static_cast<size_t>(nrows));
-    for (int64_t r = 0; r < nrows; ++r) active[static_cast<size_t>(r)] = r;
+    // and advances its state machine.  Rows are independent, so (1) and (3) run in parallel --
+    // and large jobs split the rows into two cohorts whose rounds alternate on the GPU: while
+    // one cohort's batch samples, the host consumes the other's results and stages its next
+    // batch (two staging slots in the context), so the host work hides behind the kernels.
+    // Every row still sees exactly its own sequence of requests and results.
+    struct Cohort {
+        std::vector<int64_t> active;
+        // request / result arrays: grown without value-initialisation, first touched by the
+        // parallel fill (round 0 stages ~5 requests per row: hundreds of MB at n = 2^20)
+        RawArray<expmc_level_req> req;
+        RawArray<expmc_level_stats> res;
+        std::vector<size_t> off;
+        std::vector<unsigned char> keep;
+        bool inflight = false;
+        int round = 0;
+        double build_ms = 0.0;
+    };
+    const int ncoh = nrows >= 4096 ? 2 : 1;
+    Cohort coh[2];
+    for (int64_t r = 0; r < nrows; ++r) coh[r % ncoh].active.push_back(r);
     const bool trace = std::getenv("EXPMC_TRACE") != nullptr;  // per-round timeline on stderr
     using clk = std::chrono::steady_clock;
-    int round = 0;
-    while (!active.empty()) {
+    auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+
+    auto launch = [&](Cohort& co, int slot) {
+        if (co.active.empty()) return;
         const auto t0 = clk::now();
-        const size_t na = active.size();
-        off.assign(na + 1, 0);
-        for (size_t i = 0; i < na; ++i) off[i + 1] = off[i] + st[static_cast<size_t>(active[i])].pending.size();
-        req.resize(off[na]);
-        res.resize(off[na]);  // run_level_batch writes every element
+        const size_t na = co.active.size();
+        co.off.assign(na + 1, 0);
+        for (size_t i = 0; i < na; ++i) co.off[i + 1] = co.off[i] + st[static_cast<size_t>(co.active[i])].pending.size();
+        co.req.resize(co.off[na]);
+        co.res.resize(co.off[na]);  // batch_launch writes every element
 #pragma omp parallel for schedule(static)
         for (size_t i = 0; i < na; ++i) {
-            const RowState& s = st[static_cast<size_t>(active[i])];
-            size_t k = off[i];
+            const RowState& s = st[static_cast<size_t>(co.active[i])];
+            size_t k = co.off[i];
             for (const auto& p : s.pending) {
                 const Level& l = s.lv[static_cast<size_t>(p.first)];
                 const int level = s.l0 + p.first;
-                req[k++] = expmc_level_req{s.entry, s.seed, l.samples, p.second, level, level == s.l0 ? 1 : 0};
+                co.req[k++] = expmc_level_req{s.entry, s.seed, l.samples, p.second, level, level == s.l0 ? 1 : 0};
             }
         }
+        batch_launch(ctx, slot, beta, lane, co.req.data(), static_cast<int64_t>(co.req.size()), co.res.data());
+        co.inflight = true;
+        co.build_ms = ms(t0, clk::now());
+    };
+
+    auto consume = [&](Cohort& co, int slot) {
+        const auto t0 = clk::now();
+        batch_finish(ctx, slot, co.req.data(), co.res.data());
+        co.inflight = false;
         const auto t1 = clk::now();
-        run_level_batch(ctx, beta, lane, req.data(), static_cast<int64_t>(req.size()), res.data());
-        const auto t2 = clk::now();
-        keep.assign(na, 0);
+        const size_t na = co.active.size();
+        co.keep.assign(na, 0);
         int err_code = 0;
         std::string err_msg;
 #pragma omp parallel
@@ -260,9 +281,9 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
             std::vector<uint64_t> want;
 #pragma omp for schedule(dynamic, 256)
             for (size_t i = 0; i < na; ++i) {
-                RowState& s = st[static_cast<size_t>(active[i])];
+                RowState& s = st[static_cast<size_t>(co.active[i])];
                 for (size_t j = 0; j < s.pending.size(); ++j) {  // extend(): mlmc.cpp:188-199
-                    const expmc_level_stats& d = res[off[i] + j];
+                    const expmc_level_stats& d = co.res[co.off[i] + j];
                     Level& l = s.lv[static_cast<size_t>(s.pending[j].first)];
                     l.sum += d.sum;
                     l.sum_sq += d.sum_sq;
@@ -282,24 +303,40 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
                     }
                     s.phase = Phase::done;
                 }
-                keep[i] = s.phase != Phase::done;
+                co.keep[i] = s.phase != Phase::done;
             }
         }
         if (err_code) throw Status(err_code, err_msg);
         size_t m = 0;
         for (size_t i = 0; i < na; ++i)
-            if (keep[i]) active[m++] = active[i];
+            if (co.keep[i]) co.active[m++] = co.active[i];
         if (trace) {
             uint64_t smp = 0;
-            for (size_t q = 0; q < req.size(); ++q) smp += req[q].count;
-            const auto t3 = clk::now();
-            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-            std::fprintf(stderr, "[expmc] round %d rows %zu reqs %zu samples %llu | build %.2f ms gpu %.2f ms advance %.2f ms\n",
-                         round, na, req.size(), static_cast<unsigned long long>(smp), ms(t0, t1), ms(t1, t2),
-                         ms(t2, t3));
+            for (size_t q = 0; q < co.req.size(); ++q) smp += co.req[q].count;
+            std::fprintf(stderr, "[expmc] cohort %d round %d rows %zu reqs %zu samples %llu | build %.2f ms wait %.2f ms "
+                         "advance %.2f ms\n",
+                         slot, co.round, na, co.req.size(), static_cast<unsigned long long>(smp), co.build_ms,
+                         ms(t0, t1), ms(t1, clk::now()));
         }
-        ++round;
-        active.resize(m);
+        ++co.round;
+        co.active.resize(m);
+    };
+
+    try {
+        for (int k = 0; k < ncoh; ++k) launch(coh[k], k);
+        for (;;) {
+            bool any = false;
+            for (int k = 0; k < ncoh; ++k) {
+                if (!coh[k].inflight) continue;
+                any = true;
+                consume(coh[k], k);
+                launch(coh[k], k);  // queued behind the other cohort's batch
+            }
+            if (!any) break;
+        }
+    } catch (...) {
+        batch_drain(ctx);  // no batch may outlive its staging arrays
+        throw;
     }
 
 #pragma omp parallel for schedule(static)

@@ -173,6 +173,12 @@ void run_level_batch(expmc_ctx* ctx, double beta, uint32_t lane, const expmc_lev
                      int64_t nreq, expmc_level_stats* out);
 void set_error(const std::string& m);
 bool ctx_has_load(const expmc_ctx* c);
+// Pipelined batches (two staging slots, s = 0 or 1): launch queues the device pass and returns;
+// finish waits for it and writes the totals; drain synchronises after an error.
+void batch_launch(expmc_ctx* c, int s, double beta, uint32_t lane, const expmc_level_req* req, int64_t nreq,
+                  expmc_level_stats* out);
+void batch_finish(expmc_ctx* c, int s, const expmc_level_req* req, expmc_level_stats* out);
+void batch_drain(expmc_ctx* c);
 // Classical MC batch (csrc/mc.cpp front end): validated requests, Welford reduction.
 void mc_batch(expmc_ctx* c, uint32_t lane, const expmc_mc_req* req, int64_t nreq, expmc_mc_result* out);
 }  // namespace expmc_b200
