@@ -206,7 +206,7 @@ def sampler_only_rate(ref_chain, cfg, threads, seconds=4.0):
 
 def load_issue_active():
     """Issue-slot utilisation of k_sample from the committed ncu capture (the kernel's real bound)."""
-    path = os.path.join(ROOT, "profiles", "r01", "k_sample_r1c_key_metrics.json")
+    path = os.path.join(ROOT, "profiles", "r01", "k_sample_r1g_key_metrics.json")
     try:
         with open(path) as f:
             return float(json.load(f)["smsp__issue_active.avg.pct_of_peak_sustained_active"]["value"])
@@ -479,7 +479,7 @@ def main():
                          "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
                          "issue_active_pct": load_issue_active(),
                          "binding_resource": "instruction issue (ncu smsp__issue_active, "
-                                             "profiles/r01/k_sample_r1c_key_metrics.json)",
+                                             "profiles/r01/k_sample_r1g_key_metrics.json)",
                          "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches), "clocks": clk,
         }
