@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--max-cost", type=float, default=None,
                    help="per-component model-unit budget (driver extension; default off for C1/C2, 1e10 for C3-C5)")
     p.add_argument("--sampler", default=None, choices=["reference", "event"], help="override the config's sampler")
+    p.add_argument("--full-hold", action="store_true",
+                   help="event sampler: evaluate first holding intervals in full (A/B of the closed-form hold)")
     p.add_argument("--multi", default="rows", choices=["rows", "samples"],
                    help="N>1: shard components over ranks (no collective) or shard every component's "
                         "samples with an exact NCCL all-reduce of the chunk partials")
@@ -327,6 +329,8 @@ def main():
     opts = P.MlmcOptions(epsilon=cfg.epsilon, max_levels_above_l0=cfg.max_levels_above_l0, max_cost=max_cost)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ctx = P.Context(cfg.a, cfg.u, device=local, sampler=sampler)
+    if args.full_hold:
+        ctx.set_full_hold(True)
     sample_shard = args.multi == "samples" and world > 1
     if sample_shard:  # every rank runs the same components; chunk g is sampled on rank g % world
         obj = [P.nccl_unique_id() if rank == 0 else None]
@@ -415,6 +419,8 @@ def main():
         e0.record()
         for s in range(e2e_steps):
             with P.Context(cfg.a, cfg.u, device=local, sampler=sampler) as c2:
+                if args.full_hold:
+                    c2.set_full_hold(True)
                 if sample_shard:
                     c2.shard_samples(ids[s], rank, world)
                 rows = batches[args.warmup + s]

@@ -40,6 +40,10 @@ extern "C" {
  * at O(jumps) instead of O(2^level) events per path; statistical parity. */
 #define EXPMC_SAMPLER_REFERENCE 0
 #define EXPMC_SAMPLER_EVENT 1
+/* Sampler flags (expmc_ctx_set_sampler_flags).  FULL_HOLD: the event-driven sampler evaluates
+ * every sample's first holding interval in full instead of deciding "never leaves the entry"
+ * from the first draw against a per-item threshold (same outcomes; A/B testing only). */
+#define EXPMC_SAMPLER_FLAG_FULL_HOLD 1u
 
 /* Sampling lanes of the reference's Philox key (mlmc.cpp:94-96).  ENTRY estimates
  * (e^{tA}u)_entry; FORWARD estimates sum_i (e^{tA}u)_i from paths started at a state drawn
@@ -185,6 +189,7 @@ int expmc_ctx_get_counters(const expmc_ctx* ctx, expmc_counters* out);
 /* Select the path sampler (EXPMC_SAMPLER_REFERENCE / EXPMC_SAMPLER_EVENT) for all later calls. */
 int expmc_ctx_set_sampler(expmc_ctx* ctx, int32_t mode);
 int expmc_ctx_get_sampler(const expmc_ctx* ctx, int32_t* mode);
+int expmc_ctx_set_sampler_flags(expmc_ctx* ctx, uint32_t flags);
 /* The context's CUDA stream (cudaStream_t as void*), for timing with events on the stream
  * the sampler kernels are launched on. */
 int expmc_ctx_get_stream(const expmc_ctx* ctx, void** stream);

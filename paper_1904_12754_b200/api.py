@@ -280,6 +280,11 @@ class Context:
         _check(L.lib.expmc_ctx_set_sampler(self._h, self.SAMPLERS[sampler]))
         self.sampler = sampler
 
+    def set_full_hold(self, full: bool):
+        """Event sampler only: evaluate every first holding interval in full (True) instead of
+        the closed-form stay-at-entry decision (False, the default) -- same outcomes; A/B tests."""
+        _check(L.lib.expmc_ctx_set_sampler_flags(self._h, 1 if full else 0))
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             L.lib.expmc_ctx_destroy(self._h)

@@ -49,6 +49,7 @@ struct expmc_ctx {
     int sampler_grid_ed = 0;
     int sampler_grid_fem = 0;
     int sampler = EXPMC_SAMPLER_REFERENCE;
+    uint32_t sampler_flags = 0;  // EXPMC_SAMPLER_FLAG_*
     cudaStream_t stream = nullptr;
     int64_t n = 0;
     uint64_t nedges = 0;
@@ -397,6 +398,7 @@ void sample_launch(expmc_ctx* c, Staging& S, size_t nitems, uint32_t lane, bool 
         a.counter = c->d_counter;
         a.shard_rank = static_cast<uint32_t>(c->shard_rank);
         a.shard_world = world;
+        a.flags = c->sampler_flags;
         a.init = lane_data(c);
         const uint64_t own = (w + world - 1) / world;
         const uint64_t want_blocks = (own + warps_per_block - 1) / warps_per_block;
@@ -621,7 +623,7 @@ std::vector<SampleOut> sample_debug(expmc_ctx* c, double beta, uint32_t lane, in
     cuda_check(cudaMemcpyAsync(S.d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
                "H2D");
     launch_debug(c->rows, c->edges(), S.d_items, static_cast<uint32_t>(nreq), lane_data(c), c->d_dbg, c->sampler,
-                 lane, c->stream);
+                 lane, c->sampler_flags, c->stream);
     c->ctr.kernel_launches += 1;
     cuda_check(cudaMemcpyAsync(o.data(), c->d_dbg, nreq * sizeof(SampleOut), cudaMemcpyDeviceToHost, c->stream),
                "D2H");
@@ -846,6 +848,14 @@ int expmc_ctx_set_sampler(expmc_ctx* c, int32_t mode) {
         need(mode == EXPMC_SAMPLER_REFERENCE || mode == EXPMC_SAMPLER_EVENT, EXPMC_EINVAL, "unknown sampler mode");
         c->sampler = mode;
         c->sampler_grid = mode == EXPMC_SAMPLER_EVENT ? c->sampler_grid_ed : c->sampler_grid_ref;
+    });
+}
+
+int expmc_ctx_set_sampler_flags(expmc_ctx* c, uint32_t flags) {
+    return guarded([&] {
+        need(c != nullptr, EXPMC_EINVAL, "null context");
+        need((flags & ~EXPMC_SAMPLER_FLAG_FULL_HOLD) == 0u, EXPMC_EINVAL, "unknown sampler flag");
+        c->sampler_flags = flags;
     });
 }
 

@@ -17,6 +17,17 @@
 // for the path this walker drew -- draws = jumps + #{k in 1..N : rate(s_k) > 0} (each
 // non-absorbing step ends with one rejected draw, paths.cpp:50-53), cost = draws + N -- so the
 // driver's allocation (mlmc.cpp:216) sees the same unit costs in expectation.
+//
+// Closed-form first hold (entry mode): every sample of an item starts in the same row with
+// the same clock, so whether its first holding interval outlasts [0, beta] is decided by the
+// first draw alone: E = -log(1 - u) >= rate * beta, i.e. M = 2^53 - K <= 2^53 e^{-rate beta}.
+// EdPolicy::prepare computes, once per chunk, a threshold m_safe a relative 2^-30 inside that
+// boundary (far outside the ~4 ulp error of the log / divide the full event evaluates) and the
+// values of the stay-at-entry path with the same ed_segment / ed_finish code.  A draw with
+// M < m_safe then ends the sample at once with those values -- the same outcome the full
+// event computes, without its log, divide, segment sums and exp.  On C3/C4 (t = 1/lambda)
+// over 95 % of samples never jump.  Draws near the boundary and every later event take the
+// full path.  EXPMC_SAMPLER_FLAG_FULL_HOLD switches the shortcut off (A/B tests).
 #pragma once
 
 #ifndef EXPMC_SAMPLER_MINB
@@ -27,12 +38,15 @@
 
 namespace expmc_b200 {
 
+constexpr uint32_t kFresh = 2u;
+
 struct EdWalker {
     Stream st;
     Row cur;
     uint32_t state;
     int32_t sign;
-    uint32_t dconst;   // every visited state has the entry's d (=> coupled difference is 0)
+    uint32_t dconst;   // bit 0: every visited state has the entry's d (=> coupled difference is 0)
+                       // bit 1 (kFresh): no event yet (the closed-form first hold applies)
     uint64_t kcur;     // first fine-step boundary not yet assigned a state
     double t;          // start time of the current holding interval
     double acc_a;      // doubled-weight sum of d: expo (single) or coarse (coupled)
@@ -48,7 +62,7 @@ __device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const
     w.cur = load_row(rows, s0);
     w.state = s0;
     w.sign = 1;
-    w.dconst = 1u;
+    w.dconst = 1u | kFresh;
     w.kcur = 0;
     w.t = 0.0;
     w.acc_a = 0.0;
@@ -81,6 +95,14 @@ __device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const
                                          const EdgeTables& edges, const LogEntry* s_log, unsigned long long& draws,
                                          unsigned long long& jumps) {
     stream_reserve2(w.st);
+    if (w.dconst & kFresh) {
+        w.dconst &= ~kFresh;
+        if ((uint64_t{1} << 53) - (w.st.w0 >> 11) < ic.m_safe) {  // holds past beta at the entry
+            draws += ic.nsteps;  // ed_segment(0, N) on a non-absorbing row
+            w.sign = 0;          // marks the closed-form path for ed_sample / record
+            return true;
+        }
+    }
     double tjump = INFINITY;
     if (w.cur.rate != 0.0) {
         const double e = -fast_log(__ull2double_rn((uint64_t{1} << 53) - stream_pop_bits(w.st)), -53, s_log, c_log_poly);
@@ -130,6 +152,7 @@ __device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic
 
 template <bool F>
 __device__ __forceinline__ double ed_sample(const EdWalker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows) {
+    if (w.sign == 0) return ic.hold_x;
     if (!ic.base && w.dconst) return 0.0;
     double fine, coarse;
     ed_finish<F>(w, ic, fi, rows, fine, coarse);
@@ -144,7 +167,7 @@ struct RefPolicy {
     using W = Walker;
     static constexpr bool kExtra = false;
     static constexpr int kMinBlocks = EXPMC_SAMPLER_MINB;
-    static __device__ __forceinline__ void prepare(ItemConst&) {}
+    static __device__ __forceinline__ void prepare(ItemConst&, const RowRec*, const LaneData&, uint32_t) {}
     static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
                                                  uint64_t s) {
         walker_start<F>(w, ic, ld, rows, s);
@@ -172,7 +195,30 @@ struct EdPolicy {
     using W = EdWalker;
     static constexpr bool kExtra = false;
     static constexpr int kMinBlocks = EXPMC_SAMPLER_MINB;
-    static __device__ __forceinline__ void prepare(ItemConst&) {}
+    // The closed-form first hold (header): threshold and stay-at-entry values, once per chunk.
+    static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData& ld,
+                                                   uint32_t flags) {
+        if (F || (flags & EXPMC_SAMPLER_FLAG_FULL_HOLD)) return;
+        const Row r = load_row(rows, ic.entry);
+        if (!(r.rate > 0.0)) return;  // absorbing entry: the full event draws nothing anyway
+        // P(no jump before beta) = e^{-rate beta}; M below 2^53 of that, less 2^-30 relative
+        const double m = __dmul_rn(__dmul_rn(exp(-__dmul_rn(r.rate, ic.tend)), 0x1.0p53), 1.0 - 0x1.0p-30);
+        if (!(m >= 2.0)) return;
+        EdWalker w;
+        w.cur = r;
+        w.state = ic.entry;
+        w.sign = 1;
+        w.dconst = 1u;
+        w.t = 0.0;
+        w.acc_a = 0.0;
+        w.acc_b = 0.0;
+        w.dfirst = r.d;
+        unsigned long long draws = 0;
+        ed_segment(w, ic, 0, ic.nsteps, draws);  // the holding interval covers every boundary
+        ed_finish<false>(w, ic, ld, rows, ic.hold_fine, ic.hold_coarse);
+        ic.hold_x = ic.base ? ic.hold_fine : 0.0;  // ed_sample's coupled constant-d case
+        ic.m_safe = static_cast<uint64_t>(m);
+    }
     static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
                                                  uint64_t s) {
         ed_start<F>(w, ic, ld, rows, s);
@@ -188,8 +234,14 @@ struct EdPolicy {
     }
     static __device__ __forceinline__ void record(const W& w, const ItemConst& ic, const LaneData& ld,
                                                   const RowRec* rows, SampleOut& o) {
-        ed_finish<F>(w, ic, ld, rows, o.fine, o.coarse);
-        o.value = ic.base ? o.fine : __dsub_rn(o.fine, o.coarse);
+        if (w.sign == 0) {
+            o.fine = ic.hold_fine;
+            o.coarse = ic.hold_coarse;
+            o.value = ic.hold_x;
+        } else {
+            ed_finish<F>(w, ic, ld, rows, o.fine, o.coarse);
+            o.value = ic.base ? o.fine : __dsub_rn(o.fine, o.coarse);
+        }
         o.integ_f = o.integ_c = 0.0;
         o.end_state = w.state;
     }

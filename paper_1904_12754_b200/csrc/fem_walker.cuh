@@ -136,7 +136,7 @@ struct FemPolicy {
     using W = FemWalker;
     static constexpr bool kExtra = true;
     static constexpr int kMinBlocks = EXPMC_FEM_MINB;
-    static __device__ __forceinline__ void prepare(ItemConst& ic) {
+    static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec*, const LaneData&, uint32_t) {
         ic.h_fine = __ddiv_rn(ic.dt, 3.0);  // scaled_simpson's h = step / 3 (mlmc.cpp:68)
         ic.h_coarse = __ddiv_rn(__dmul_rn(2.0, ic.dt), 3.0);
     }

@@ -129,6 +129,7 @@ struct SamplerArgs {
     unsigned int* counter;    // dynamic chunk counter, zeroed before launch
     uint32_t shard_rank;      // sample sharding: this launch samples the chunks g with
     uint32_t shard_world;     //   g % shard_world == shard_rank (the others stay zero)
+    uint32_t flags;           // EXPMC_SAMPLER_FLAG_*
 };
 
 void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s);
@@ -138,7 +139,7 @@ void launch_combine_welford(const uint64_t* chunk0, const DevItem* items, uint32
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
                     const ChunkPartials& partials, bool with_extra, Partial* totals, cudaStream_t s);
 void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n,
-                  const LaneData& init, SampleOut* out, int mode, uint32_t lane, cudaStream_t s);
+                  const LaneData& init, SampleOut* out, int mode, uint32_t lane, uint32_t flags, cudaStream_t s);
 constexpr int kSamplerFem = 2;  // sampler_blocks_per_sm: the fem instantiation
 int sampler_blocks_per_sm(int mode);
 int sampler_threads();

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
         {
             if (lane == 0) {
                 ItemConst c = load_item(a.items, item);
-                P::prepare(c);
+                P::prepare(c, a.rows, a.init, a.flags);
                 ic = c;
             }
             __syncwarp();
@@ -245,14 +245,15 @@ __global__ void k_combine_welford(const uint64_t* __restrict__ chunk0, const Dev
 
 template <class P>
 __global__ void k_debug(const RowRec* __restrict__ rows, EdgeTables edges,
-                        const DevItem* __restrict__ items, uint32_t n, LaneData init, SampleOut* __restrict__ out) {
+                        const DevItem* __restrict__ items, uint32_t n, LaneData init, uint32_t flags,
+                        SampleOut* __restrict__ out) {
     __shared__ LogEntry s_log[128];
     load_log_table(s_log);
     __syncthreads();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     ItemConst ic = load_item(items, i);
-    P::prepare(ic);
+    P::prepare(ic, rows, init, flags);
     typename P::W w;
     P::start(w, ic, init, rows, items[i].first);
     unsigned long long draws = 0, jumps = 0;
@@ -496,16 +497,16 @@ void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, u
 }
 
 void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n, const LaneData& init,
-                  SampleOut* out, int mode, uint32_t lane, cudaStream_t s) {
+                  SampleOut* out, int mode, uint32_t lane, uint32_t flags, cudaStream_t s) {
     const int g = grid_for(n, 128);
     if (lane == EXPMC_LANE_FEM) {
-        k_debug<FemPolicy><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+        k_debug<FemPolicy><<<g, 128, 0, s>>>(rows, edges, items, n, init, flags, out);
     } else if (mode == EXPMC_SAMPLER_EVENT) {
-        if (lane == EXPMC_LANE_FORWARD) k_debug<EdPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
-        else k_debug<EdPolicy<false>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+        if (lane == EXPMC_LANE_FORWARD) k_debug<EdPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, flags, out);
+        else k_debug<EdPolicy<false>><<<g, 128, 0, s>>>(rows, edges, items, n, init, flags, out);
     } else {
-        if (lane == EXPMC_LANE_FORWARD) k_debug<RefPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
-        else k_debug<RefPolicy<false>><<<g, 128, 0, s>>>(rows, edges, items, n, init, out);
+        if (lane == EXPMC_LANE_FORWARD) k_debug<RefPolicy<true>><<<g, 128, 0, s>>>(rows, edges, items, n, init, flags, out);
+        else k_debug<RefPolicy<false>><<<g, 128, 0, s>>>(rows, edges, items, n, init, flags, out);
     }
     cuda_check(cudaGetLastError(), "k_debug launch");
 }

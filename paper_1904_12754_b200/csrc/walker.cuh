@@ -205,6 +205,11 @@ struct ItemConst {
     uint32_t entry;
     uint32_t key3;
     uint32_t base;
+    // event-driven entry mode: closed-form first holding interval (EdPolicy::prepare)
+    uint64_t m_safe;    // M = 2^53 - K < m_safe => the path never leaves the entry (0: off)
+    double hold_fine;   // that path's (fine, coarse) and run_level sample x
+    double hold_coarse;
+    double hold_x;
 };
 
 // sample_initial (paths.cpp:32-36): the path's first draw picks the start state by
@@ -375,6 +380,8 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.entry = it.entry;
     ic.key3 = it.key3;
     ic.base = it.base;
+    ic.m_safe = 0;
+    ic.hold_fine = ic.hold_coarse = ic.hold_x = 0.0;
     return ic;
 }
 

@@ -89,3 +89,36 @@ def test_ed_driver_c1_rows_vs_exact(gpu, oracle_lib):
     assert res["converged"].all()
     assert math.sqrt(float(np.mean(err ** 2))) <= cfg.epsilon
     assert float(np.mean(np.abs(err) > 3 * res["statistical_error"] + res["bias_estimate"])) <= 0.02
+
+
+@pytest.mark.parametrize("level,base", [(0, 1), (3, 1), (1, 0), (4, 0)])
+def test_ed_closed_form_first_hold_is_exact(gpu, level, base):
+    # The closed-form first hold (ed_walker.cuh) must reproduce the full first event bit for
+    # bit: per-sample values, costs, jumps and end states, and the run_level sums, with the
+    # shortcut on and off.  Small rates so that most samples never leave the entry, plus a row
+    # with d != 0 (non-trivial exponent), a negative off-diagonal and an absorbing row.
+    rng = np.random.default_rng(5)
+    n = 40
+    dense = np.where(rng.random((n, n)) < 0.1, rng.uniform(-1.0, 1.0, (n, n)), 0.0)
+    np.fill_diagonal(dense, rng.uniform(-2.0, 1.0, n))
+    dense[7, :] = 0.0
+    dense[7, 7] = -0.5  # absorbing
+    a = P.SparseMatrix.from_dense(dense)
+    u = rng.uniform(-1.0, 1.0, n)
+    rows = np.array([0, 3, 7, 11, 39])
+    with P.Context(a, u, sampler="event") as c:
+        for beta in (0.05, 0.7):
+            c.set_full_hold(False)
+            fast = c.sample_debug(beta, rows[:, None].repeat(400, 1).ravel(), level, base,
+                                  (1000 + rows)[:, None].repeat(400, 1).ravel(), np.tile(np.arange(400), len(rows)))
+            rf = c.run_level_batch(beta, rows, level, base, 3, 40_000, 1000 + rows)
+            c.set_full_hold(True)
+            full = c.sample_debug(beta, rows[:, None].repeat(400, 1).ravel(), level, base,
+                                  (1000 + rows)[:, None].repeat(400, 1).ravel(), np.tile(np.arange(400), len(rows)))
+            rr = c.run_level_batch(beta, rows, level, base, 3, 40_000, 1000 + rows)
+            for k in ("fine", "coarse", "cost", "jumps", "end_state"):
+                assert np.array_equal(fast[k], full[k]), (beta, k)
+            for k in ("sum", "sum_sq", "cost", "jumps"):
+                assert np.array_equal(rf[k], rr[k]), (beta, k)
+            if beta == 0.05:
+                assert np.mean(fast["jumps"] == 0) > 0.5  # the shortcut was exercised
