@@ -166,6 +166,8 @@ template <bool F>
 struct RefPolicy {
     using W = Walker;
     static constexpr bool kExtra = false;
+    static constexpr bool kScreen = false;
+    static __device__ __forceinline__ bool screen(const ItemConst&, uint64_t) { return false; }
     static constexpr int kMinBlocks = EXPMC_SAMPLER_MINB;
     static __device__ __forceinline__ void prepare(ItemConst&, const RowRec*, const LaneData&, uint32_t) {}
     static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
@@ -194,6 +196,14 @@ template <bool F>
 struct EdPolicy {
     using W = EdWalker;
     static constexpr bool kExtra = false;
+    static constexpr bool kScreen = !F;  // entry mode: all samples start in ic.entry
+    // The first event's closed-form test alone: block 0 of the sample's stream, first word.
+    static __device__ __forceinline__ bool screen(const ItemConst& ic, uint64_t sample) {
+        uint32_t c0 = 0, c1 = static_cast<uint32_t>(sample), c2 = static_cast<uint32_t>(sample >> 32), c3 = ic.key3;
+        philox10(c0, c1, c2, c3, static_cast<uint32_t>(ic.seed), static_cast<uint32_t>(ic.seed >> 32));
+        const uint64_t k53 = ((static_cast<uint64_t>(c2) << 32) | c3) >> 11;  // rng.hpp:32-35
+        return (uint64_t{1} << 53) - k53 < ic.m_safe;
+    }
     static constexpr int kMinBlocks = EXPMC_SAMPLER_MINB;
     // The closed-form first hold (header): threshold and stay-at-entry values, once per chunk.
     static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData& ld,

@@ -135,6 +135,8 @@ __device__ __forceinline__ double fem_finish(const FemWalker& f, const ItemConst
 struct FemPolicy {
     using W = FemWalker;
     static constexpr bool kExtra = true;
+    static constexpr bool kScreen = false;
+    static __device__ __forceinline__ bool screen(const ItemConst&, uint64_t) { return false; }
     static constexpr int kMinBlocks = EXPMC_FEM_MINB;
     static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec*, const LaneData&, uint32_t) {
         ic.h_fine = __ddiv_rn(ic.dt, 3.0);  // scaled_simpson's h = step / 3 (mlmc.cpp:68)

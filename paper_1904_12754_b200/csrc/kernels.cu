@@ -92,6 +92,9 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
     const unsigned full = 0xFFFFFFFFu;
     __shared__ double s_x[W ? kWarps * kChunk : 1];
     double* const wx = s_x + (W ? (threadIdx.x >> 5) * kChunk : 0);
+    // screened policies: the chunk's slots that need the full walker, ascending
+    __shared__ uint16_t s_list[P::kScreen ? kWarps * kChunk : 1];
+    uint16_t* const wl = s_list + (P::kScreen ? (threadIdx.x >> 5) * kChunk : 0);
     __shared__ LogEntry s_log[128];
     load_log_table(s_log);
     __syncthreads();
@@ -129,17 +132,48 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
 
         double sum = 0.0, sum_sq = 0.0, extra = 0.0;
         unsigned long long cost = 0, jumps = 0;
+        // Work list of the walker loop: slots 0..cnt-1 of the chunk or -- when the item has a
+        // closed-form first hold (ed_walker.cuh) -- only the slots that a converged screening
+        // pass found to need the full walker.  The screen costs one Philox block per sample with
+        // every lane busy; closed-form samples never enter the divergent walker loop.
+        uint32_t nwork = cnt;
+        bool listed = false;
+        if constexpr (P::kScreen) {
+            if (ic.m_safe != 0) {
+                listed = true;
+                nwork = 0;
+                const double hx = ic.hold_x;
+                for (uint32_t j0 = 0; j0 < cnt; j0 += 32u) {
+                    const uint32_t j = j0 + lane;
+                    const bool valid = j < cnt;
+                    const bool held = valid && P::screen(ic, lo + j);
+                    if (held) {
+                        if constexpr (W) {
+                            wx[j] = hx;
+                        } else {
+                            sum = __dadd_rn(sum, hx);
+                            sum_sq = __dadd_rn(sum_sq, __dmul_rn(hx, hx));
+                        }
+                        cost += 2u * ic.nsteps;  // N rejected draws + N steps (ed_segment(0, N))
+                    }
+                    const unsigned need = __ballot_sync(full, valid && !held);
+                    if (valid && !held) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>(j);
+                    nwork += __popc(need);
+                }
+                __syncwarp();
+            }
+        }
         typename P::W w;
         bool active = false;
-        uint32_t my = 0;  // Welford: the running sample's slot in the chunk
-        // Lanes start samples lo + lane; a lane whose sample ends takes the next unstarted
-        // index in the same divergent section as its finish (one ballot per trip).
-        if (lane < cnt) {
-            P::start(w, ic, a.init, a.rows, lo + lane);
+        uint32_t my = 0;  // the running sample's slot in the chunk
+        // Lanes start work entries 0..31; a lane whose sample ends takes the next unstarted
+        // entry in the same divergent section as its finish (one ballot per trip).
+        if (lane < nwork) {
+            my = listed ? wl[lane] : lane;
+            P::start(w, ic, a.init, a.rows, lo + my);
             active = true;
-            if constexpr (W) my = lane;
         }
-        uint32_t next = cnt < 32u ? cnt : 32u;
+        uint32_t next = nwork < 32u ? nwork : 32u;
         while (__any_sync(full, active)) {
             const bool done = active && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps);
             const unsigned fin = __ballot_sync(full, done);
@@ -155,9 +189,9 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
                 }
                 cost += ic.nsteps;
                 const uint32_t mine = next + __popc(fin & lanemask_lt());
-                if (mine < cnt) {
-                    P::start(w, ic, a.init, a.rows, lo + mine);
-                    if constexpr (W) my = mine;
+                if (mine < nwork) {
+                    my = listed ? wl[mine] : mine;
+                    P::start(w, ic, a.init, a.rows, lo + my);
                 } else {
                     active = false;
                 }
@@ -198,31 +232,83 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
     }
 }
 
-__global__ void k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems, uint64_t g_begin,
-                          uint64_t g_end, ChunkPartials p, bool with_extra, Partial* __restrict__ totals) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nitems) return;
+// Ordered combines: one warp per item.  The fp64 sums must be taken in ascending chunk order
+// (one dependent add per chunk), so the warp stages tiles of the item's chunk partials in
+// shared memory with coalesced loads (32 in flight per lane group) and lane 0 runs the
+// sequential chain out of shared memory; the integer counts are associative and are reduced
+// across the lanes.  (A thread per item waited one global-load latency per chunk: 280 ms of a
+// 16k-component C4 step went to the hub items' 10^4-10^5 chunks.)
+constexpr int kCombWarps = 4;
+constexpr int kCombTile = 256;
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    return x;
+}
+
+__global__ void __launch_bounds__(kCombWarps * 32) k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems,
+                                                             uint64_t g_begin, uint64_t g_end, ChunkPartials p,
+                                                             bool with_extra, Partial* __restrict__ totals) {
+    __shared__ double s_v[kCombWarps][3][kCombTile];
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t i = blockIdx.x * kCombWarps + w;
+    if (i >= nitems) return;  // warp-uniform
     const uint64_t c0 = chunk0[i] > g_begin ? chunk0[i] : g_begin;
     const uint64_t c1 = chunk0[i + 1] < g_end ? chunk0[i + 1] : g_end;
     if (c0 >= c1) return;
-    Partial t = totals[i];
-    for (uint64_t g = c0; g < c1; ++g) {  // ascending chunk order (parallel.hpp:52)
-        const uint64_t k = g - g_begin;
-        t.sum = __dadd_rn(t.sum, p.sum[k]);
-        t.sum_sq = __dadd_rn(t.sum_sq, p.sum_sq[k]);
-        if (with_extra) t.extra = __dadd_rn(t.extra, p.extra[k]);
-        t.cost += p.cost[k];
-        t.jumps += p.jumps[k];
+    double sum = 0.0, sum_sq = 0.0, extra = 0.0;
+    if (lane == 0) {
+        sum = totals[i].sum;
+        sum_sq = totals[i].sum_sq;
+        extra = totals[i].extra;
     }
-    totals[i] = t;
+    unsigned long long cost = 0, jumps = 0;
+    for (uint64_t base = c0; base < c1; base += kCombTile) {
+        const uint32_t n = static_cast<uint32_t>(c1 - base < kCombTile ? c1 - base : kCombTile);
+        for (uint32_t j = lane; j < n; j += 32) {
+            const uint64_t k = base + j - g_begin;
+            s_v[w][0][j] = p.sum[k];
+            s_v[w][1][j] = p.sum_sq[k];
+            if (with_extra) s_v[w][2][j] = p.extra[k];
+            cost += p.cost[k];
+            jumps += p.jumps[k];
+        }
+        __syncwarp();
+        if (lane == 0) {  // ascending chunk order (parallel.hpp:52)
+#pragma unroll 8
+            for (uint32_t j = 0; j < n; ++j) {
+                sum = __dadd_rn(sum, s_v[w][0][j]);
+                sum_sq = __dadd_rn(sum_sq, s_v[w][1][j]);
+                if (with_extra) extra = __dadd_rn(extra, s_v[w][2][j]);
+            }
+        }
+        __syncwarp();
+    }
+    cost = warp_sum_u64(cost);
+    jumps = warp_sum_u64(jumps);
+    if (lane == 0) {
+        Partial t = totals[i];
+        t.sum = sum;
+        t.sum_sq = sum_sq;
+        if (with_extra) t.extra = extra;
+        t.cost += cost;
+        t.jumps += jumps;
+        totals[i] = t;
+    }
 }
 
 // Welford combine: per item, Chan-merge its chunks' (mean, m2, n) in ascending chunk order
 // (parallel_samples' ordered combine, parallel.hpp:52).  n of a chunk is its sample count.
-__global__ void k_combine_welford(const uint64_t* __restrict__ chunk0, const DevItem* __restrict__ items,
-                                  uint32_t nitems, uint64_t g_begin, uint64_t g_end, ChunkPartials p,
-                                  Partial* __restrict__ totals) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+// Same warp-per-item staging as k_combine.
+__global__ void __launch_bounds__(kCombWarps * 32) k_combine_welford(const uint64_t* __restrict__ chunk0,
+                                                                     const DevItem* __restrict__ items,
+                                                                     uint32_t nitems, uint64_t g_begin, uint64_t g_end,
+                                                                     ChunkPartials p, Partial* __restrict__ totals) {
+    __shared__ double s_v[kCombWarps][2][kCombTile];
+    __shared__ uint32_t s_n[kCombWarps][kCombTile];
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const uint32_t i = blockIdx.x * kCombWarps + w;
     if (i >= nitems) return;
     const uint64_t c0 = chunk0[i] > g_begin ? chunk0[i] : g_begin;
     const uint64_t c1 = chunk0[i + 1] < g_end ? chunk0[i + 1] : g_end;
@@ -230,17 +316,34 @@ __global__ void k_combine_welford(const uint64_t* __restrict__ chunk0, const Dev
     Partial t = totals[i];  // sum = mean, sum_sq = m2, extra = n (exact below 2^53)
     uint64_t n = static_cast<uint64_t>(t.extra);
     const uint64_t first = items[i].first, end = first + items[i].count;
-    for (uint64_t g = c0; g < c1; ++g) {
-        const uint64_t k = g - g_begin;
-        const uint64_t chunk = first / kChunk + (g - chunk0[i]);
-        const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
-        const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
-        welford_merge(t.sum, t.sum_sq, n, p.sum[k], p.sum_sq[k], hi > lo ? hi - lo : 0);
-        t.cost += p.cost[k];
-        t.jumps += p.jumps[k];
+    unsigned long long cost = 0, jumps = 0;
+    for (uint64_t base = c0; base < c1; base += kCombTile) {
+        const uint32_t m = static_cast<uint32_t>(c1 - base < kCombTile ? c1 - base : kCombTile);
+        for (uint32_t j = lane; j < m; j += 32) {
+            const uint64_t g = base + j;
+            const uint64_t k = g - g_begin;
+            const uint64_t chunk = first / kChunk + (g - chunk0[i]);
+            const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
+            const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
+            s_v[w][0][j] = p.sum[k];
+            s_v[w][1][j] = p.sum_sq[k];
+            s_n[w][j] = static_cast<uint32_t>(hi > lo ? hi - lo : 0);
+            cost += p.cost[k];
+            jumps += p.jumps[k];
+        }
+        __syncwarp();
+        if (lane == 0)
+            for (uint32_t j = 0; j < m; ++j) welford_merge(t.sum, t.sum_sq, n, s_v[w][0][j], s_v[w][1][j], s_n[w][j]);
+        __syncwarp();
     }
-    t.extra = static_cast<double>(n);
-    totals[i] = t;
+    cost = warp_sum_u64(cost);
+    jumps = warp_sum_u64(jumps);
+    if (lane == 0) {
+        t.cost += cost;
+        t.jumps += jumps;
+        t.extra = static_cast<double>(n);
+        totals[i] = t;
+    }
 }
 
 template <class P>
@@ -486,13 +589,15 @@ void launch_sampler_welford(const SamplerArgs& a, int grid, int mode, uint32_t l
 
 void launch_combine_welford(const uint64_t* chunk0, const DevItem* items, uint32_t nitems, uint64_t g_begin,
                             uint64_t g_end, const ChunkPartials& partials, Partial* totals, cudaStream_t s) {
-    k_combine_welford<<<grid_for(nitems, 256), 256, 0, s>>>(chunk0, items, nitems, g_begin, g_end, partials, totals);
+    k_combine_welford<<<grid_for(nitems, kCombWarps), kCombWarps * 32, 0, s>>>(chunk0, items, nitems, g_begin, g_end,
+                                                                               partials, totals);
     cuda_check(cudaGetLastError(), "k_combine_welford launch");
 }
 
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
                     const ChunkPartials& partials, bool with_extra, Partial* totals, cudaStream_t s) {
-    k_combine<<<grid_for(nitems, 256), 256, 0, s>>>(chunk0, nitems, g_begin, g_end, partials, with_extra, totals);
+    k_combine<<<grid_for(nitems, kCombWarps), kCombWarps * 32, 0, s>>>(chunk0, nitems, g_begin, g_end, partials,
+                                                                       with_extra, totals);
     cuda_check(cudaGetLastError(), "k_combine launch");
 }
 
