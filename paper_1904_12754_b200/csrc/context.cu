@@ -679,11 +679,13 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
                 int64_t *d_rp = nullptr, *d_col = nullptr;
                 double *d_val = nullptr, *d_u = nullptr, *d_st = nullptr;
                 uint64_t *d_deg = nullptr, *d_begin = nullptr;
-                unsigned* d_err = nullptr;
+                unsigned* d_err = nullptr;  // [0] error bits, [1] heavy-row count
+                uint32_t* d_heavy = nullptr;
                 void* tmp = nullptr;
                 auto cleanup = [&] {
                     cudaFree(d_rp); cudaFree(d_col); cudaFree(d_val); cudaFree(d_u);
                     cudaFree(d_deg); cudaFree(d_begin); cudaFree(d_err); cudaFree(tmp); cudaFree(d_st);
+                    cudaFree(d_heavy);
                 };
                 try {
                     dev_alloc(&d_rp, n + 1);
@@ -692,7 +694,8 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
                     dev_alloc(&d_u, n);
                     dev_alloc(&d_deg, n);
                     dev_alloc(&d_begin, n);
-                    dev_alloc(&d_err, 1);
+                    dev_alloc(&d_err, 2);
+                    dev_alloc(&d_heavy, static_cast<size_t>(std::min<int64_t>(n, nnz / 128 + 1)));
                     dev_alloc(&d_st, 2);
                     cuda_check(cudaMemcpyAsync(d_rp, A->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream), "H2D");
                     if (nnz) {
@@ -701,8 +704,8 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
                     }
                     cuda_check(cudaMemcpyAsync(d_u, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
                     c->ctr.h2d_bytes += (n + 1) * 8 + nnz * 16 + n * 8;
-                    cuda_check(cudaMemsetAsync(d_err, 0, sizeof(unsigned), c->stream), "memset");
-                    launch_count_edges(n, d_rp, d_col, d_val, d_deg, d_err, c->stream);
+                    cuda_check(cudaMemsetAsync(d_err, 0, 2 * sizeof(unsigned), c->stream), "memset");
+                    launch_count_edges(n, d_rp, d_col, d_val, d_deg, d_err, d_heavy, d_err + 1, c->num_sms, c->stream);
                     unsigned err = 0;
                     cuda_check(cudaMemcpyAsync(&err, d_err, sizeof err, cudaMemcpyDeviceToHost, c->stream), "D2H");
                     cuda_check(cudaStreamSynchronize(c->stream), "count edges");
@@ -721,12 +724,13 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
                     dev_alloc(&c->rows, n);
                     dev_alloc(&c->cdf, c->nedges);
                     dev_alloc(&c->tgt, c->nedges);
-                    launch_fill_tables(n, d_rp, d_col, d_val, d_u, d_begin, c->rows, c->cdf, c->tgt, c->stream);
+                    launch_fill_tables(n, d_rp, d_col, d_val, d_u, d_begin, c->rows, c->cdf, c->tgt, d_heavy, d_err + 1,
+                                       c->num_sms, c->stream);
                     d_stats(c->rows, n, d_st, tmp, tb, c->stream);
                     double st[2];
                     cuda_check(cudaMemcpyAsync(st, d_st, sizeof st, cudaMemcpyDeviceToHost, c->stream), "D2H");
                     c->ctr.d2h_bytes += 32;
-                    c->ctr.kernel_launches += 5;
+                    c->ctr.kernel_launches += 7;
                     cuda_check(cudaStreamSynchronize(c->stream), "build tables");
                     c->d_max = st[0];                            // chain.cpp:70
                     c->d_bar = st[1] / static_cast<double>(n);   // chain.cpp:71 (tree-summed)

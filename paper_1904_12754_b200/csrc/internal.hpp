@@ -148,10 +148,11 @@ float bench_gather(uint64_t bytes, int loads_per_thread, int reps, int num_sms, 
 
 // table builder
 void launch_count_edges(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
-                        uint64_t* deg, unsigned int* err, cudaStream_t s);
+                        uint64_t* deg, unsigned int* err, uint32_t* heavy, unsigned int* nheavy, int num_sms,
+                        cudaStream_t s);
 void launch_fill_tables(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
                         const double* u, const uint64_t* begin, RowRec* rows, double* cdf, uint32_t* tgt,
-                        cudaStream_t s);
+                        const uint32_t* heavy, const unsigned int* nheavy, int num_sms, cudaStream_t s);
 void launch_set_vector(int64_t n, const double* u, RowRec* rows, cudaStream_t s);
 void launch_export(int64_t n, const RowRec* rows, double* d, double* rate, int64_t* row_ptr,
                    cudaStream_t s);

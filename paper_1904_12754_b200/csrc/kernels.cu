@@ -372,13 +372,23 @@ __global__ void k_debug(const RowRec* __restrict__ rows, EdgeTables edges,
 // ---------------------------------------------------------------- transition-table builder
 enum : unsigned { kErrNonFinite = 1u, kErrRange = 2u, kErrCanon = 4u };
 
+// Rows with more than kHeavyNnz stored entries (graph hubs: up to ~10^5-10^6 at C3/C4) are
+// handled by a warp each (k_count_heavy / k_fill_heavy); the thread-per-row kernels skip them
+// and queue them.  One thread walking a hub row serialised ~200 ms of the C4 build.
+constexpr int64_t kHeavyNnz = 128;
+
 __global__ void k_count_edges(int64_t n, const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col,
-                              const double* __restrict__ val, uint64_t* __restrict__ deg, unsigned* err) {
+                              const double* __restrict__ val, uint64_t* __restrict__ deg, unsigned* err,
+                              uint32_t* __restrict__ heavy, unsigned* nheavy) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t b = row_ptr[i], e = row_ptr[i + 1];
     unsigned bad = 0;
     if (e < b) bad |= kErrCanon;
+    if (e - b > kHeavyNnz) {
+        heavy[atomicAdd(nheavy, 1u)] = static_cast<uint32_t>(i);
+        return;
+    }
     uint64_t cnt = 0;
     int64_t prev = -1;
     for (int64_t k = b; k < e; ++k) {
@@ -394,6 +404,37 @@ __global__ void k_count_edges(int64_t n, const int64_t* __restrict__ row_ptr, co
     if (bad) atomicOr(err, bad);
 }
 
+// Warp per queued heavy row: the same checks and count, lanes striding over the row.
+__global__ void k_count_heavy(int64_t n, const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col,
+                              const double* __restrict__ val, uint64_t* __restrict__ deg, unsigned* err,
+                              const uint32_t* __restrict__ heavy, const unsigned* nheavy) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); h < *nheavy; h += nw) {
+        const int64_t i = heavy[h];
+        const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+        unsigned bad = 0;
+        unsigned long long cnt = 0;
+        for (int64_t k = b + lane; k < e; k += 32) {
+            const int64_t c = col[k];
+            const double v = val[k];
+            if (c < 0 || c >= n) bad |= kErrRange;
+            if (!isfinite(v)) bad |= kErrNonFinite;
+            if (k > b && c <= col[k - 1]) bad |= kErrCanon;
+            if (c != i && v != 0.0) ++cnt;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+            bad |= __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+        }
+        if (lane == 0) {
+            deg[i] = cnt;
+            if (bad) atomicOr(err, bad);
+        }
+    }
+}
+
 // decompose_impl per row (chain.cpp:29-64), same operation order: running |a_ij| sum, CDF =
 // running sum / rate, last entry exactly 1, sign = (a_ij < 0), d = a_ii + rate.
 __global__ void k_fill_tables(int64_t n, const int64_t* __restrict__ row_ptr, const int64_t* __restrict__ col,
@@ -402,6 +443,7 @@ __global__ void k_fill_tables(int64_t n, const int64_t* __restrict__ row_ptr, co
                               double* __restrict__ cdf, uint32_t* __restrict__ tgt) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (row_ptr[i + 1] - row_ptr[i] > kHeavyNnz) return;  // k_fill_heavy
     const uint64_t e0 = begin[i];
     uint64_t e = e0;
     double diag = 0.0, rate = 0.0;
@@ -435,6 +477,90 @@ __global__ void k_fill_tables(int64_t n, const int64_t* __restrict__ row_ptr, co
     r.begin = static_cast<uint32_t>(e0);
     r.deg = deg | (uniform && deg > 0 ? kUniformRow : 0u);
     rows[i] = r;
+}
+
+// The same per heavy row with one warp: tiles of 32 entries are compacted with a ballot (chain
+// edges keep column order), the running |a_ij| sum stays ONE sequential fp64 chain (lane 0,
+// out of shared memory) so every CDF entry is bit-identical to the thread-per-row result, and
+// the normalisation / uniformity pass runs across the lanes.
+constexpr int kFillWarps = 4;
+
+__global__ void __launch_bounds__(kFillWarps * 32) k_fill_heavy(const int64_t* __restrict__ row_ptr,
+                                                                const int64_t* __restrict__ col,
+                                                                const double* __restrict__ val,
+                                                                const double* __restrict__ u,
+                                                                const uint64_t* __restrict__ begin,
+                                                                RowRec* __restrict__ rows, double* __restrict__ cdf,
+                                                                uint32_t* __restrict__ tgt,
+                                                                const uint32_t* __restrict__ heavy,
+                                                                const unsigned* nheavy) {
+    __shared__ double s_a[kFillWarps][32];
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+    const unsigned full = 0xFFFFFFFFu;
+    const uint32_t nw = gridDim.x * kFillWarps;
+    for (uint32_t h = blockIdx.x * kFillWarps + w; h < *nheavy; h += nw) {
+        const int64_t i = heavy[h];
+        const int64_t b = row_ptr[i], e = row_ptr[i + 1];
+        const uint64_t e0 = begin[i];
+        uint64_t pos = e0;
+        double diag = 0.0, rate = 0.0;  // rate: lane 0's chain, broadcast after the row
+        for (int64_t k0 = b; k0 < e; k0 += 32) {
+            const int64_t k = k0 + lane;
+            int64_t c = -1;
+            double v = 0.0;
+            if (k < e) {
+                c = col[k];
+                v = val[k];
+                if (c == i) diag = v;  // at most one lane of one tile (canonical CSR)
+            }
+            const bool edge = k < e && c != i && v != 0.0;
+            const unsigned m = __ballot_sync(full, edge);
+            const uint32_t r = __popc(m & lanemask_lt());
+            if (edge) {
+                s_a[w][r] = fabs(v);
+                tgt[pos + r] = static_cast<uint32_t>(c) | (v < 0.0 ? kSignBit : 0u);
+            }
+            __syncwarp();
+            const uint32_t cntt = __popc(m);
+            if (lane == 0) {
+                for (uint32_t j = 0; j < cntt; ++j) {
+                    rate = __dadd_rn(rate, s_a[w][j]);  // chain.cpp:39-46, column order
+                    s_a[w][j] = rate;
+                }
+            }
+            __syncwarp();
+            if (lane < cntt) cdf[pos + lane] = s_a[w][lane];
+            __syncwarp();
+            pos += cntt;
+        }
+        rate = __shfl_sync(full, rate, 0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // diag: the one lane that saw it (others hold 0.0)
+            const double od = __shfl_xor_sync(full, diag, o);
+            if (od != 0.0) diag = od;
+        }
+        const uint32_t deg = static_cast<uint32_t>(pos - e0);
+        bool uniform = true;
+        if (rate > 0.0) {
+            __syncwarp();  // the row's cdf stores are visible to the warp
+            for (uint64_t k = e0 + lane; k + 1 < pos; k += 32) {
+                const double c = __ddiv_rn(cdf[k], rate);
+                cdf[k] = c;
+                uniform = uniform && c == __ddiv_rn(static_cast<double>(k - e0 + 1), static_cast<double>(deg));
+            }
+            if (lane == 0) cdf[pos - 1] = 1.0;
+        }
+        uniform = __all_sync(full, uniform);
+        if (lane == 0) {
+            RowRec rr;
+            rr.d = __dadd_rn(diag, rate);
+            rr.rate = rate;
+            rr.u = u[i];
+            rr.begin = static_cast<uint32_t>(e0);
+            rr.deg = deg | (uniform && deg > 0 ? kUniformRow : 0u);
+            rows[i] = rr;
+        }
+    }
 }
 
 __global__ void k_set_vector(int64_t n, const double* __restrict__ u, RowRec* __restrict__ rows) {
@@ -617,17 +743,22 @@ void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, ui
 }
 
 void launch_count_edges(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val, uint64_t* deg,
-                        unsigned int* err, cudaStream_t s) {
+                        unsigned int* err, uint32_t* heavy, unsigned int* nheavy, int num_sms, cudaStream_t s) {
     if (n == 0) return;
-    k_count_edges<<<grid_for(n, 256), 256, 0, s>>>(n, row_ptr, col, val, deg, err);
+    k_count_edges<<<grid_for(n, 256), 256, 0, s>>>(n, row_ptr, col, val, deg, err, heavy, nheavy);
     cuda_check(cudaGetLastError(), "k_count_edges launch");
+    k_count_heavy<<<num_sms * 4, 256, 0, s>>>(n, row_ptr, col, val, deg, err, heavy, nheavy);
+    cuda_check(cudaGetLastError(), "k_count_heavy launch");
 }
 
 void launch_fill_tables(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val, const double* u,
-                        const uint64_t* begin, RowRec* rows, double* cdf, uint32_t* tgt, cudaStream_t s) {
+                        const uint64_t* begin, RowRec* rows, double* cdf, uint32_t* tgt, const uint32_t* heavy,
+                        const unsigned int* nheavy, int num_sms, cudaStream_t s) {
     if (n == 0) return;
     k_fill_tables<<<grid_for(n, 128), 128, 0, s>>>(n, row_ptr, col, val, u, begin, rows, cdf, tgt);
     cuda_check(cudaGetLastError(), "k_fill_tables launch");
+    k_fill_heavy<<<num_sms * 8, kFillWarps * 32, 0, s>>>(row_ptr, col, val, u, begin, rows, cdf, tgt, heavy, nheavy);
+    cuda_check(cudaGetLastError(), "k_fill_heavy launch");
 }
 
 void launch_set_vector(int64_t n, const double* u, RowRec* rows, cudaStream_t s) {

@@ -303,3 +303,44 @@ def test_set_vector_rebinds_u(gpu):
         ctx.set_vector(2.0 * cfg.u)
         b = ctx.sample_debug(1.0, 3, 2, 0, 9, np.arange(64))
     assert np.array_equal(b["fine"], 2.0 * a["fine"]) and np.array_equal(a["cost"], b["cost"])
+
+
+def test_tables_heavy_rows_bitwise_equal_oracle(gpu, oracle_lib):
+    # Rows above the warp-per-row threshold (kHeavyNnz = 128 stored entries; kernels.cu
+    # k_count_heavy / k_fill_heavy): random magnitudes (non-uniform CDF, one sequential sum
+    # chain), explicit zeros, negative entries, the diagonal mid-row, a uniform-weight hub, and
+    # light rows in between -- every table entry bit-identical to decompose (chain.cpp:15-71).
+    rng = np.random.default_rng(11)
+    n = 3000
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        if i in (5, 1700):
+            k = 2500 if i == 5 else 129
+            c = np.sort(rng.choice(n, size=k, replace=False))
+            v = rng.uniform(-2.0, 2.0, k) * (rng.random(k) > 0.05)
+        elif i == 2999:
+            c = np.arange(0, n, 2)
+            v = np.ones(len(c))
+        else:
+            c = np.sort(rng.choice(n, size=int(rng.integers(0, 12)), replace=False))
+            v = rng.uniform(-1.0, 1.0, len(c))
+        rows += [i] * len(c)
+        cols += list(c)
+        vals += list(v)
+    rp = np.concatenate([[0], np.cumsum(np.bincount(np.array(rows), minlength=n))]).astype(np.int64)
+    a = P.SparseMatrix(n, rp, np.array(cols, np.int64), np.array(vals, np.float64))  # explicit zeros kept
+    ref = oracle_lib.chain(CSR(a.n, a.row_ptr, a.col, a.val)).decomposition()
+    u = rng.random(n)
+    with P.Context(a, u) as ctx:
+        dec = ctx.decomposition()
+        for k in ("d", "rate", "row_ptr", "jump_cdf", "jump_target", "sign"):
+            assert np.array_equal(dec[k], ref[k]), k
+        assert ctx.d_max == ref["d_max"]
+        # paths through the hubs: per-sample parity with the oracle (cost / jumps / end state exact)
+        och = oracle_lib.chain(CSR(a.n, a.row_ptr, a.col, a.val))
+        for entry in (5, 1700, 2999):
+            s = ctx.sample_debug(0.3, entry, 2, 1, 7, np.arange(500))
+            o = och.samples(u, entry, 0.3, 2, 1, 7, np.arange(500))
+            for k in ("cost", "jumps", "end_state"):
+                assert np.array_equal(s[k], o[k]), (entry, k)
+            assert ulp_diff(s["fine"], o["fine"]).max() <= ULP_TOL
