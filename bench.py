@@ -290,8 +290,10 @@ def main():
     graph_like = cfg.name.startswith(("c3", "c4", "c5"))
     # C1/C2: the whole job per step.  C3-C5 (10^6-10^7 components, hub rows infeasible at the
     # stated eps): a seeded sample of components per step and a per-component budget.
-    r = args.rows_per_step if args.rows_per_step or not graph_like else 65536
-    max_cost = args.max_cost if args.max_cost is not None else (1e10 if graph_like else 0.0)
+    r = args.rows_per_step if args.rows_per_step or not graph_like else (4096 if cfg.name.startswith("c5") else 65536)
+    # per-component budgets of DESIGN §7b: 1e10 model units for C3/C4, 1e9 for C5 (eps = 1e-4)
+    default_budget = (1e9 if cfg.name.startswith("c5") else 1e10) if graph_like else 0.0
+    max_cost = args.max_cost if args.max_cost is not None else default_budget
     sampler = args.sampler or cfg.sampler
     universe = cfg.rows if cfg.rows is not None else np.arange(cfg.a.n, dtype=np.int64)
     if args.impl == "reference":
