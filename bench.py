@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--sampler", default=None, choices=["reference", "event"], help="override the config's sampler")
     p.add_argument("--full-hold", action="store_true",
                    help="event sampler: evaluate first holding intervals in full (A/B of the closed-form hold)")
+    p.add_argument("--log-hold", action="store_true",
+                   help="reference-order sampler: time-space holding tests with a log per event (A/B of S-mode)")
     p.add_argument("--multi", default="rows", choices=["rows", "samples"],
                    help="N>1: shard components over ranks (no collective) or shard every component's "
                         "samples with an exact NCCL all-reduce of the chunk partials")
@@ -333,6 +335,8 @@ def main():
     ctx = P.Context(cfg.a, cfg.u, device=local, sampler=sampler)
     if args.full_hold:
         ctx.set_full_hold(True)
+    if args.log_hold:
+        ctx.set_log_hold(True)
     sample_shard = args.multi == "samples" and world > 1
     if sample_shard:  # every rank runs the same components; chunk g is sampled on rank g % world
         obj = [P.nccl_unique_id() if rank == 0 else None]
@@ -423,6 +427,8 @@ def main():
             with P.Context(cfg.a, cfg.u, device=local, sampler=sampler) as c2:
                 if args.full_hold:
                     c2.set_full_hold(True)
+                if args.log_hold:
+                    c2.set_log_hold(True)
                 if sample_shard:
                     c2.shard_samples(ids[s], rank, world)
                 rows = batches[args.warmup + s]

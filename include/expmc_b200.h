@@ -44,6 +44,10 @@ extern "C" {
  * every sample's first holding interval in full instead of deciding "never leaves the entry"
  * from the first draw against a per-item threshold (same outcomes; A/B testing only). */
 #define EXPMC_SAMPLER_FLAG_FULL_HOLD 1u
+/* LOG_HOLD: the reference-order sampler runs every holding test in time space (E = -log1p(-u)
+ * against rate * remaining) instead of probability space (1 - u against e^{-rate*remaining},
+ * no logarithm); same draws and outcomes up to ulp ties (A/B testing only). */
+#define EXPMC_SAMPLER_FLAG_LOG_HOLD 2u
 
 /* Sampling lanes of the reference's Philox key (mlmc.cpp:94-96).  ENTRY estimates
  * (e^{tA}u)_entry; FORWARD estimates sum_i (e^{tA}u)_i from paths started at a state drawn

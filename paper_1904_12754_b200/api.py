@@ -283,7 +283,15 @@ class Context:
     def set_full_hold(self, full: bool):
         """Event sampler only: evaluate every first holding interval in full (True) instead of
         the closed-form stay-at-entry decision (False, the default) -- same outcomes; A/B tests."""
-        _check(L.lib.expmc_ctx_set_sampler_flags(self._h, 1 if full else 0))
+        self._flags = (getattr(self, "_flags", 0) & ~1) | (1 if full else 0)
+        _check(L.lib.expmc_ctx_set_sampler_flags(self._h, self._flags))
+
+    def set_log_hold(self, log: bool):
+        """Reference-order sampler: run every holding test in time space with a logarithm
+        (True) instead of probability space (False, the default) -- same draws and outcomes up
+        to ulp ties; A/B tests."""
+        self._flags = (getattr(self, "_flags", 0) & ~2) | (2 if log else 0)
+        _check(L.lib.expmc_ctx_set_sampler_flags(self._h, self._flags))
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:

@@ -858,7 +858,8 @@ int expmc_ctx_set_sampler(expmc_ctx* c, int32_t mode) {
 int expmc_ctx_set_sampler_flags(expmc_ctx* c, uint32_t flags) {
     return guarded([&] {
         need(c != nullptr, EXPMC_EINVAL, "null context");
-        need((flags & ~EXPMC_SAMPLER_FLAG_FULL_HOLD) == 0u, EXPMC_EINVAL, "unknown sampler flag");
+        need((flags & ~(EXPMC_SAMPLER_FLAG_FULL_HOLD | EXPMC_SAMPLER_FLAG_LOG_HOLD)) == 0u, EXPMC_EINVAL,
+             "unknown sampler flag");
         c->sampler_flags = flags;
     });
 }

@@ -169,7 +169,9 @@ struct RefPolicy {
     static constexpr bool kScreen = false;
     static __device__ __forceinline__ bool screen(const ItemConst&, uint64_t) { return false; }
     static constexpr int kMinBlocks = EXPMC_SAMPLER_MINB;
-    static __device__ __forceinline__ void prepare(ItemConst&, const RowRec*, const LaneData&, uint32_t) {}
+    static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData&, uint32_t flags) {
+        prepare_hold(ic, rows, flags);
+    }
     static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
                                                  uint64_t s) {
         walker_start<F>(w, ic, ld, rows, s);

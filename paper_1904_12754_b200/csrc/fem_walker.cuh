@@ -106,7 +106,7 @@ __device__ __forceinline__ bool fem_event(FemWalker& f, const ItemConst& ic, con
         f.e1 = e[1];
     }
     if (++w.step == ic.nsteps) return true;
-    w.remaining = ic.dt;
+    w.hold = fresh_hold(ic, w.cur.rate);
     return false;
 }
 
@@ -138,7 +138,8 @@ struct FemPolicy {
     static constexpr bool kScreen = false;
     static __device__ __forceinline__ bool screen(const ItemConst&, uint64_t) { return false; }
     static constexpr int kMinBlocks = EXPMC_FEM_MINB;
-    static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec*, const LaneData&, uint32_t) {
+    static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData&, uint32_t flags) {
+        prepare_hold(ic, rows, flags);
         ic.h_fine = __ddiv_rn(ic.dt, 3.0);  // scaled_simpson's h = step / 3 (mlmc.cpp:68)
         ic.h_coarse = __ddiv_rn(__dmul_rn(2.0, ic.dt), 3.0);
     }

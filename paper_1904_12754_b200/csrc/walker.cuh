@@ -182,15 +182,21 @@ __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begi
 }
 
 // ----------------------------------------------------------------------------- walker
-// Holding-interval test in log space.  The reference decides "no jump in the rest of the
-// interval" by u >= q with q = -expm1(-rate*remaining) (paths.cpp:53, 68, 90) and, on a jump,
-// spends E = -log1p(-u) of the interval (paths.cpp:54).  Mathematically u >= 1 - e^{-x} is
-// E >= x (x = rate*remaining), so the walker computes E once per event and compares it with
-// x: the draws consumed, the jump chain, the exponents and every sample value are the
-// reference's; the only difference is that a u lying within one ulp of the threshold may
-// round the other way (probability ~1e-16 per event -- the same order as the CUDA-vs-glibc
-// expm1 ulp differences that reference-order sampling has to accept anyway).  This removes the
-// expm1 from every event and the per-level nojump_ table altogether.
+// Holding-interval test.  The reference decides "no jump in the rest of the interval" by
+// u >= q with q = -expm1(-rate*remaining) (paths.cpp:53, 68, 90) and, on a jump, spends
+// E = -log1p(-u) of the interval (paths.cpp:54).  With 1 - u = M 2^-53 exactly (M = 2^53 - K),
+// u < q is 1 - u > S, S = e^{-rate*remaining}: the walker carries S itself ("S-mode", scaled by
+// 2^53: hold = S 2^53, compared with the integer M) and a jump multiplies it by 1/(1 - u)
+// (e^{-rate (remaining - E/rate)} = S / (1 - u)) -- one correctly-rounded-to-1-ulp divide, no
+// logarithm, no exponential.  A fresh step starts from S0 = e^{-rate dt}, cached per item for
+// the entry row's rate (every interior row of C1/C2/C5 shares it).  When a jump changes the
+// rate, the rest of the step continues in time space ("T-mode", hold = -remaining with
+// remaining = -log(S)/rate, then the reference's log-space test E < rate*remaining per event);
+// so does a step whose S0 would underflow (rate dt >= 690).  Draws, jump chain and every
+// sample value are the reference's; only a u within a few ulps of its threshold may round the
+// other way (probability ~1e-16 per event, the same order as the CUDA-vs-glibc expm1/log1p
+// differences that reference-order sampling accepts anyway).
+constexpr double kSModeMaxX = 690.0;  // e^{-690} ~ 2^-995: S0 2^53 stays a normal number
 
 // Per-item constants (uniform across the warp while it works on one chunk).
 struct ItemConst {
@@ -205,6 +211,10 @@ struct ItemConst {
     uint32_t entry;
     uint32_t key3;
     uint32_t base;
+    // reference-order walker: S-mode start value S0 2^53 for steps in rows of rate s0_rate
+    double s0_rate;     // -1: no cached rate
+    double s0_hold;
+    double smode_max_x; // rate dt below which a fresh step runs in S-mode (-1: T-mode only)
     // event-driven entry mode: closed-form first holding interval (EdPolicy::prepare)
     uint64_t m_safe;    // M = 2^53 - K < m_safe => the path never leaves the entry (0: off)
     double hold_fine;   // that path's (fine, coarse) and run_level sample x
@@ -250,11 +260,32 @@ struct Walker {
     uint32_t state;
     int32_t sign;
     uint32_t half;         // coupled: 0 before the pair's middle node, 1 after
-    double remaining;      // time left in the current fine step
+    double hold;           // S-mode (> 0): e^{-rate*remaining} 2^53; T-mode (<= 0): -remaining
     double acc_a, acc_b;   // single: expo; coupled: coarse, delta
     double d0, d1;         // d[s0], d[s1]
     uint64_t step;         // completed fine steps
 };
+
+// Start value of a fresh fine step in a row of the given rate (paths.cpp:95-96).
+__device__ __forceinline__ double fresh_hold(const ItemConst& ic, double rate) {
+    if (rate == ic.s0_rate) return ic.s0_hold;
+    const double x = __dmul_rn(rate, ic.dt);
+    return x < ic.smode_max_x ? __dmul_rn(exp(-x), 0x1.0p53) : -ic.dt;
+}
+
+// Per chunk (lane 0): the S0 cache for the entry row's rate; flags may force T-mode.
+__device__ __forceinline__ void prepare_hold(ItemConst& ic, const RowRec* __restrict__ rows, uint32_t flags) {
+    if (flags & EXPMC_SAMPLER_FLAG_LOG_HOLD) {
+        ic.smode_max_x = -1.0;
+        return;
+    }
+    const double rate = __ldg(&rows[ic.entry].rate);
+    const double x = __dmul_rn(rate, ic.dt);
+    if (x < ic.smode_max_x) {
+        ic.s0_rate = rate;
+        ic.s0_hold = __dmul_rn(exp(-x), 0x1.0p53);
+    }
+}
 
 template <bool F>
 __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
@@ -265,7 +296,7 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
     w.state = s0;
     w.sign = 1;
     w.half = 0;
-    w.remaining = ic.dt;
+    w.hold = fresh_hold(ic, w.cur.rate);
     w.acc_a = 0.0;
     w.acc_b = 0.0;
     w.d0 = w.cur.d;  // d1 is written at the pair's middle node before it is read
@@ -284,18 +315,32 @@ __device__ __forceinline__ bool walker_hold(Walker& w, const RowRec* __restrict_
     if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
         const uint64_t k53 = stream_pop_bits(w.st);
         ++draws;
-        // E = -log1p(-u), the event's only transcendental.  u = K 2^-53, so 1 - u = (2^53 - K) 2^-53
-        // exactly and log(1 - u) is the same real number as log1p(-u) (fastmath.cuh: <= 1 ulp).
-        const double e = -fast_log(__ull2double_rn((uint64_t{1} << 53) - k53), -53, s_log, c_log_poly);
-        if (e < __dmul_rn(w.cur.rate, w.remaining)) {  // == (u < q), see above
-            w.remaining = __dsub_rn(w.remaining, fast_div(e, w.cur.rate));  // paths.cpp:54
+        const double m = __ull2double_rn((uint64_t{1} << 53) - k53);  // (1 - u) 2^53, exact
+        const bool smode = w.hold > 0.0;
+        double e = 0.0;
+        bool jump;
+        if (smode) {
+            jump = m > w.hold;  // 1 - u > S  <=>  u < q
+        } else {
+            // T-mode: E = -log1p(-u) = -log(m 2^-53) (fastmath.cuh: <= 1 ulp), jump iff E < rate * remaining
+            e = -fast_log(m, -53, s_log, c_log_poly);
+            jump = e < __dmul_rn(w.cur.rate, -w.hold);
+        }
+        if (jump) {
+            // S-mode: S / (1 - u) (scaled); T-mode: -(remaining - E / rate) (paths.cpp:54)
+            const double q = fast_div(smode ? __dmul_rn(w.hold, 0x1.0p53) : e, smode ? m : w.cur.rate);
+            double h1 = smode ? q : -__dsub_rn(-w.hold, q);
             ++jumps;
+            const double rate0 = w.cur.rate;
             const uint32_t ts = pick_edge(edges, w.cur.begin, w.cur.deg, stream_pop_bits(w.st));
             if (ts & kSignBit) w.sign = -w.sign;
             w.state = ts & kTargetMask;
             w.cur = load_row(rows, w.state);
+            if (smode && w.cur.rate != rate0)  // S-mode needs one rate per step: to T-mode
+                h1 = fast_div(fast_log(h1, -53, s_log, c_log_poly), rate0);  // -remaining = log(S) / rate
+            w.hold = h1;
             // remaining <= 0: rounding pushed past the boundary, the step ends (paths.cpp:67)
-            step_done = !(w.remaining > 0.0);
+            step_done = !(smode ? h1 != 0.0 : h1 < 0.0);
         }
     }
     return step_done;
@@ -327,7 +372,7 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
         w.half = 0u;
     }
     if (++w.step == ic.nsteps) return true;
-    w.remaining = ic.dt;  // next fine step: fresh holding interval of length dt (paths.cpp:95-96)
+    w.hold = fresh_hold(ic, w.cur.rate);  // next fine step: fresh holding interval of length dt (paths.cpp:95-96)
     return false;
 }
 
@@ -382,6 +427,9 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.base = it.base;
     ic.m_safe = 0;
     ic.hold_fine = ic.hold_coarse = ic.hold_x = 0.0;
+    ic.s0_rate = -1.0;
+    ic.s0_hold = 0.0;
+    ic.smode_max_x = kSModeMaxX;
     return ic;
 }
 

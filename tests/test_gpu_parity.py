@@ -344,3 +344,31 @@ def test_tables_heavy_rows_bitwise_equal_oracle(gpu, oracle_lib):
             for k in ("cost", "jumps", "end_state"):
                 assert np.array_equal(s[k], o[k]), (entry, k)
             assert ulp_diff(s["fine"], o["fine"]).max() <= ULP_TOL
+
+
+@pytest.mark.parametrize("beta", [0.4, 3.0, 900.0])
+def test_probability_space_hold_equals_time_space(gpu, oracle_lib, beta):
+    # walker.cuh: S-mode (1 - u against e^{-rate*remaining}, no log) vs T-mode (the log-space
+    # test) and the oracle.  Varied rates exercise the S->T switch on rate changes; beta = 900
+    # pushes rate*dt past the S-mode range (T-mode from the first event).  Same jump chains,
+    # costs and end states; values within the parity tolerance.
+    rng = np.random.default_rng(17)
+    n = 60
+    dense = np.where(rng.random((n, n)) < 0.08, rng.uniform(-1.5, 1.5, (n, n)), 0.0)
+    np.fill_diagonal(dense, rng.uniform(-3.0, 0.5, n))
+    dense[:, 3] *= 1.0 - (np.arange(n) != 3)  # column 3 unreachable, row 3 keeps its entries
+    a = P.SparseMatrix.from_dense(dense)
+    u = rng.uniform(-1.0, 1.0, n)
+    och = oracle_lib.chain(CSR(a.n, a.row_ptr, a.col, a.val))
+    with P.Context(a, u) as ctx:
+        for entry, level, base in ((0, 0, 1), (7, 3, 1), (11, 1, 0), (42, 5, 0)):
+            got = {}
+            for log in (False, True):
+                ctx.set_log_hold(log)
+                got[log] = ctx.sample_debug(beta, entry, level, base, 5 + entry, np.arange(300))
+            exp = och.samples(u, entry, beta, level, base, 5 + entry, np.arange(300))
+            for s in (got[False], got[True]):
+                for k in ("cost", "jumps", "end_state"):
+                    assert np.array_equal(s[k], exp[k]), (entry, level, k)
+                assert ulp_diff(s["fine"], exp["fine"]).max() <= ULP_TOL
+                assert ulp_diff(s["coarse"], exp["coarse"]).max() <= ULP_TOL
