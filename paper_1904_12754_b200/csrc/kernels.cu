@@ -142,24 +142,25 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
             if (ic.m_safe != 0) {
                 listed = true;
                 nwork = 0;
-                const double hx = ic.hold_x;
+                uint32_t nheld = 0;  // this lane's closed-form samples, all of value hold_x
                 for (uint32_t j0 = 0; j0 < cnt; j0 += 32u) {
                     const uint32_t j = j0 + lane;
                     const bool valid = j < cnt;
                     const bool held = valid && P::screen(ic, lo + j);
-                    if (held) {
-                        if constexpr (W) {
-                            wx[j] = hx;
-                        } else {
-                            sum = __dadd_rn(sum, hx);
-                            sum_sq = __dadd_rn(sum_sq, __dmul_rn(hx, hx));
-                        }
-                        cost += 2u * ic.nsteps;  // N rejected draws + N steps (ed_segment(0, N))
+                    if constexpr (W) {
+                        if (held) wx[j] = ic.hold_x;
                     }
+                    nheld += held;
                     const unsigned need = __ballot_sync(full, valid && !held);
                     if (valid && !held) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>(j);
                     nwork += __popc(need);
                 }
+                if constexpr (!W) {  // n equal terms: n x and n x^2 (the statistical sampler's sums)
+                    const double hx = ic.hold_x, k = static_cast<double>(nheld);
+                    sum = __dmul_rn(k, hx);
+                    sum_sq = __dmul_rn(k, __dmul_rn(hx, hx));
+                }
+                cost += 2ull * nheld * ic.nsteps;  // N rejected draws + N steps each (ed_segment(0, N))
                 __syncwarp();
             }
         }
