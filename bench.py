@@ -175,15 +175,23 @@ def load_peaks():
     return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic():
-    """DRAM bytes per ms of k_sample time from the committed ncu capture (profiles/ncu_traffic.json:
-    dram__bytes_read.sum + dram__bytes_write.sum of one C2 main-round launch / its duration)."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(path):
+def load_capture(cfg_name):
+    """The committed ncu --set full capture of this config's k_sample (profiles/r01/
+    k_sample_<config>_r1h_key_metrics.json, scripts/prof_c4.sh): DRAM bytes per kernel-ms
+    (dram__bytes_read.sum + dram__bytes_write.sum over the launch) and issue-slot utilisation.
+    None for configs without a capture."""
+    name = cfg_name.split("-")[0]
+    path = os.path.join(ROOT, "profiles", "r01", f"k_sample_{name}_r1h_key_metrics.json")
+    try:
         with open(path) as f:
-            t = json.load(f)
-        return t["dram_bytes"] / t["launch_ms"]
-    return None
+            k = json.load(f)
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        dram = sum(float(k[m]["value"]) * scale[k[m]["unit"]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        return {"bytes_per_ms": dram / float(k["gpu__time_duration.sum"]["value"]),
+                "issue_active_pct": float(k["smsp__issue_active.avg.pct_of_peak_sustained_active"]["value"]),
+                "source": os.path.relpath(path, ROOT)}
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def sampler_only_rate(ref_chain, cfg, threads, seconds=4.0):
@@ -206,16 +214,6 @@ def sampler_only_rate(ref_chain, cfg, threads, seconds=4.0):
         out[f"level{level}"] = {"transitions_per_s": jumps / dt, "samples_per_s": m / dt, "samples": m,
                                 "seconds": dt}
     return out
-
-
-def load_issue_active():
-    """Issue-slot utilisation of k_sample from the committed ncu capture (the kernel's real bound)."""
-    path = os.path.join(ROOT, "profiles", "r01", "k_sample_r1g_key_metrics.json")
-    try:
-        with open(path) as f:
-            return float(json.load(f)["smsp__issue_active.avg.pct_of_peak_sustained_active"]["value"])
-    except (OSError, KeyError, ValueError):
-        return None
 
 
 # ------------------------------------------------------------------------------ reference arm
@@ -396,7 +394,8 @@ def main():
     achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
     peaks, peak_src = load_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic_rate = load_traffic()
+    cap = load_capture(cfg.name)
+    traffic_rate = cap["bytes_per_ms"] if cap else None
     launches = max(1, ctr["sampler_launches"])
     # per launch, like `achieved`: the capture's DRAM bytes per kernel-ms x this run's mean launch length
     traffic = traffic_rate * ctr["sampler_ms"] / launches if traffic_rate else None
@@ -487,13 +486,12 @@ def main():
                          "kernel": "k_sample", "sampler_launches": ctr["sampler_launches"],
                          "kernel_ms": ctr["sampler_ms"], "step_share": ctr["sampler_ms"] / ms_local,
                          "alg_bytes_per_launch": alg_bytes / max(1, ctr["sampler_launches"]),
-                         "traffic_source": "profiles/ncu_traffic.json (C2 main-round launch, ncu --set full): "
-                                           "DRAM bytes per kernel-ms x this run's mean launch ms",
+                         "traffic_source": (cap["source"] + " (ncu --set full of one launch of this config): DRAM "
+                                            "bytes per kernel-ms x this run's mean launch ms") if cap else None,
                          "alg_bytes": f"{ALG_BYTES_PER_JUMP} B/transition + {ALG_BYTES_PER_SAMPLE} B/sample",
                          "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
-                         "issue_active_pct": load_issue_active(),
-                         "binding_resource": "instruction issue (ncu smsp__issue_active, "
-                                             "profiles/r01/k_sample_r1g_key_metrics.json)",
+                         "issue_active_pct": cap["issue_active_pct"] if cap else None,
+                         "binding_resource": "instruction issue (ncu smsp__issue_active)" if cap else None,
                          "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches), "clocks": clk,
         }
