@@ -421,7 +421,8 @@ void sample_launch(expmc_ctx* c, Staging& S, size_t nitems, uint32_t lane, bool 
             launch_combine_welford(S.d_chunk0, S.d_items, static_cast<uint32_t>(nitems), g0, g1, cp, S.d_totals,
                                    c->stream);
         else
-            launch_combine(S.d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, fem, S.d_totals, c->stream);
+            launch_combine(S.d_chunk0, static_cast<uint32_t>(nitems), g0, g1, cp, fem,
+                           fem || c->sampler != EXPMC_SAMPLER_EVENT, S.d_totals, c->stream);
         c->ctr.kernel_launches += 2;
         c->ctr.sampler_launches += 1;
         c->last_window = w;

@@ -137,7 +137,7 @@ void launch_sampler_welford(const SamplerArgs& a, int grid, int mode, uint32_t l
 void launch_combine_welford(const uint64_t* chunk0, const DevItem* items, uint32_t nitems, uint64_t g_begin,
                             uint64_t g_end, const ChunkPartials& partials, Partial* totals, cudaStream_t s);
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
-                    const ChunkPartials& partials, bool with_extra, Partial* totals, cudaStream_t s);
+                    const ChunkPartials& partials, bool with_extra, bool ordered, Partial* totals, cudaStream_t s);
 void launch_debug(const RowRec* rows, EdgeTables edges, const DevItem* items, uint32_t n,
                   const LaneData& init, SampleOut* out, int mode, uint32_t lane, uint32_t flags, cudaStream_t s);
 constexpr int kSamplerFem = 2;  // sampler_blocks_per_sm: the fem instantiation

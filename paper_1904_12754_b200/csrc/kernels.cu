@@ -248,9 +248,13 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x)
     return x;
 }
 
+// ordered == false (event-driven sampler: statistical parity, no sequential order to keep):
+// each lane sums a strided share of the chunks and a fixed xor tree joins the lanes -- still
+// deterministic and GPU-count independent, without the sequential chain.
 __global__ void __launch_bounds__(kCombWarps * 32) k_combine(const uint64_t* __restrict__ chunk0, uint32_t nitems,
                                                              uint64_t g_begin, uint64_t g_end, ChunkPartials p,
-                                                             bool with_extra, Partial* __restrict__ totals) {
+                                                             bool with_extra, bool ordered,
+                                                             Partial* __restrict__ totals) {
     __shared__ double s_v[kCombWarps][3][kCombTile];
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
     const uint32_t i = blockIdx.x * kCombWarps + w;
@@ -265,7 +269,27 @@ __global__ void __launch_bounds__(kCombWarps * 32) k_combine(const uint64_t* __r
         extra = totals[i].extra;
     }
     unsigned long long cost = 0, jumps = 0;
-    for (uint64_t base = c0; base < c1; base += kCombTile) {
+    if (!ordered) {
+        double ls = 0.0, lq = 0.0, le = 0.0;
+        for (uint64_t g = c0 + lane; g < c1; g += 32) {
+            const uint64_t k = g - g_begin;
+            ls = __dadd_rn(ls, p.sum[k]);
+            lq = __dadd_rn(lq, p.sum_sq[k]);
+            if (with_extra) le = __dadd_rn(le, p.extra[k]);
+            cost += p.cost[k];
+            jumps += p.jumps[k];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ls = __dadd_rn(ls, __shfl_xor_sync(0xFFFFFFFFu, ls, o));
+            lq = __dadd_rn(lq, __shfl_xor_sync(0xFFFFFFFFu, lq, o));
+            if (with_extra) le = __dadd_rn(le, __shfl_xor_sync(0xFFFFFFFFu, le, o));
+        }
+        sum = __dadd_rn(sum, ls);
+        sum_sq = __dadd_rn(sum_sq, lq);
+        extra = __dadd_rn(extra, le);
+    }
+    for (uint64_t base = c0; ordered && base < c1; base += kCombTile) {
         const uint32_t n = static_cast<uint32_t>(c1 - base < kCombTile ? c1 - base : kCombTile);
         for (uint32_t j = lane; j < n; j += 32) {
             const uint64_t k = base + j - g_begin;
@@ -722,9 +746,9 @@ void launch_combine_welford(const uint64_t* chunk0, const DevItem* items, uint32
 }
 
 void launch_combine(const uint64_t* chunk0, uint32_t nitems, uint64_t g_begin, uint64_t g_end,
-                    const ChunkPartials& partials, bool with_extra, Partial* totals, cudaStream_t s) {
+                    const ChunkPartials& partials, bool with_extra, bool ordered, Partial* totals, cudaStream_t s) {
     k_combine<<<grid_for(nitems, kCombWarps), kCombWarps * 32, 0, s>>>(chunk0, nitems, g_begin, g_end, partials,
-                                                                       with_extra, totals);
+                                                                       with_extra, ordered, totals);
     cuda_check(cudaGetLastError(), "k_combine launch");
 }
 
