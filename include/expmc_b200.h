@@ -328,6 +328,9 @@ int expmc_mc_auto(expmc_ctx* ctx, int64_t entry, double beta, double epsilon, ui
 /* Roofline denominator: random 32-B-sector gather throughput of `device` over a buffer of
  * `bytes` (L2-resident or HBM-sized), `loads_per_thread` independent sector loads per thread,
  * best of `reps` launches.  Writes achieved GB/s (32 B per load / kernel time). */
+/* Self-test: out[2i] = the sampler's exp (constant-memory coefficients), out[2i+1] = the
+ * toolkit's exp, for n arguments x (tests: the two must agree bit for bit). */
+int expmc_selftest_exp(int device, int64_t n, const double* x, double* out);
 int expmc_bench_gather(int device, uint64_t bytes, int32_t loads_per_thread, int32_t reps, double* gbps);
 
 /* Host input generators for the BASELINE configs (no GPU needed; csrc/gen.cpp).

@@ -93,6 +93,7 @@ SYMBOLS = [
     ("expmc_ctx_get_sampler", C.c_int, [_P, C.POINTER(_I32)]),
     ("expmc_ctx_set_sampler_flags", C.c_int, [_P, C.c_uint32]),
     ("expmc_bench_gather", C.c_int, [C.c_int, _U64, _I32, _I32, C.POINTER(_D)]),
+    ("expmc_selftest_exp", C.c_int, [C.c_int, _I64, _P, _P]),
     ("expmc_nccl_unique_id", C.c_int, [_P]),
     ("expmc_ctx_shard_samples", C.c_int, [_P, _P, _I32, _I32]),
     ("expmc_ctx_set_shard", C.c_int, [_P, _I32, _I32]),

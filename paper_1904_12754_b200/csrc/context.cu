@@ -933,6 +933,24 @@ int expmc_ctx_get_stream(const expmc_ctx* c, void** stream) {
     });
 }
 
+int expmc_selftest_exp(int device, int64_t n, const double* x, double* out) {
+    return guarded([&] {
+        need(n >= 0 && (n == 0 || (x && out)), EXPMC_EINVAL, "null argument");
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        double* d = nullptr;
+        cuda_check(cudaMalloc(&d, std::max<int64_t>(1, 3 * n) * sizeof(double)), "cudaMalloc");
+        try {
+            cuda_check(cudaMemcpy(d, x, n * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+            math_check(d, n, d + n, nullptr);
+            cuda_check(cudaMemcpy(out, d + n, 2 * n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        } catch (...) {
+            cudaFree(d);
+            throw;
+        }
+        cudaFree(d);
+    });
+}
+
 int expmc_bench_gather(int device, uint64_t bytes, int32_t loads_per_thread, int32_t reps, double* gbps) {
     return guarded([&] {
         need(gbps != nullptr && bytes >= 64 && loads_per_thread > 0 && reps > 0, EXPMC_EINVAL, "bad gather arguments");

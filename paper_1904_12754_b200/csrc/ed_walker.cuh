@@ -139,14 +139,14 @@ __device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic
     const double h = __dmul_rn(0.5, ic.dt);
     if (ic.base) {
         const double expo = __dmul_rn(h, w.acc_a);
-        fine = __dmul_rn(__dmul_rn(sg, expo == 0.0 ? 1.0 : exp(expo)), u_end);
+        fine = __dmul_rn(__dmul_rn(sg, expo == 0.0 ? 1.0 : dexp(expo)), u_end);
         coarse = 0.0;
     } else {
         const double uf = __dmul_rn(sg, u_end);
         const double c = __dmul_rn(h, w.acc_a);
-        const double ec = c == 0.0 ? 1.0 : exp(c);
+        const double ec = c == 0.0 ? 1.0 : dexp(c);
         coarse = __dmul_rn(uf, ec);
-        fine = w.dconst ? coarse : __dmul_rn(uf, exp(__dadd_rn(c, __dmul_rn(h, w.acc_b))));
+        fine = w.dconst ? coarse : __dmul_rn(uf, dexp(__dadd_rn(c, __dmul_rn(h, w.acc_b))));
     }
 }
 
@@ -214,7 +214,7 @@ struct EdPolicy {
         const Row r = load_row(rows, ic.entry);
         if (!(r.rate > 0.0)) return;  // absorbing entry: the full event draws nothing anyway
         // P(no jump before beta) = e^{-rate beta}; M below 2^53 of that, less 2^-30 relative
-        const double m = __dmul_rn(__dmul_rn(exp(-__dmul_rn(r.rate, ic.tend)), 0x1.0p53), 1.0 - 0x1.0p-30);
+        const double m = __dmul_rn(__dmul_rn(dexp(-__dmul_rn(r.rate, ic.tend)), 0x1.0p53), 1.0 - 0x1.0p-30);
         if (!(m >= 2.0)) return;
         EdWalker w;
         w.cur = r;

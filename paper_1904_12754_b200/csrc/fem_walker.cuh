@@ -86,7 +86,7 @@ __device__ __forceinline__ bool fem_event(FemWalker& f, const ItemConst& ic, con
     }
     double e[2];
 #pragma unroll 1
-    for (int k = 0; k < nexp; ++k) e[k] = exp(k == 0 ? x0 : x1);
+    for (int k = 0; k < nexp; ++k) e[k] = dexp(k == 0 ? x0 : x1);
     const double sg = static_cast<double>(w.sign);
     const double g = __ldg(load + w.state);
     if (nexp == 1) {

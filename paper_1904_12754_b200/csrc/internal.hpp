@@ -144,6 +144,7 @@ constexpr int kSamplerFem = 2;  // sampler_blocks_per_sm: the fem instantiation
 int sampler_blocks_per_sm(int mode);
 int sampler_threads();
 
+void math_check(const double* x, int64_t n, double* out /* 2n: dexp, exp */, cudaStream_t s);
 float bench_gather(uint64_t bytes, int loads_per_thread, int reps, int num_sms, uint64_t* total_loads);
 
 // table builder

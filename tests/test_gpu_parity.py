@@ -372,3 +372,22 @@ def test_probability_space_hold_equals_time_space(gpu, oracle_lib, beta):
                     assert np.array_equal(s[k], exp[k]), (entry, level, k)
                 assert ulp_diff(s["fine"], exp["fine"]).max() <= ULP_TOL
                 assert ulp_diff(s["coarse"], exp["coarse"]).max() <= ULP_TOL
+
+
+def test_exp_bitwise_equal_cuda(gpu):
+    # fastmath.cuh exp_fast (constant-memory coefficients) must be the toolkit's exp bit for bit:
+    # random arguments over the sampler's range, the reduction's rounding boundaries (n ln2 / 2),
+    # extremes and specials.
+    import ctypes as C
+    from paper_1904_12754_b200 import _lib as L
+
+    rng = np.random.default_rng(23)
+    x = np.concatenate([rng.uniform(-1, 1, 400_000), rng.uniform(-40, 40, 400_000), rng.uniform(-750, 750, 200_000),
+                        rng.standard_normal(100_000) * 1e-8, (np.arange(-2000, 2000) + 0.5) * math.log(2),
+                        np.nextafter((np.arange(-2000, 2000) + 0.5) * math.log(2), np.inf),
+                        [0.0, -0.0, 1.0, -1.0, 707.99, 708.0, 709.7, 709.8, -708.0, -745.1, -745.2, 1e-320,
+                         np.inf, -np.inf, np.nan]])
+    out = np.empty(2 * len(x))
+    rc = L.lib.expmc_selftest_exp(0, len(x), x.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p))
+    assert rc == 0
+    assert out[0::2].tobytes() == out[1::2].tobytes()
