@@ -59,7 +59,7 @@ __device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const
                                          uint64_t sample) {
     stream_init(w.st, ic.seed, sample, ic.key3);
     const uint32_t s0 = draw_start<F>(w.st, ic, fi);
-    w.cur = load_row(rows, s0);
+    w.cur = F ? load_row(rows, s0) : ic.r0;  // entry mode: the item's row (EdPolicy::prepare)
     w.state = s0;
     w.sign = 1;
     w.dconst = 1u | kFresh;
@@ -210,8 +210,10 @@ struct EdPolicy {
     // The closed-form first hold (header): threshold and stay-at-entry values, once per chunk.
     static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData& ld,
                                                    uint32_t flags) {
-        if (F || (flags & EXPMC_SAMPLER_FLAG_FULL_HOLD)) return;
+        if (F) return;
         const Row r = load_row(rows, ic.entry);
+        ic.r0 = r;
+        if (flags & EXPMC_SAMPLER_FLAG_FULL_HOLD) return;
         if (!(r.rate > 0.0)) return;  // absorbing entry: the full event draws nothing anyway
         // P(no jump before beta) = e^{-rate beta}; M below 2^53 of that, less 2^-30 relative
         const double m = __dmul_rn(__dmul_rn(dexp(-__dmul_rn(r.rate, ic.tend)), 0x1.0p53), 1.0 - 0x1.0p-30);

@@ -219,6 +219,8 @@ struct ItemConst {
     double s0_rate;     // -1: no cached rate
     double s0_hold;
     double smode_max_x; // rate dt below which a fresh step runs in S-mode (-1: T-mode only)
+    Row r0;             // entry mode: the entry's row record and its fresh-step hold (the
+    double h0;          //   restart of every sample reads them from here, not from the tables)
     // event-driven entry mode: closed-form first holding interval (EdPolicy::prepare)
     uint64_t m_safe;    // M = 2^53 - K < m_safe => the path never leaves the entry (0: off)
     double hold_fine;   // that path's (fine, coarse) and run_level sample x
@@ -277,18 +279,20 @@ __device__ __forceinline__ double fresh_hold(const ItemConst& ic, double rate) {
     return x < ic.smode_max_x ? __dmul_rn(dexp(-x), 0x1.0p53) : -ic.dt;
 }
 
-// Per chunk (lane 0): the S0 cache for the entry row's rate; flags may force T-mode.
+// Per chunk (lane 0): the entry row and its fresh-step hold (every sample restarts from them)
+// and the S0 cache for the entry row's rate; flags may force T-mode.
 __device__ __forceinline__ void prepare_hold(ItemConst& ic, const RowRec* __restrict__ rows, uint32_t flags) {
+    ic.r0 = load_row(rows, ic.entry);
     if (flags & EXPMC_SAMPLER_FLAG_LOG_HOLD) {
         ic.smode_max_x = -1.0;
-        return;
+    } else {
+        const double x = __dmul_rn(ic.r0.rate, ic.dt);
+        if (x < ic.smode_max_x) {
+            ic.s0_rate = ic.r0.rate;
+            ic.s0_hold = __dmul_rn(dexp(-x), 0x1.0p53);
+        }
     }
-    const double rate = __ldg(&rows[ic.entry].rate);
-    const double x = __dmul_rn(rate, ic.dt);
-    if (x < ic.smode_max_x) {
-        ic.s0_rate = rate;
-        ic.s0_hold = __dmul_rn(dexp(-x), 0x1.0p53);
-    }
+    ic.h0 = fresh_hold(ic, ic.r0.rate);
 }
 
 template <bool F>
@@ -296,11 +300,16 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
                                              uint64_t sample) {
     stream_init(w.st, ic.seed, sample, ic.key3);
     const uint32_t s0 = draw_start<F>(w.st, ic, fi);
-    w.cur = load_row(rows, s0);  // entry mode: L1-resident, every lane of the warp starts here
+    if (!F) {  // entry mode: the item's cached start (prepare_hold; +3 % on C2)
+        w.cur = ic.r0;
+        w.hold = ic.h0;
+    } else {
+        w.cur = load_row(rows, s0);
+        w.hold = fresh_hold(ic, w.cur.rate);
+    }
     w.state = s0;
     w.sign = 1;
     w.half = 0;
-    w.hold = fresh_hold(ic, w.cur.rate);
     w.acc_a = 0.0;
     w.acc_b = 0.0;
     w.d0 = w.cur.d;  // d1 is written at the pair's middle node before it is read
@@ -434,6 +443,8 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.s0_rate = -1.0;
     ic.s0_hold = 0.0;
     ic.smode_max_x = kSModeMaxX;
+    ic.r0 = Row{0.0, 0.0, 0u, 0u};
+    ic.h0 = 0.0;
     return ic;
 }
 
