@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
                     sum = __dmul_rn(k, hx);
                     sum_sq = __dmul_rn(k, __dmul_rn(hx, hx));
                 }
-                cost += 2ull * nheld * ic.nsteps;  // N rejected draws + N steps each (ed_segment(0, N))
+                cost += static_cast<unsigned long long>(nheld) * ic.nsteps;  // N rejected draws each (ed_segment(0, N))
                 __syncwarp();
             }
         }
@@ -188,7 +188,6 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
                     sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
                     if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
                 }
-                cost += ic.nsteps;
                 const uint32_t mine = next + __popc(fin & lanemask_lt());
                 if (mine < nwork) {
                     my = listed ? wl[mine] : mine;
@@ -214,6 +213,8 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
             }
             __syncwarp();
         }
+        // the fine steps of every sample (cost = draws + steps, paths.hpp:22-23): cnt N, once
+        if (lane == 0) cost += static_cast<unsigned long long>(cnt) * ic.nsteps;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             if constexpr (!W) sum = __dadd_rn(sum, __shfl_xor_sync(full, sum, o));
