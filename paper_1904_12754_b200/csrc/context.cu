@@ -112,11 +112,31 @@ void need(bool ok, int code, const char* msg) {
     if (!ok) throw Status(code, msg);
 }
 
+// Device buffers come from the device's stream-ordered memory pool (cudaMallocAsync /
+// cudaFreeAsync on the context's stream) with the release threshold raised, so a context
+// created after another one was destroyed reuses its blocks: no cudaMalloc / cudaFree (each a
+// device-wide synchronisation, hundreds of ms for GB-sized tables) per context.
+void keep_pool_memory(int device) {
+    static std::mutex m;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> g(m);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return;
+    cudaMemPool_t pool;
+    cuda_check(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+    uint64_t threshold = ~uint64_t{0};
+    cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold), "cudaMemPoolSetAttribute");
+    done.push_back(device);
+}
+
+void dev_free(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
 template <class T>
-void dev_alloc(T** p, size_t count) {
-    if (*p) cudaFree(*p);
+void dev_alloc(T** p, size_t count, cudaStream_t s) {
+    dev_free(*p, s);
     *p = nullptr;
-    cuda_check(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T), s), "cudaMallocAsync");
 }
 
 // Process-wide pool of pinned staging blocks.  Page-locking hundreds of MB (the C2 warm-up round
@@ -161,12 +181,12 @@ void host_alloc(T** p, size_t count, size_t old_count) {
     *p = static_cast<T*>(pinned_get(std::max<size_t>(count, 1) * sizeof(T)));
 }
 
-void ensure_items(Staging& S, size_t nitems) {
+void ensure_items(Staging& S, size_t nitems, cudaStream_t st) {
     if (nitems + 1 > S.cap_items) {
         const size_t cap = std::max<size_t>(nitems + 1, S.cap_items * 2);
-        dev_alloc(&S.d_items, cap);
-        dev_alloc(&S.d_chunk0, cap);
-        dev_alloc(&S.d_totals, cap);
+        dev_alloc(&S.d_items, cap, st);
+        dev_alloc(&S.d_chunk0, cap, st);
+        dev_alloc(&S.d_totals, cap, st);
         S.cap_items = cap;
     }
     if (nitems + 1 > S.cap_h) {
@@ -266,13 +286,13 @@ void ensure_forward_init(expmc_ctx* c) {
         const double edge = std::ldexp(static_cast<double>(k), -static_cast<int>(bits));
         guide[k] = static_cast<uint32_t>(std::upper_bound(cdf.begin(), cdf.end(), edge) - cdf.begin());
     }
-    if (!c->d_init_guide || bits != c->guide_bits) dev_alloc(&c->d_init_guide, nb);
+    if (!c->d_init_guide || bits != c->guide_bits) dev_alloc(&c->d_init_guide, nb, c->stream);
     c->guide_bits = bits;
     cuda_check(cudaMemcpyAsync(c->d_init_guide, guide.data(), nb * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                c->stream),
                "H2D guide");
     c->ctr.h2d_bytes += nb * sizeof(uint32_t);
-    if (!c->d_init_cdf) dev_alloc(&c->d_init_cdf, n);
+    if (!c->d_init_cdf) dev_alloc(&c->d_init_cdf, n, c->stream);
     cuda_check(cudaMemcpyAsync(c->d_init_cdf, cdf.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream),
                "H2D initial CDF");
     cuda_check(cudaStreamSynchronize(c->stream), "H2D initial CDF");
@@ -364,9 +384,9 @@ void sample_launch(expmc_ctx* c, Staging& S, size_t nitems, uint32_t lane, bool 
         const char* wenv = std::getenv("EXPMC_WINDOW_CHUNKS");
         const uint64_t wreq = wenv ? std::strtoull(wenv, nullptr, 10) : 0;
         c->cap_partials = wreq > 0 && wreq <= (kWindowChunks << 4) ? wreq : kWindowChunks;
-        dev_alloc(&c->d_pf, 3 * c->cap_partials);
-        dev_alloc(&c->d_pu, 2 * c->cap_partials);
-        dev_alloc(&c->d_counter, 1);
+        dev_alloc(&c->d_pf, 3 * c->cap_partials, c->stream);
+        dev_alloc(&c->d_pu, 2 * c->cap_partials, c->stream);
+        dev_alloc(&c->d_counter, 1, c->stream);
     }
     const ChunkPartials cp{c->d_pf, c->d_pf + c->cap_partials, c->d_pf + 2 * c->cap_partials, c->d_pu,
                            c->d_pu + c->cap_partials};
@@ -476,7 +496,7 @@ void mc_batch(expmc_ctx* c, uint32_t lane, const expmc_mc_req* req, int64_t nreq
     const size_t nitems = static_cast<size_t>(nreq);
     Staging& S = c->stage[0];
     sample_wait(c, S);
-    ensure_items(S, nitems);
+    ensure_items(S, nitems, c->stream);
     for (size_t k = 0; k < nitems; ++k) {
         const expmc_mc_req& r = req[k];
         DevItem it{};
@@ -546,7 +566,7 @@ void batch_launch(expmc_ctx* c, int s, double beta, uint32_t lane, const expmc_l
     if (forward) ensure_forward_init(c);  // run_level builds it before sampling (mlmc.cpp)
     c->ctr.rounds += 1;
     need(nitems < (size_t{1} << 31), EXPMC_EINVAL, "too many run_level requests in one batch");
-    ensure_items(S, nitems);
+    ensure_items(S, nitems, c->stream);
 #pragma omp parallel for schedule(static)
     for (size_t k = 0; k < nitems; ++k) {
         const expmc_level_req& r = req[S.slot[k]];
@@ -616,9 +636,9 @@ std::vector<SampleOut> sample_debug(expmc_ctx* c, double beta, uint32_t lane, in
     if (lane == EXPMC_LANE_FORWARD) ensure_forward_init(c);
     Staging& S = c->stage[0];
     sample_wait(c, S);
-    ensure_items(S, static_cast<size_t>(nreq));
+    ensure_items(S, static_cast<size_t>(nreq), c->stream);
     if (static_cast<size_t>(nreq) > c->cap_dbg) {
-        dev_alloc(&c->d_dbg, nreq);
+        dev_alloc(&c->d_dbg, nreq, c->stream);
         c->cap_dbg = nreq;
     }
     cuda_check(cudaMemcpyAsync(S.d_items, items.data(), nreq * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
@@ -668,6 +688,7 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
         try {
             c->device = device;
             bind(c);
+            keep_pool_memory(device);
             cuda_check(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
             cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
             c->sampler_grid_ref = c->num_sms * sampler_blocks_per_sm(EXPMC_SAMPLER_REFERENCE);
@@ -684,20 +705,21 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
                 uint32_t* d_heavy = nullptr;
                 void* tmp = nullptr;
                 auto cleanup = [&] {
-                    cudaFree(d_rp); cudaFree(d_col); cudaFree(d_val); cudaFree(d_u);
-                    cudaFree(d_deg); cudaFree(d_begin); cudaFree(d_err); cudaFree(tmp); cudaFree(d_st);
-                    cudaFree(d_heavy);
+                    for (void* p : {static_cast<void*>(d_rp), static_cast<void*>(d_col), static_cast<void*>(d_val),
+                                    static_cast<void*>(d_u), static_cast<void*>(d_deg), static_cast<void*>(d_begin),
+                                    static_cast<void*>(d_err), tmp, static_cast<void*>(d_st), static_cast<void*>(d_heavy)})
+                        dev_free(p, c->stream);
                 };
                 try {
-                    dev_alloc(&d_rp, n + 1);
-                    dev_alloc(&d_col, nnz);
-                    dev_alloc(&d_val, nnz);
-                    dev_alloc(&d_u, n);
-                    dev_alloc(&d_deg, n);
-                    dev_alloc(&d_begin, n);
-                    dev_alloc(&d_err, 2);
-                    dev_alloc(&d_heavy, static_cast<size_t>(std::min<int64_t>(n, nnz / 128 + 1)));
-                    dev_alloc(&d_st, 2);
+                    dev_alloc(&d_rp, n + 1, c->stream);
+                    dev_alloc(&d_col, nnz, c->stream);
+                    dev_alloc(&d_val, nnz, c->stream);
+                    dev_alloc(&d_u, n, c->stream);
+                    dev_alloc(&d_deg, n, c->stream);
+                    dev_alloc(&d_begin, n, c->stream);
+                    dev_alloc(&d_err, 2, c->stream);
+                    dev_alloc(&d_heavy, static_cast<size_t>(std::min<int64_t>(n, nnz / 128 + 1)), c->stream);
+                    dev_alloc(&d_st, 2, c->stream);
                     cuda_check(cudaMemcpyAsync(d_rp, A->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream), "H2D");
                     if (nnz) {
                         cuda_check(cudaMemcpyAsync(d_col, A->col, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream), "H2D");
@@ -714,7 +736,7 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
                     need(!(err & 1u), EXPMC_EINVAL, "matrix entry is NaN or Inf");
                     need(!(err & 4u), EXPMC_EINVAL, "CSR is not canonical (sorted, duplicate-free columns)");
                     const size_t tb = std::max(scan_temp_bytes(n), dstat_temp_bytes(n));
-                    cuda_check(cudaMalloc(&tmp, tb), "cudaMalloc");
+                    cuda_check(cudaMallocAsync(&tmp, tb, c->stream), "cudaMallocAsync");
                     exclusive_scan_u64(d_deg, d_begin, n, tmp, tb, c->stream);
                     uint64_t last[2];
                     cuda_check(cudaMemcpyAsync(&last[0], d_begin + (n - 1), 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
@@ -722,9 +744,9 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
                     cuda_check(cudaStreamSynchronize(c->stream), "scan");
                     c->nedges = last[0] + last[1];
                     need(c->nedges < (uint64_t{1} << 32), EXPMC_EINVAL, "more than 2^32 chain edges");
-                    dev_alloc(&c->rows, n);
-                    dev_alloc(&c->cdf, c->nedges);
-                    dev_alloc(&c->tgt, c->nedges);
+                    dev_alloc(&c->rows, n, c->stream);
+                    dev_alloc(&c->cdf, c->nedges, c->stream);
+                    dev_alloc(&c->tgt, c->nedges, c->stream);
                     launch_fill_tables(n, d_rp, d_col, d_val, d_u, d_begin, c->rows, c->cdf, c->tgt, d_heavy, d_err + 1,
                                        c->num_sms, c->stream);
                     d_stats(c->rows, n, d_st, tmp, tb, c->stream);
@@ -752,31 +774,29 @@ int expmc_ctx_create(const expmc_csr* A, const double* u, int device, expmc_ctx*
 void expmc_ctx_destroy(expmc_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    if (c->stream) cudaStreamSynchronize(c->stream);
-    cudaFree(c->rows);
-    cudaFree(c->cdf);
-    cudaFree(c->tgt);
+    cudaStream_t st = c->stream;
     for (Staging& S : c->stage) {
-        cudaFree(S.d_items);
-        cudaFree(S.d_chunk0);
-        cudaFree(S.d_totals);
+        dev_free(S.d_items, st);
+        dev_free(S.d_chunk0, st);
+        dev_free(S.d_totals, st);
         if (S.cap_h) {  // staging blocks go back to the process-wide pool
             pinned_put(S.h_items, S.cap_h * sizeof(DevItem));
             pinned_put(S.h_chunk0, S.cap_h * sizeof(uint64_t));
             pinned_put(S.h_totals, S.cap_h * sizeof(Partial));
         }
+    }
+    for (void* p : {static_cast<void*>(c->rows), static_cast<void*>(c->cdf), static_cast<void*>(c->tgt),
+                    static_cast<void*>(c->d_pf), static_cast<void*>(c->d_pu), static_cast<void*>(c->d_counter),
+                    static_cast<void*>(c->d_init_cdf), static_cast<void*>(c->d_init_guide),
+                    static_cast<void*>(c->d_load), static_cast<void*>(c->d_dbg)})
+        dev_free(p, st);  // back to the device pool, in stream order
+    if (st) cudaStreamSynchronize(st);
+    for (Staging& S : c->stage) {
         for (cudaEvent_t e : S.ev) cudaEventDestroy(e);
         if (S.done) cudaEventDestroy(S.done);
     }
-    cudaFree(c->d_pf);
-    cudaFree(c->d_pu);
     if (c->nccl) nccl().comm_destroy(c->nccl);
-    cudaFree(c->d_counter);
-    cudaFree(c->d_init_cdf);
-    cudaFree(c->d_init_guide);
-    cudaFree(c->d_load);
-    cudaFree(c->d_dbg);
-    if (c->stream) cudaStreamDestroy(c->stream);
+    if (st) cudaStreamDestroy(st);
     delete c;
 }
 
@@ -799,13 +819,13 @@ int expmc_ctx_set_vector(expmc_ctx* c, const double* u) {
         if (c->n == 0) return;
         bind(c);
         double* d_u = nullptr;
-        dev_alloc(&d_u, c->n);
+        dev_alloc(&d_u, c->n, c->stream);
         cuda_check(cudaMemcpyAsync(d_u, u, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
         launch_set_vector(c->n, d_u, c->rows, c->stream);
         c->ctr.h2d_bytes += c->n * 8;
         c->ctr.kernel_launches += 1;
         cudaError_t e = cudaStreamSynchronize(c->stream);
-        cudaFree(d_u);
+        dev_free(d_u, c->stream);
         c->init_valid = false;  // the forward CDF follows u
         cuda_check(e, "set vector");
     });
@@ -821,8 +841,8 @@ int expmc_ctx_export_tables(const expmc_ctx* c, double* d, double* rate, int64_t
         double *dd = nullptr, *dr = nullptr, *dc = nullptr;
         int64_t *drp = nullptr, *dt = nullptr;
         uint8_t* ds = nullptr;
-        dev_alloc(&dd, n); dev_alloc(&dr, n); dev_alloc(&drp, n + 1);
-        dev_alloc(&dc, m); dev_alloc(&dt, m); dev_alloc(&ds, m);
+        dev_alloc(&dd, n, c->stream); dev_alloc(&dr, n, c->stream); dev_alloc(&drp, n + 1, c->stream);
+        dev_alloc(&dc, m, c->stream); dev_alloc(&dt, m, c->stream); dev_alloc(&ds, m, c->stream);
         launch_export(n, c->rows, dd, dr, drp, c->stream);
         launch_export_edges(m, c->edges(), dc, dt, ds, c->stream);
         cudaError_t e = cudaStreamSynchronize(c->stream);
@@ -835,7 +855,9 @@ int expmc_ctx_export_tables(const expmc_ctx* c, double* d, double* rate, int64_t
         if (e == cudaSuccess && cdf) e = cudaMemcpy(cdf, dc, m * 8, cudaMemcpyDeviceToHost);
         if (e == cudaSuccess && target) e = cudaMemcpy(target, dt, m * 8, cudaMemcpyDeviceToHost);
         if (e == cudaSuccess && sign) e = cudaMemcpy(sign, ds, m, cudaMemcpyDeviceToHost);
-        cudaFree(dd); cudaFree(dr); cudaFree(drp); cudaFree(dc); cudaFree(dt); cudaFree(ds);
+        for (void* p : {static_cast<void*>(dd), static_cast<void*>(dr), static_cast<void*>(drp), static_cast<void*>(dc),
+                        static_cast<void*>(dt), static_cast<void*>(ds)})
+            dev_free(p, c->stream);
         cuda_check(e, "export tables");
     });
 }
@@ -1037,7 +1059,7 @@ int expmc_ctx_set_load(expmc_ctx* c, const double* load) {
         need(c && (load || c->n == 0), EXPMC_EINVAL, "null argument");
         if (c->n == 0) return;
         bind(c);
-        if (!c->d_load) dev_alloc(&c->d_load, c->n);
+        if (!c->d_load) dev_alloc(&c->d_load, c->n, c->stream);
         cuda_check(cudaMemcpyAsync(c->d_load, load, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "H2D");
         c->ctr.h2d_bytes += c->n * sizeof(double);
         cuda_check(cudaStreamSynchronize(c->stream), "set load");
