@@ -366,7 +366,10 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
                                              const EdgeTables& edges, const LogEntry* s_log,
                                              unsigned long long& draws, unsigned long long& jumps) {
     if (!walker_hold(w, rows, edges, s_log, draws, jumps)) return false;
-    // ---- the fine step ended in w.state
+    // The sample's last step ends it; its sums are taken by walker_finish / walker_sample, in
+    // the finishing lanes' own divergent section (level-0 chunks: no step-end section at all).
+    if (w.step + 1 == ic.nsteps) return true;
+    // ---- a non-final fine step ended in w.state
     const double dn = w.cur.d;
     if (ic.base) {
         // expo += dt_ * 0.5 * (d[s0] + d[state])                             paths.cpp:110
@@ -384,9 +387,25 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
         w.d0 = dn;
         w.half = 0u;
     }
-    if (++w.step == ic.nsteps) return true;
+    ++w.step;
     w.hold = fresh_hold(ic, w.cur.rate);  // next fine step: fresh holding interval of length dt (paths.cpp:95-96)
     return false;
+}
+
+// The last step's sums, the same operations walker_event applies to every other step:
+// single: expo + dt_ 0.5 (d[s0] + d[end]) (paths.cpp:110); coupled (the last step closes a pair):
+// coarse + dt (d0 + d2), delta + dt (d1 - 0.5 (d0 + d2)) (paths.cpp:134-136).
+__device__ __forceinline__ void last_step_sums(const Walker& w, const ItemConst& ic, double& a, double& b) {
+    const double dn = w.cur.d;
+    if (ic.base) {
+        a = __dadd_rn(w.acc_a, __dmul_rn(ic.half_dt, __dadd_rn(w.d0, dn)));
+        b = w.acc_b;
+    } else {
+        const double s02 = __dadd_rn(w.d0, dn);
+        const double half_ends = __dmul_rn(0.5, s02);
+        a = __dadd_rn(w.acc_a, __dmul_rn(ic.dt, s02));
+        b = __dadd_rn(w.acc_b, __dmul_rn(ic.dt, __dsub_rn(w.d1, half_ends)));
+    }
 }
 
 // exp(x) with the exact shortcut exp(0) = 1 (both libms return exactly 1): rows whose d is
@@ -398,15 +417,17 @@ __device__ __forceinline__ double exp_or_one(double x) { return x == 0.0 ? 1.0 :
 template <bool F>
 __device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                               double& fine, double& coarse) {
+    double acc_a, acc_b;
+    last_step_sums(w, ic, acc_a, acc_b);
     const double sg = static_cast<double>(w.sign);
     const double u_end = terminal_factor<F>(ic, fi, rows, w.state);  // same sector as the last row record read
     if (ic.base) {
-        fine = __dmul_rn(__dmul_rn(sg, exp_or_one(w.acc_a)), u_end);
+        fine = __dmul_rn(__dmul_rn(sg, exp_or_one(acc_a)), u_end);
         coarse = 0.0;
     } else {
         const double uf = __dmul_rn(sg, u_end);
-        fine = __dmul_rn(uf, exp_or_one(__dadd_rn(w.acc_a, w.acc_b)));
-        coarse = __dmul_rn(uf, exp_or_one(w.acc_a));
+        fine = __dmul_rn(uf, exp_or_one(__dadd_rn(acc_a, acc_b)));
+        coarse = __dmul_rn(uf, exp_or_one(acc_a));
     }
 }
 
@@ -414,14 +435,16 @@ __device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& 
 // it (mlmc.cpp:103-108).  delta == 0 makes fine and coarse bitwise equal, so x = 0 exactly.
 template <bool F>
 __device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows) {
-    if (!ic.base && w.acc_b == 0.0) return 0.0;
+    double acc_a, acc_b;
+    last_step_sums(w, ic, acc_a, acc_b);
+    if (!ic.base && acc_b == 0.0) return 0.0;
     // same values as walker_finish, with one exp call site shared by both modes
     const double sg = static_cast<double>(w.sign);
     const double u_end = terminal_factor<F>(ic, fi, rows, w.state);
-    const double ea = exp_or_one(w.acc_a);  // single: e^expo; coupled: e^coarse
+    const double ea = exp_or_one(acc_a);  // single: e^expo; coupled: e^coarse
     if (ic.base) return __dmul_rn(__dmul_rn(sg, ea), u_end);
     const double uf = __dmul_rn(sg, u_end);
-    return __dsub_rn(__dmul_rn(uf, dexp(__dadd_rn(w.acc_a, w.acc_b))), __dmul_rn(uf, ea));
+    return __dsub_rn(__dmul_rn(uf, dexp(__dadd_rn(acc_a, acc_b))), __dmul_rn(uf, ea));
 }
 
 __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items, uint32_t i) {
