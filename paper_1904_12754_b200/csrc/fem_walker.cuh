@@ -57,7 +57,7 @@ __device__ __forceinline__ bool fem_event(FemWalker& f, const ItemConst& ic, con
     Walker& w = f.w;
     if (!walker_hold(w, rows, edges, s_log, draws, jumps)) return false;
     const double dn = w.cur.d;
-    const uint64_t j = w.step + 1;  // fine node index of the step that just ended
+    const uint64_t j = ic.nsteps - w.left + 1;  // fine node index of the step that just ended
     // exponents of this node
     //   base:      expo += dt_ * 0.5 * (d[s0] + d[state])                       paths.cpp:198
     //   pair mid:  mid = coarse + delta + dt_ * 0.5 * (d[s0] + d[s1])          paths.cpp:230
@@ -105,7 +105,7 @@ __device__ __forceinline__ bool fem_event(FemWalker& f, const ItemConst& ic, con
         f.e0 = e[0];
         f.e1 = e[1];
     }
-    if (++w.step == ic.nsteps) return true;
+    if (--w.left == 0) return true;
     w.hold = fresh_hold(ic, w.cur.rate);
     return false;
 }

@@ -269,7 +269,8 @@ struct Walker {
     double hold;           // S-mode (> 0): e^{-rate*remaining} 2^53; T-mode (<= 0): -remaining
     double acc_a, acc_b;   // single: expo; coupled: coarse, delta
     double d0, d1;         // d[s0], d[s1]
-    uint64_t step;         // completed fine steps
+    uint64_t left;         // fine steps not yet completed, the current one included (counts down:
+                           //   the step-end test needs no item constant)
 };
 
 // Start value of a fresh fine step in a row of the given rate (paths.cpp:95-96).
@@ -313,7 +314,7 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
     w.acc_a = 0.0;
     w.acc_b = 0.0;
     w.d0 = w.cur.d;  // d1 is written at the pair's middle node before it is read
-    w.step = 0;
+    w.left = ic.nsteps;
 }
 
 // One pass of evolve_common's for(;;) body (paths.cpp:48-69): the holding-interval test and,
@@ -368,7 +369,7 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
     if (!walker_hold(w, rows, edges, s_log, draws, jumps)) return false;
     // The sample's last step ends it; its sums are taken by walker_finish / walker_sample, in
     // the finishing lanes' own divergent section (level-0 chunks: no step-end section at all).
-    if (w.step + 1 == ic.nsteps) return true;
+    if (w.left == 1u) return true;
     // ---- a non-final fine step ended in w.state
     const double dn = w.cur.d;
     if (ic.base) {
@@ -387,7 +388,7 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
         w.d0 = dn;
         w.half = 0u;
     }
-    ++w.step;
+    --w.left;
     w.hold = fresh_hold(ic, w.cur.rate);  // next fine step: fresh holding interval of length dt (paths.cpp:95-96)
     return false;
 }
