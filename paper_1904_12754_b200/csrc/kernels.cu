@@ -234,6 +234,129 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
     }
 }
 
+// Screened event sampler, chunk groups (EdPolicy<false>, sums): a warp claims kGroup consecutive
+// chunks of its window and screens all of an item's chunks in the group before it runs the
+// walker loop, so the few samples that jump (5-10 % on C3/C4) fill the lanes of one walker pass
+// instead of a fraction of 32 per chunk.  The portion's totals go to its first chunk's partial
+// and the other chunks of the portion get zeros; the event sampler's combine is an unordered
+// sum, so the item totals are the same terms (determinism: the group boundaries are fixed and
+// the lane assignment is the ballot's, as in k_sample).
+constexpr uint32_t kGroup = 4;
+
+template <class P>
+__global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(SamplerArgs a) {
+    static_assert(P::kScreen && !P::kExtra, "grouped chunks: screened policies only");
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t wid = threadIdx.x >> 5;
+    const unsigned full = 0xFFFFFFFFu;
+    __shared__ uint16_t s_list[kWarps * kGroup * kChunk];  // (group slot << 9) | offset in chunk
+    uint16_t* const wl = s_list + wid * kGroup * kChunk;
+    __shared__ uint64_t s_lo[kWarps][kGroup];              // first sample of each group slot
+    __shared__ LogEntry s_log[128];
+    load_log_table(s_log);
+    __syncthreads();
+    __shared__ ItemConst s_ic[kWarps];
+    ItemConst& ic = s_ic[wid];
+    uint32_t hint = 0;
+    const uint64_t rem = a.g_begin % a.shard_world;
+    const uint64_t own0 = a.g_begin + (a.shard_rank + a.shard_world - rem) % a.shard_world;
+    for (;;) {
+        uint32_t gi = 0;
+        if (lane == 0) gi = atomicAdd(a.counter, 1u);
+        gi = __shfl_sync(full, gi, 0);
+        const uint64_t k0 = static_cast<uint64_t>(gi) * kGroup;
+        if (own0 + k0 * a.shard_world >= a.g_end) return;
+        uint32_t j = 0;
+        while (j < kGroup) {
+            const uint64_t gp = own0 + (k0 + j) * a.shard_world;  // first chunk of this portion
+            if (gp >= a.g_end) break;
+            const uint32_t item = find_item(a.chunk0, a.nitems, gp, hint);
+            hint = item;
+            if (lane == 0) {
+                ItemConst c = load_item(a.items, item);
+                P::prepare(c, a.rows, a.init, a.flags);
+                ic = c;
+            }
+            __syncwarp();
+            const DevItem& it = a.items[item];
+            const uint64_t first = it.first, end = it.first + it.count;
+            const uint64_t item_g1 = a.chunk0[item + 1];
+            // ---- screen the portion: the group's chunks of this item
+            const uint32_t j0 = j;
+            uint32_t nwork = 0, nheld = 0;
+            unsigned long long nsamp = 0;
+            for (; j < kGroup; ++j) {
+                const uint64_t g = own0 + (k0 + j) * a.shard_world;
+                if (g >= a.g_end || g >= item_g1) break;
+                const uint64_t chunk = first / kChunk + (g - a.chunk0[item]);
+                const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
+                const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
+                const uint32_t cnt = hi > lo ? static_cast<uint32_t>(hi - lo) : 0u;  // parallel.hpp:46-49
+                if (lane == 0) s_lo[wid][j] = lo;
+                nsamp += cnt;
+                for (uint32_t q0 = 0; q0 < cnt; q0 += 32u) {
+                    const uint32_t q = q0 + lane;
+                    const bool valid = q < cnt;
+                    const bool held = valid && ic.m_safe != 0 && P::screen(ic, lo + q);
+                    nheld += held;
+                    const unsigned need = __ballot_sync(full, valid && !held);
+                    if (valid && !held) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>((j << 9) | q);
+                    nwork += __popc(need);
+                }
+            }
+            __syncwarp();
+            // ---- the walker loop over the listed samples (k_sample's, entries decoded)
+            const double hx = ic.hold_x, kh = static_cast<double>(nheld);
+            double sum = __dmul_rn(kh, hx), sum_sq = __dmul_rn(kh, __dmul_rn(hx, hx));
+            unsigned long long cost = static_cast<unsigned long long>(nheld) * ic.nsteps, jumps = 0;
+            typename P::W w;
+            bool active = false;
+            if (lane < nwork) {
+                const uint32_t e = wl[lane];
+                P::start(w, ic, a.init, a.rows, s_lo[wid][e >> 9] + (e & 511u));
+                active = true;
+            }
+            uint32_t next = nwork < 32u ? nwork : 32u;
+            while (__any_sync(full, active)) {
+                const bool done = active && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps);
+                const unsigned fin = __ballot_sync(full, done);
+                if (done) {
+                    double ex;
+                    const double x = P::sample(w, ic, a.init, a.rows, ex);
+                    sum = __dadd_rn(sum, x);
+                    sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
+                    const uint32_t mine = next + __popc(fin & lanemask_lt());
+                    if (mine < nwork) {
+                        const uint32_t e = wl[mine];
+                        P::start(w, ic, a.init, a.rows, s_lo[wid][e >> 9] + (e & 511u));
+                    } else {
+                        active = false;
+                    }
+                }
+                next += __popc(fin);
+            }
+            if (lane == 0) cost += nsamp * ic.nsteps;  // the fine steps of every sample
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                sum = __dadd_rn(sum, __shfl_xor_sync(full, sum, o));
+                sum_sq = __dadd_rn(sum_sq, __shfl_xor_sync(full, sum_sq, o));
+                cost += __shfl_xor_sync(full, cost, o);
+                jumps += __shfl_xor_sync(full, jumps, o);
+            }
+            // portion totals on its first chunk, zeros on the rest
+            for (uint32_t t = j0 + lane; t < j; t += 32u) {
+                const uint64_t k = own0 + (k0 + t) * a.shard_world - a.g_begin;
+                const bool head = t == j0;
+                a.partials.sum[k] = head ? sum : 0.0;
+                a.partials.sum_sq[k] = head ? sum_sq : 0.0;
+                a.partials.cost[k] = head ? cost : 0ull;
+                a.partials.jumps[k] = head ? jumps : 0ull;
+            }
+            __syncwarp();  // ic and the list are rewritten by the next portion
+        }
+    }
+}
+
 // Ordered combines: one warp per item.  The fp64 sums must be taken in ascending chunk order
 // (one dependent add per chunk), so the warp stages tiles of the item's chunk partials in
 // shared memory with coalesced loads (32 in flight per lane group) and lane 0 runs the
@@ -709,7 +832,7 @@ int sampler_blocks_per_sm(int mode) {
     if (mode == kSamplerFem)
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<FemPolicy, false>, kThreads, 0), "occupancy");
     else if (mode == EXPMC_SAMPLER_EVENT)
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<EdPolicy<false>, false>, kThreads, 0),
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_grouped<EdPolicy<false>>, kThreads, 0),
                    "occupancy");
     else
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<RefPolicy<false>, false>, kThreads, 0),
@@ -730,7 +853,8 @@ void launch_sampler_t(const SamplerArgs& a, int grid, int mode, uint32_t lane, c
     }
     if (mode == EXPMC_SAMPLER_EVENT) {
         if (lane == EXPMC_LANE_FORWARD) k_sample<EdPolicy<true>, W><<<grid, kThreads, 0, s>>>(a);
-        else k_sample<EdPolicy<false>, W><<<grid, kThreads, 0, s>>>(a);
+        else if constexpr (W) k_sample<EdPolicy<false>, W><<<grid, kThreads, 0, s>>>(a);
+        else k_sample_grouped<EdPolicy<false>><<<grid, kThreads, 0, s>>>(a);
     } else {
         if (lane == EXPMC_LANE_FORWARD) k_sample<RefPolicy<true>, W><<<grid, kThreads, 0, s>>>(a);
         else k_sample<RefPolicy<false>, W><<<grid, kThreads, 0, s>>>(a);
