@@ -241,7 +241,10 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
 // and the other chunks of the portion get zeros; the event sampler's combine is an unordered
 // sum, so the item totals are the same terms (determinism: the group boundaries are fixed and
 // the lane assignment is the ballot's, as in k_sample).
-constexpr uint32_t kGroup = 4;
+#ifndef EXPMC_GROUP
+#define EXPMC_GROUP 4
+#endif
+constexpr uint32_t kGroup = EXPMC_GROUP;
 
 template <class P>
 __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(SamplerArgs a) {
