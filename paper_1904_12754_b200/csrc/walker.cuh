@@ -221,6 +221,8 @@ struct ItemConst {
     double smode_max_x; // rate dt below which a fresh step runs in S-mode (-1: T-mode only)
     Row r0;             // entry mode: the entry's row record and its fresh-step hold (the
     double h0;          //   restart of every sample reads them from here, not from the tables)
+    double ea_key;      // base level: e^{ea_key} = ea_val, the exponent of a path that keeps the
+    double ea_val;      //   entry's d (every interior path of C5) -- one exp per chunk, not per sample
     // event-driven entry mode: closed-form first holding interval (EdPolicy::prepare)
     uint64_t m_safe;    // M = 2^53 - K < m_safe => the path never leaves the entry (0: off)
     double hold_fine;   // that path's (fine, coarse) and run_level sample x
@@ -294,6 +296,12 @@ __device__ __forceinline__ void prepare_hold(ItemConst& ic, const RowRec* __rest
         }
     }
     ic.h0 = fresh_hold(ic, ic.r0.rate);
+    if (ic.base && ic.nsteps <= 64u) {  // walker_event / last_step_sums on a constant-d path
+        double a = 0.0;
+        for (uint64_t k = 0; k < ic.nsteps; ++k) a = __dadd_rn(a, __dmul_rn(ic.half_dt, __dadd_rn(ic.r0.d, ic.r0.d)));
+        ic.ea_key = a;
+        ic.ea_val = a == 0.0 ? 1.0 : dexp(a);
+    }
 }
 
 template <bool F>
@@ -423,7 +431,7 @@ __device__ __forceinline__ void walker_finish(const Walker& w, const ItemConst& 
     const double sg = static_cast<double>(w.sign);
     const double u_end = terminal_factor<F>(ic, fi, rows, w.state);  // same sector as the last row record read
     if (ic.base) {
-        fine = __dmul_rn(__dmul_rn(sg, exp_or_one(acc_a)), u_end);
+        fine = __dmul_rn(__dmul_rn(sg, acc_a == ic.ea_key ? ic.ea_val : exp_or_one(acc_a)), u_end);
         coarse = 0.0;
     } else {
         const double uf = __dmul_rn(sg, u_end);
@@ -442,7 +450,8 @@ __device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst
     // same values as walker_finish, with one exp call site shared by both modes
     const double sg = static_cast<double>(w.sign);
     const double u_end = terminal_factor<F>(ic, fi, rows, w.state);
-    const double ea = exp_or_one(acc_a);  // single: e^expo; coupled: e^coarse
+    // single: e^expo (the item's cached value when the path kept the entry's d); coupled: e^coarse
+    const double ea = ic.base && acc_a == ic.ea_key ? ic.ea_val : exp_or_one(acc_a);
     if (ic.base) return __dmul_rn(__dmul_rn(sg, ea), u_end);
     const double uf = __dmul_rn(sg, u_end);
     return __dsub_rn(__dmul_rn(uf, dexp(__dadd_rn(acc_a, acc_b))), __dmul_rn(uf, ea));
@@ -469,6 +478,8 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.smode_max_x = kSModeMaxX;
     ic.r0 = Row{0.0, 0.0, 0u, 0u};
     ic.h0 = 0.0;
+    ic.ea_key = 0.0;  // exp_or_one(0) = 1
+    ic.ea_val = 1.0;
     return ic;
 }
 
