@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
     }
 }
 
-// Screened event sampler, chunk groups (EdPolicy<false>, sums): a warp claims kGroup consecutive
-// chunks of its window and screens all of an item's chunks in the group before it runs the
+// Screened event sampler, chunk groups (EdPolicy<false>, sums): a warp claims an aligned group
+// of kGroup consecutive chunks of its window and screens all of an item's chunks in the group before it runs the
 // walker loop, so the few samples that jump (5-10 % on C3/C4) fill the lanes of one walker pass
 // instead of a fraction of 32 per chunk.  The portion's totals go to its first chunk's partial
 // and the other chunks of the portion get zeros; the event sampler's combine is an unordered
@@ -261,18 +261,24 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(Samp
     __shared__ ItemConst s_ic[kWarps];
     ItemConst& ic = s_ic[wid];
     uint32_t hint = 0;
-    const uint64_t rem = a.g_begin % a.shard_world;
-    const uint64_t own0 = a.g_begin + (a.shard_rank + a.shard_world - rem) % a.shard_world;
+    // Groups are aligned blocks of kGroup absolute chunk ids, dealt to the ranks of a sample-
+    // sharded run whole (group q on rank q % world): the portions -- and so every chunk
+    // partial -- are the same for any GPU count, and the all-reduced window is the one-GPU one.
+    const uint64_t q_begin = a.g_begin / kGroup;
+    const uint64_t qrem = q_begin % a.shard_world;
+    const uint64_t qown = q_begin + (a.shard_rank + a.shard_world - qrem) % a.shard_world;
     for (;;) {
         uint32_t gi = 0;
         if (lane == 0) gi = atomicAdd(a.counter, 1u);
         gi = __shfl_sync(full, gi, 0);
-        const uint64_t k0 = static_cast<uint64_t>(gi) * kGroup;
-        if (own0 + k0 * a.shard_world >= a.g_end) return;
-        uint32_t j = 0;
-        while (j < kGroup) {
-            const uint64_t gp = own0 + (k0 + j) * a.shard_world;  // first chunk of this portion
-            if (gp >= a.g_end) break;
+        const uint64_t q = qown + static_cast<uint64_t>(gi) * a.shard_world;
+        const uint64_t gq = q * kGroup;  // first chunk id of the group
+        if (gq >= a.g_end) return;
+        const uint64_t glo = gq > a.g_begin ? gq : a.g_begin;
+        const uint64_t ghi = gq + kGroup < a.g_end ? gq + kGroup : a.g_end;
+        uint32_t j = static_cast<uint32_t>(glo - gq);
+        while (gq + j < ghi) {
+            const uint64_t gp = gq + j;  // first chunk of this portion
             const uint32_t item = find_item(a.chunk0, a.nitems, gp, hint);
             hint = item;
             if (lane == 0) {
@@ -288,9 +294,9 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(Samp
             const uint32_t j0 = j;
             uint32_t nwork = 0, nheld = 0;
             unsigned long long nsamp = 0;
-            for (; j < kGroup; ++j) {
-                const uint64_t g = own0 + (k0 + j) * a.shard_world;
-                if (g >= a.g_end || g >= item_g1) break;
+            for (; gq + j < ghi; ++j) {
+                const uint64_t g = gq + j;
+                if (g >= item_g1) break;
                 const uint64_t chunk = first / kChunk + (g - a.chunk0[item]);
                 const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
                 const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
@@ -298,12 +304,12 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(Samp
                 if (lane == 0) s_lo[wid][j] = lo;
                 nsamp += cnt;
                 for (uint32_t q0 = 0; q0 < cnt; q0 += 32u) {
-                    const uint32_t q = q0 + lane;
-                    const bool valid = q < cnt;
-                    const bool held = valid && ic.m_safe != 0 && P::screen(ic, lo + q);
+                    const uint32_t qq = q0 + lane;
+                    const bool valid = qq < cnt;
+                    const bool held = valid && ic.m_safe != 0 && P::screen(ic, lo + qq);
                     nheld += held;
                     const unsigned need = __ballot_sync(full, valid && !held);
-                    if (valid && !held) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>((j << 9) | q);
+                    if (valid && !held) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>((j << 9) | qq);
                     nwork += __popc(need);
                 }
             }
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(Samp
             }
             // portion totals on its first chunk, zeros on the rest
             for (uint32_t t = j0 + lane; t < j; t += 32u) {
-                const uint64_t k = own0 + (k0 + t) * a.shard_world - a.g_begin;
+                const uint64_t k = gq + t - a.g_begin;
                 const bool head = t == j0;
                 a.partials.sum[k] = head ? sum : 0.0;
                 a.partials.sum_sq[k] = head ? sum_sq : 0.0;

@@ -60,3 +60,32 @@ def test_nccl_world_one_is_identity(gpu):
         r2, _ = P.mlmc_driver_rows(ctx2, cfg.beta, rows, configs.row_seeds(rows), P.MlmcOptions(epsilon=1e-2))
     assert a.tobytes() == b.tobytes()
     assert r1.tobytes() == r2.tobytes()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_ranks_event_sampler_groups(gpu, world):
+    # k_sample_grouped deals aligned chunk groups to ranks whole, so each rank's window holds
+    # exactly the one-GPU partials of its groups (zeros elsewhere): the elementwise sum over the
+    # emulated ranks is the unsharded window bit for bit, and the item totals follow.
+    cfg = configs.make_config("c3-20000")
+    with P.Context(cfg.a, cfg.u, sampler="event") as ctx:
+        entries = np.array([0, 5, 77, 1234, 19999])
+        levels = np.array([7, 8, 9, 7, 10])
+        args = (cfg.beta, entries, levels, (levels == 7).astype(np.int32), [0, 100, 3, 512, 9],
+                [300000, 70000, 20000, 4096, 9000], 1000 + entries)
+        full = ctx.run_level_batch(*args)
+        ref = ctx.last_partials()
+        parts, outs = [], []
+        for r in range(world):
+            ctx.set_shard(r, world)
+            outs.append(ctx.run_level_batch(*args))
+            parts.append(ctx.last_partials())
+        ctx.set_shard(0, 1)
+    for k in ("sum", "sum_sq"):
+        tot = np.zeros_like(ref[k])
+        for p in parts:
+            tot = tot + p[k]
+        assert tot.tobytes() == ref[k].tobytes(), k
+    for k in ("cost", "jumps"):
+        assert np.array_equal(sum(p[k] for p in parts), ref[k])
+    assert full["cost"].sum() == ref["cost"].sum()
