@@ -140,7 +140,12 @@ __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begi
     const uint32_t deg = degf & kDegMask;
     uint32_t k = 0;
     bool done = false;
-    if (degf & kUniformRow) {
+    if ((degf & kUniformRow) && (deg & (deg - 1u)) == 0u) {
+        // power-of-two degree 2^p (every interior row of a 2-D Laplacian: 4): cdf_j = (j+1) 2^-p
+        // and v 2^p = K 2^(p-53) are exact, so upper_bound = K >> (53 - p), no boundary case
+        k = static_cast<uint32_t>(k53 >> (53 - (31 - __clz(deg))));
+        done = true;
+    } else if (degf & kUniformRow) {
 #ifdef EXPMC_PICK_INT
         const uint64_t lo = k53 * deg;
         const uint64_t hi = __umul64hi(k53, static_cast<uint64_t>(deg));
