@@ -9,11 +9,13 @@
 //                path length, not the longest path.  The chunk's (sum, sum_sq, cost, jumps)
 //                is reduced with a fixed xor-shuffle tree -> deterministic, independent of
 //                grid size, GPU count and scheduling.
+//  k_sample_grouped -- the event sampler's entry-mode variant: closed-form samples screened
+//                out over groups of 4 chunks, one walker pass over the rest (ed_walker.cuh).
 //  k_combine  -- per-item ordered combine of the chunk partials (SumAcc::combine in
-//                ascending chunk order, parallel.hpp:52).
+//                ascending chunk order, parallel.hpp:52); a tree for event-sampler batches.
 //  k_debug    -- one thread per requested sample (golden per-sample parity).
-//  k_count_edges / k_fill_tables -- the transition-table builder (decompose_impl,
-//                chain.cpp:15-71) straight from CSR on the device.
+//  k_count_edges / k_fill_tables (+ _heavy: hub rows, a warp each) -- the transition-table
+//                builder (decompose_impl, chain.cpp:15-71) straight from CSR on the device.
 #include <cub/device/device_scan.cuh>
 
 #include "internal.hpp"

@@ -5,13 +5,14 @@
 //   ::coupled (paths.cpp:99-141), LevelSampler ctor thresholds (paths.cpp:84-91).
 // Every floating-point expression that can round differently under FMA contraction is
 // written with explicit __d*_rn intrinsics in the reference's evaluation order; the only
-// remaining source of difference is CUDA's log1p/expm1/exp vs glibc (both < 1 ulp).
+// remaining sources of difference are CUDA's exp vs glibc (< 1 ulp) and holding tests whose
+// draw lies within a few ulps of the threshold (the probability-space test below).
 //
 // SIMT shape: a warp advances 32 independent paths one EVENT per loop trip (one pass of
 // evolve_common's for(;;) body).  Each event has exactly one call site for every expensive
 // operation -- one Philox block (the stream keeps a 3-word queue so one refill per event is
-// always enough for the u and v draws) and one log1p (the threshold test runs in log space,
-// see below) -- so a diverged warp pays each of them at most once per trip.
+// always enough for the u and v draws) and one divide (the holding test runs in probability
+// space, see below) -- so a diverged warp pays each of them at most once per trip.
 #pragma once
 
 #include <cuda_runtime.h>
