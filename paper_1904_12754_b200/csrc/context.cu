@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <omp.h>
+
 #include "internal.hpp"
 
 using namespace expmc_b200;
@@ -33,7 +35,8 @@ struct Staging {
     uint64_t* h_chunk0 = nullptr;
     Partial* h_totals = nullptr;
     size_t cap_h = 0;
-    std::vector<int64_t> slot;        // request index of each item (count > 0)
+    std::vector<int64_t> slot;        // request index of each item (count > 0), unless identity
+    bool identity = false;            // every request has count > 0: item k is request k
     size_t nitems = 0;
     bool inflight = false;
     std::vector<cudaEvent_t> ev;      // sampler launch brackets (timing)
@@ -365,11 +368,38 @@ bool ctx_has_load(const expmc_ctx* c) { return c->d_load != nullptr; }
 // sharded), ordered combine, totals back to S.h_totals -- all queued on the context's stream;
 // sample_wait collects them.  welford: the classical-MC reduction.
 void sample_launch(expmc_ctx* c, Staging& S, size_t nitems, uint32_t lane, bool welford) {
+    // exclusive prefix of the chunk counts: per-thread block sums, then the blocks' offsets
     uint64_t total = 0;
-    for (size_t k = 0; k < nitems; ++k) {  // exclusive prefix of the chunk counts
-        const uint64_t n = S.h_chunk0[k];
-        S.h_chunk0[k] = total;
-        total += n;
+    if (nitems < (size_t{1} << 16)) {
+        for (size_t k = 0; k < nitems; ++k) {
+            const uint64_t n = S.h_chunk0[k];
+            S.h_chunk0[k] = total;
+            total += n;
+        }
+    } else {
+        std::vector<uint64_t> part(static_cast<size_t>(omp_get_max_threads()) + 1, 0);
+        size_t used = 1;
+#pragma omp parallel
+        {
+            const size_t nt = static_cast<size_t>(omp_get_num_threads()), t = static_cast<size_t>(omp_get_thread_num());
+            const size_t b = nitems * t / nt, e = nitems * (t + 1) / nt;
+            uint64_t acc = 0;
+            for (size_t k = b; k < e; ++k) acc += S.h_chunk0[k];
+            part[t + 1] = acc;
+#pragma omp barrier
+#pragma omp single
+            {
+                for (size_t q = 1; q <= nt; ++q) part[q] += part[q - 1];
+                used = nt;
+            }  // implicit barrier
+            acc = part[t];
+            for (size_t k = b; k < e; ++k) {
+                const uint64_t n = S.h_chunk0[k];
+                S.h_chunk0[k] = acc;
+                acc += n;
+            }
+        }
+        total = part[used];
     }
     S.h_chunk0[nitems] = total;
     cuda_check(cudaMemcpyAsync(S.d_items, S.h_items, nitems * sizeof(DevItem), cudaMemcpyHostToDevice, c->stream),
@@ -545,10 +575,11 @@ void batch_launch(expmc_ctx* c, int s, double beta, uint32_t lane, const expmc_l
     need(!S.inflight, EXPMC_EINTERNAL, "staging slot busy");
     S.nitems = 0;
     // validate (first failing request wins, as a sequential loop would report it)
-    int64_t bad = nreq;
-#pragma omp parallel for schedule(static) reduction(min : bad)
+    int64_t bad = nreq, empty = 0;
+#pragma omp parallel for schedule(static) reduction(min : bad) reduction(+ : empty)
     for (int64_t i = 0; i < nreq; ++i) {
         out[i] = expmc_level_stats{0.0, 0.0, 0, 0, 0, 0.0};
+        empty += req[i].count == 0;
         try {
             validate_req(c, req[i], beta, lane);
         } catch (const Status&) {
@@ -557,10 +588,13 @@ void batch_launch(expmc_ctx* c, int s, double beta, uint32_t lane, const expmc_l
     }
     if (bad < nreq) validate_req(c, req[bad], beta, lane);  // rethrows with the right code
     S.slot.clear();
-    S.slot.reserve(static_cast<size_t>(nreq));
-    for (int64_t i = 0; i < nreq; ++i)
-        if (req[i].count > 0) S.slot.push_back(i);
-    const size_t nitems = S.slot.size();
+    S.identity = empty == 0;  // the driver's batches: no empty requests, no index list to build
+    if (!S.identity) {
+        S.slot.reserve(static_cast<size_t>(nreq));
+        for (int64_t i = 0; i < nreq; ++i)
+            if (req[i].count > 0) S.slot.push_back(i);
+    }
+    const size_t nitems = S.identity ? static_cast<size_t>(nreq) : S.slot.size();
     if (nitems == 0) return;
     const bool forward = lane == EXPMC_LANE_FORWARD;
     if (forward) ensure_forward_init(c);  // run_level builds it before sampling (mlmc.cpp)
@@ -569,7 +603,7 @@ void batch_launch(expmc_ctx* c, int s, double beta, uint32_t lane, const expmc_l
     ensure_items(S, nitems, c->stream);
 #pragma omp parallel for schedule(static)
     for (size_t k = 0; k < nitems; ++k) {
-        const expmc_level_req& r = req[S.slot[k]];
+        const expmc_level_req& r = req[S.identity ? static_cast<int64_t>(k) : S.slot[k]];
         S.h_items[k] = make_item(r, beta, lane);
         const uint64_t first_chunk = r.first_index / kChunk;
         const uint64_t last_chunk = (r.first_index + r.count - 1) / kChunk;  // parallel.hpp:36-38
@@ -588,8 +622,9 @@ void batch_finish(expmc_ctx* c, int s, const expmc_level_req* req, expmc_level_s
     uint64_t samples = 0, jumps = 0, steps = 0;
 #pragma omp parallel for schedule(static) reduction(+ : samples, jumps, steps)
     for (size_t k = 0; k < nitems; ++k) {
-        const expmc_level_req& r = req[S.slot[k]];
-        expmc_level_stats& o = out[S.slot[k]];
+        const int64_t i = S.identity ? static_cast<int64_t>(k) : S.slot[k];
+        const expmc_level_req& r = req[i];
+        expmc_level_stats& o = out[i];
         o.sum = S.h_totals[k].sum;
         o.sum_sq = S.h_totals[k].sum_sq;
         o.samples = sampled_count(r.first_index, r.count);
