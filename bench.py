@@ -33,6 +33,12 @@ import sys
 import threading
 import time
 
+# torchrun exports OMP_NUM_THREADS=1 to every rank; the library's host driver (request staging,
+# per-row state machines, combines of results) is OpenMP-parallel, so each rank gets its share of
+# the host cores instead.  Set before numpy / torch / the library load libgomp.
+if os.environ.get("OMP_NUM_THREADS") == "1" and "LOCAL_WORLD_SIZE" in os.environ:
+    os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // max(1, int(os.environ["LOCAL_WORLD_SIZE"]))))
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -303,12 +309,22 @@ def main():
 
     import paper_1904_12754_b200 as P
 
+    # EXPMC_BENCH_SHARE_DEVICE=1 (functional check of the N > 1 path on a one-GPU box, never a
+    # measurement): every rank on cuda:0, host plumbing over gloo.  Row sharding has no
+    # device-side exchange, so the ranks' kernels never wait on one another.
+    shared = os.environ.get("EXPMC_BENCH_SHARE_DEVICE") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if shared else "cuda"
 
     def barrier():
         if dist:
@@ -317,14 +333,14 @@ def main():
     def max_over_ranks(x):
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
         if not dist:
             return x
-        t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t)
         return float(t.item())
 
@@ -385,6 +401,7 @@ def main():
     rows_done = agg(len(res))
     conv = agg(int(res["converged"].sum()))
     over = agg(int(res["over_budget"].sum()))
+    total_cost = agg(int(res["total_cost"].sum()))  # every rank takes part in the reduction
     proj_over = float(res["projected_cost"][res["over_budget"] != 0].max()) if (res["over_budget"] != 0).any() else 0.0
     value = jumps / (ms * 1e-3)
 
@@ -478,7 +495,7 @@ def main():
                                        f"rows sharded over {world} rank(s), no data-path collective")},
             "rows_per_s": rows_done / (ms * 1e-3), "samples_per_s": samples / (ms * 1e-3),
             "path_steps_per_s": fine_steps / (ms * 1e-3),
-            "cost_units_per_s": agg(int(res["total_cost"].sum())) / (ms * 1e-3),
+            "cost_units_per_s": total_cost / (ms * 1e-3),
             "converged_rows": int(conv), "rows": int(rows_done), "sampler": sampler,
             "over_budget_rows": int(over), "max_cost": max_cost, "max_projected_cost_over_budget": proj_over,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
