@@ -147,13 +147,6 @@ __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begi
         k = static_cast<uint32_t>(k53 >> (53 - (31 - __clz(deg))));
         done = true;
     } else if (degf & kUniformRow) {
-#ifdef EXPMC_PICK_INT
-        const uint64_t lo = k53 * deg;
-        const uint64_t hi = __umul64hi(k53, static_cast<uint64_t>(deg));
-        const uint64_t rem = lo & ((uint64_t{1} << 53) - 1);
-        k = static_cast<uint32_t>((hi << 11) | (lo >> 53));
-        done = rem >= deg && rem <= (uint64_t{1} << 53) - deg;
-#else
         // t = fl(v deg) is within deg 2^-53 of v deg; a fractional part at least 2 deg 2^-53 away
         // from 0 and 1 puts v deg at least deg 2^-53 from every integer: floor(t) is then the
         // exact upper_bound and the boundary condition above holds.
@@ -164,7 +157,6 @@ __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begi
         const double margin = __dmul_rn(dg, 0x1.0p-52);
         k = static_cast<uint32_t>(fl);
         done = f >= margin && f <= __dsub_rn(1.0, margin);
-#endif
     }
     if (!done) {
         const double v = to_uniform(k53);

@@ -123,3 +123,25 @@ def test_long_paths_and_mixed_batch(gpu, oracle_lib):
             o = och.run_level(cfg.u, e, cfg.beta, l, b, f, c, 1000 + e)
             assert int(out[k]["cost"]) == o["cost"] and int(out[k]["jumps"]) == o["jumps"]
             assert float(out[k]["sum"]) == pytest.approx(o["sum"], rel=1e-12, abs=1e-13)
+
+
+def test_event_sampler_multi_window_groups(gpu, monkeypatch):
+    """k_sample_grouped with windows that are not a multiple of the 4-chunk group (groups
+    straddle launches): same sample counts and costs as one window, sums to 1e-12."""
+    from paper_1904_12754_b200 import configs
+
+    cfg = configs.make_config("c3-20000")
+    entries = np.array([0, 5, 77, 1234, 19999])
+    levels = np.array([7, 8, 9, 7, 10])
+    args = (cfg.beta, entries, levels, (levels == 7).astype(np.int32), [0, 100, 3, 512, 9],
+            [300000, 70000, 20000, 4096, 9000], 1000 + entries)
+    out = {}
+    for w in ("", "7"):
+        if w:
+            monkeypatch.setenv("EXPMC_WINDOW_CHUNKS", w)
+        with P.Context(cfg.a, cfg.u, sampler="event") as ctx:
+            out[w] = ctx.run_level_batch(*args)
+    for k in ("samples", "cost", "jumps"):
+        assert np.array_equal(out[""][k], out["7"][k]), k
+    for k in ("sum", "sum_sq"):
+        assert np.allclose(out[""][k], out["7"][k], rtol=1e-12, atol=1e-12 * np.abs(out[""][k]).max()), k
