@@ -12,6 +12,9 @@ fixed permutation (strong scaling, no data-path collective -- components are ind
 problems; only timings are reduced).  `--rows-per-step R` instead gives every rank R
 components per step (weak scaling).
 
+`--gpus N` without torchrun re-launches this script under `torch.distributed.run` with N ranks
+(one per GPU); under torchrun WORLD_SIZE must equal N or the run fails.
+
 Timed region (`value`): tables already resident in HBM; K steps bracketed by barrier +
 torch.cuda.synchronize(), CUDA events recorded on the library's own stream; max over ranks.
 L2 is flushed (256 MB write) before every step inside the timed region.
@@ -20,14 +23,17 @@ host CSR + u (H2D), the solve, results back to host -- per step, CUDA events on 
 stream around the call.
 
 `--impl reference`: the UNMODIFIED reference (oracle/_ref/libexpmc_ref.so, compiled from
-/root/reference by oracle/Makefile) runs its own mlmc_driver per component on all host
-cores (OpenMP), rank 0 only, each step a bounded sample of rows of the same batches.
+/root/reference by oracle/Makefile) runs its own mlmc_driver per component with OpenMP on all
+host cores, rank 0 only.  Its process never imports the product package: the inputs come from
+`workloads.py` (numpy) and the reference's own generator.  Each of its steps is a bounded
+sample of the same job (`sample` key); `config` is the same dict as this arm's.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -44,13 +50,17 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+import workloads as W  # noqa: E402  (numpy only: safe for the reference arm)
+
 METRIC = "random-walk transitions/sec and exp(tA)v rows/sec at target ε; % gather roofline"
 UNIT = "transitions/s"
-ALG_BYTES_PER_JUMP = 64    # destination row record (32 B sector) + edge record sector
-ALG_BYTES_PER_SAMPLE = 32  # terminal u[state] sector
+ALG_BYTES_PER_JUMP = 64  # destination row record (32-B sector: d, rate, u, begin, deg) + edge-record sector
+PROFILE_DIR = os.path.join(ROOT, "profiles", "r02")
+# reference-arm components per step (as-shipped driver, all host cores): ~1-3 s per step on 16 cores
+REF_ROWS_PER_STEP = {"c1": 64, "c2": 32, "c3": 1, "c4": 1, "c5": 1}
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
@@ -58,7 +68,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="c2")
     p.add_argument("--rows-per-step", type=int, default=0, help="components per rank per step (0: default)")
-    p.add_argument("--ref-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    p.add_argument("--ref-seconds", type=float, default=15.0, help="cpu_baseline sample budget (our arm)")
+    p.add_argument("--ref-rows-per-step", type=int, default=0, help="reference arm: components per step (0: default)")
     p.add_argument("--max-cost", type=float, default=None,
                    help="per-component model-unit budget (driver extension; default off for C1/C2, 1e10 for C3-C5)")
     p.add_argument("--sampler", default=None, choices=["reference", "event"], help="override the config's sampler")
@@ -66,12 +77,13 @@ def parse():
                    help="event sampler: evaluate first holding intervals in full (A/B of the closed-form hold)")
     p.add_argument("--log-hold", action="store_true",
                    help="reference-order sampler: time-space holding tests with a log per event (A/B of S-mode)")
-    p.add_argument("--multi", default="rows", choices=["rows", "samples"],
-                   help="N>1: shard components over ranks (no collective) or shard every component's "
-                        "samples with an exact NCCL all-reduce of the chunk partials")
+    p.add_argument("--multi", default=None, choices=["rows", "samples"],
+                   help="N>1: shard components over ranks (no collective; default for C1/C2) or shard every "
+                        "component's samples with an exact NCCL all-reduce of the chunk partials (default for "
+                        "the hub-heavy C3/C4)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    return p.parse_args()
+    return p.parse_args(argv)
 
 
 def dist_env():
@@ -79,6 +91,23 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     return rank, world, local
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`--gpus N` (N > 1) without torchrun: start N ranks with torch.distributed.run on this node
+    and return its exit code.  NCCL_DEBUG=INFO (unless set) so the log shows every rank's comm."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
 
 
 _PERM = {}
@@ -90,37 +119,32 @@ def perm_rows(n):
     return _PERM[n]
 
 
+def row_shard(n, rank, world):
+    """Components of rank `rank` when the whole job is dealt over `world` ranks: every world-th
+    entry of the fixed permutation, sorted (paper_1904_12754_b200.shard.row_shard)."""
+    return np.sort(perm_rows(n)[rank::world])
+
+
 def batch_rows(n, step, rank, world, r):
     """Rows rank `rank` solves in `step`.  r == 0: the whole job -- every component, dealt
     round-robin over a fixed permutation to the ranks (strong scaling).  r > 0: r components
     per rank per step, consecutive slices of the permutation (weak scaling)."""
-    perm = perm_rows(n)
     if r == 0:
-        from paper_1904_12754_b200.shard import row_shard
-
-        return row_shard(n, rank, world)  # == np.sort(perm[rank::world])
+        return row_shard(n, rank, world)
     k = (step * world + rank) * r
-    idx = (np.arange(k, k + r) % n)
-    return np.sort(perm[idx])
+    return np.sort(perm_rows(n)[np.arange(k, k + r) % n])
 
 
-def sample_rows(n, step, r):
-    """Unsorted rows for the bounded CPU sample (a random subset of the step's batch)."""
-    perm = perm_rows(n)
-    if r == 0:
-        return np.roll(perm, -step * 1024)
-    return perm[(np.arange(step * r, step * r + r) % n)]
-
-
-def cpu_rows(cfg, step, r):
-    """Components for the CPU reference sample.  Graph/3-D configs: light rows only (degree <= 32)
-    -- the reference has no cost budget and one hub row can run for hours."""
-    universe = cfg.rows if cfg.rows is not None else np.arange(cfg.a.n, dtype=np.int64)
-    rows = universe[sample_rows(len(universe), step, r)]
-    if cfg.name.startswith(("c3", "c4", "c5")):
-        deg = np.diff(cfg.a.row_ptr)
-        rows = rows[deg[rows] <= 32]
-    return rows
+def cpu_sample_rows(universe, deg, name, step, count):
+    """Components of CPU-reference step `step`: consecutive slices of the same fixed permutation the
+    GPU arm deals its batches from.  Graph / 3-D configs keep light components only (degree <= 8):
+    the reference has no cost budget and a hub component runs for hours."""
+    perm = perm_rows(len(universe))
+    cand = universe[perm]
+    if name.startswith(("c3", "c4", "c5")):
+        cand = cand[deg[cand] <= 8]
+    k = step * count
+    return cand[np.arange(k, k + count) % len(cand)]
 
 
 class Clocks:
@@ -181,37 +205,171 @@ def load_peaks():
     return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
+_SCALE = {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+
+
 def load_capture(cfg_name):
-    """The committed ncu --set full capture of this config's k_sample (profiles/r01/
-    k_sample_<config>_r1h_key_metrics.json, scripts/prof_c4.sh): DRAM bytes per kernel-ms
-    (dram__bytes_read.sum + dram__bytes_write.sum over the launch) and issue-slot utilisation.
+    """This config's committed `ncu --set full` capture of one k_sample launch
+    (profiles/r02/k_sample_<config>_key_metrics.json, written by scripts/ncu_keys.py from the
+    .ncu-rep): the measured DRAM bytes, L2 / L1 throughput and issue utilisation of that launch.
     None for configs without a capture."""
     name = cfg_name.split("-")[0]
-    path = os.path.join(ROOT, "profiles", "r01", f"k_sample_{name}_r1h_key_metrics.json")
+    path = os.path.join(PROFILE_DIR, f"k_sample_{name}_key_metrics.json")
     try:
         with open(path) as f:
             k = json.load(f)
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
-        dram = sum(float(k[m]["value"]) * scale[k[m]["unit"]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        return {"bytes_per_ms": dram / float(k["gpu__time_duration.sum"]["value"]),
-                "issue_active_pct": float(k["smsp__issue_active.avg.pct_of_peak_sustained_active"]["value"]),
+        ms = float(k["gpu__time_duration.sum"]["value"]) * (1e-3 if k["gpu__time_duration.sum"]["unit"] == "us" else 1.0)
+        dram = sum(float(k[m]["value"]) * _SCALE[k[m]["unit"]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+
+        def pct(key):
+            return float(k[key]["value"]) / 100.0 if key in k else None
+
+        return {"ms": ms, "dram_bytes": dram, "dram_bytes_per_ms": dram / ms,
+                "l2_frac": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                "l1_frac": pct("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                "issue_frac": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "threads_per_inst": float(k["smsp__thread_inst_executed_per_inst_executed.ratio"]["value"]),
+                "l1_hit": pct("l1tex__t_sector_hit_rate.pct"), "l2_hit": pct("lts__t_sector_hit_rate.pct"),
                 "source": os.path.relpath(path, ROOT)}
     except (OSError, KeyError, ValueError):
         return None
 
 
-def sampler_only_rate(ref_chain, cfg, threads, seconds=4.0):
-    """The reference's sampler without the driver: one large run_level per level
-    (its LevelSampler table is built once per call, so the O(n) construction is amortised),
-    OpenMP on all cores.  transitions = cost - 2 M 2^l (every fine step of a non-absorbing row
-    ends with one draw).  Level 0 (base) and level 2 (coupled), each sized to ~seconds/2."""
+# ------------------------------------------------------------------------------ reference arm
+def reference_problem(name):
+    """The reference's own objects for config `name`, built without the product package:
+    (RefChain, u, beta, universe, degree, max_levels_above_l0, eps)."""
+    from oracle import CSR, Reference
+
+    ref = Reference()
+    base = name.split("-")[0]
+    if name in ("c1", "c2") or name.startswith("grid"):
+        g = {"c1": 64, "c2": 1024}.get(name) or int(name[4:])
+        n, rp, col, val = W.grid_laplacian(g)
+        u = W.philox_first_uniform(W.VECTOR_SEED, 0, np.arange(n, dtype=np.uint64), 6)
+        beta = 0.5 if name == "c2" else 1.0
+        return ref.chain(CSR(n, rp, col, val)), u, beta, np.arange(n, dtype=np.int64), np.diff(rp), 30, 1e-3
+    if base == "c5":
+        g = int(name[3:]) if "-" in name else 256
+        n, rp, col, val = W.convdiff3d(g, 10.0, 0)
+        u = 2.0 * W.philox_first_uniform(W.VECTOR_SEED, 0, np.arange(n, dtype=np.uint64), 6) - 1.0
+        return ref.chain(CSR(n, rp, col, val)), u, 0.1, np.arange(n, dtype=np.int64), np.diff(rp), 4, 1e-4
+    if base == "c3":
+        n = int(name[3:]) if "-" in name else 1_000_000
+        chain = ref.pref(n, 5, W.GRAPH_SEED)  # the reference's own netgen (netgen.cpp:61-107)
+        dec = chain.decomposition()           # 0/1 adjacency, zero diagonal: CSR = (row_ptr, targets, 1)
+        rp, col = dec["row_ptr"], dec["jump_target"]
+        lam = W.power_iteration(n, rp, col, np.ones(col.size), 50)
+        return chain, np.ones(n), 1.0 / lam, np.arange(n, dtype=np.int64), np.diff(rp), 30, 1e-3
+    if base == "c4":
+        # R-MAT exists only in the product's host generator (the reference has none, SURVEY §2):
+        # generated in a SEPARATE process and handed over as arrays, so this process never loads it
+        scale = int(name[3:]) if "-" in name else 24
+        path = os.path.join("/tmp", f"expmc_rmat{scale}.npz")
+        if not os.path.exists(path):
+            code = (f"import numpy as np; from paper_1904_12754_b200 import configs as c; a = c.gen_rmat({scale}, 16); "
+                    f"np.savez({path!r}, rp=a.row_ptr, col=a.col)")
+            subprocess.run([sys.executable, "-c", code], check=True, cwd=ROOT)
+        z = np.load(path)
+        rp, col = z["rp"], z["col"]
+        n = rp.size - 1
+        lam = W.power_iteration(n, rp, col, np.ones(col.size), 50)
+        rows = W.seeded_rows(n, min(n, 1 << 20))
+        return ref.chain(CSR(n, rp, col, np.ones(col.size))), np.ones(n), 1.0 / lam, rows, np.diff(rp), 30, 1e-3
+    raise ValueError(f"unknown config {name!r}")
+
+
+def reference_step(chain, u, beta, rows, deg, eps, mla, threads):
+    """The as-shipped reference mlmc_driver on `rows`, one after another (reference OpenMP inside
+    run_level).  Returns (transitions, samples, components)."""
+    jumps = samples = 0
+    for r in rows:
+        (res,) = chain.driver_rows(u, beta, [int(r)], [W.ROW_SEED_BASE + int(r)], epsilon=eps, threads=threads,
+                                   max_levels_above_l0=mla)
+        # transitions = sum_l (cost_l - 2 M_l 2^l); an isolated (absorbing) row never jumps
+        jumps += 0 if deg[int(r)] == 0 else res["total_jumps"]
+        samples += res["total_samples"]
+    return jumps, samples, len(rows)
+
+
+def run_reference(args, rank, world):
+    """`--impl reference`: rank 0 times the unmodified reference on `--steps` steps, each a fixed
+    sample of the job's components (the first REF_ROWS_PER_STEP of consecutive slices of the same
+    permutation the GPU arm deals from), after `--warmup` untimed steps."""
+    if rank != 0:
+        return 0
+    from oracle import have_reference
+
+    if not have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libexpmc_ref.so not built"}))
+        return 0
+    threads = os.cpu_count() or 1
+    chain, u, beta, universe, deg, mla, eps = reference_problem(args.config)
+    per_step = args.ref_rows_per_step or REF_ROWS_PER_STEP.get(args.config.split("-")[0], 16)
+    for w in range(args.warmup):
+        reference_step(chain, u, beta, cpu_sample_rows(universe, deg, args.config, w, per_step), deg, eps, mla, threads)
+    tj = ts = tr = 0
+    step_ms = []
+    for s in range(args.steps):
+        rows = cpu_sample_rows(universe, deg, args.config, args.warmup + s, per_step)
+        t0 = time.perf_counter()
+        j, smp, nr = reference_step(chain, u, beta, rows, deg, eps, mla, threads)
+        step_ms.append(1e3 * (time.perf_counter() - t0))
+        tj, ts, tr = tj + j, ts + smp, tr + nr
+    tt = sum(step_ms) * 1e-3
+    value = tj / tt if tt > 0 else None
+    sample = (f"{per_step} components per step ({tr} timed), consecutive slices of the GPU arm's fixed component "
+              f"permutation" + (", degree <= 8 only" if args.config.startswith(("c3", "c4", "c5")) else "")
+              + "; as-shipped reference mlmc_driver per component, row seed 1000 + row")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(np.mean(step_ms)) if step_ms else None, "higher_is_better": True,
+        "scaling": "strong" if args.config in ("c1", "c2") and not args.rows_per_step else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": W.config_dict(args.config), "sample": sample,
+        "parallelism": f"OpenMP {threads} host threads (reference run_level), rank 0 only",
+        "rows_per_s": tr / tt if tt > 0 else None, "samples_per_s": ts / tt if tt > 0 else None,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline_leg(args, threads):
+    """cpu_baseline of our arm (rank 0, N = 1): the unmodified reference on a bounded ~ref-seconds
+    sample of the same job, plus its sampler alone."""
+    from oracle import have_reference
+
+    if not have_reference():
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": "oracle/_ref not built"}
+    chain, u, beta, universe, deg, mla, eps = reference_problem(args.config)
+    per_step = REF_ROWS_PER_STEP.get(args.config.split("-")[0], 16)
+    tj = ts = tr = 0
+    t0 = time.perf_counter()
+    s = 0
+    while time.perf_counter() - t0 < args.ref_seconds:
+        j, smp, nr = reference_step(chain, u, beta, cpu_sample_rows(universe, deg, args.config, 1000 + s, per_step),
+                                    deg, eps, mla, threads)
+        tj, ts, tr, s = tj + j, ts + smp, tr + nr, s + 1
+    dt = time.perf_counter() - t0
+    return {"value": tj / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{tr} {args.config.upper()} components through the as-shipped reference mlmc_driver "
+                      f"(OpenMP, {dt:.1f} s)", "rows_per_s": tr / dt,
+            "sampler_only": sampler_only_rate(chain, u, beta, universe, threads)}
+
+
+def sampler_only_rate(chain, u, beta, universe, threads, seconds=4.0):
+    """The reference's sampler without the driver: one large run_level per level (its
+    LevelSampler table is built once per call, so the O(n) construction is amortised), OpenMP on all
+    cores.  transitions = cost - 2 M 2^l.  Level 0 (base) and level 2 (coupled), ~seconds/2 each."""
     out = {}
-    row = cfg.a.n // 2 + 7
+    row = int(universe[len(universe) // 2])
     for level, base in ((0, True), (2, False)):
         m = 1 << 16
         while True:  # grow the sample until one call takes ~seconds / 2
             t0 = time.perf_counter()
-            r = ref_chain.run_level(cfg.u, row, cfg.beta, level, base, 1 << 40, m, 99, threads=threads)
+            r = chain.run_level(u, row, beta, level, base, 1 << 40, m, 99, threads=threads)
             dt = time.perf_counter() - t0
             if dt >= seconds / 4 or m >= (1 << 34):
                 break
@@ -222,74 +380,11 @@ def sampler_only_rate(ref_chain, cfg, threads, seconds=4.0):
     return out
 
 
-# ------------------------------------------------------------------------------ reference arm
-def reference_rows(ref_chain, cfg, rows, seconds, threads, max_rows):
-    """Reference mlmc_driver on rows one at a time, in a worker thread, for at most `seconds`.
-
-    A single reference run cannot be interrupted and some components never finish in practice
-    (the bias test can escalate to 2^(l0+30) steps per path), so the worker is
-    abandoned at the deadline (it dies with the process) and only completed components count:
-    throughput = their transitions / the time the last of them finished."""
-    deg = np.diff(cfg.a.row_ptr)
-    done_rows = []
-    t0 = time.perf_counter()
-
-    def work():
-        for r in rows[:max_rows]:
-            (res,) = ref_chain.driver_rows(cfg.u, cfg.beta, [int(r)], [1000 + int(r)], epsilon=cfg.epsilon,
-                                           threads=threads, max_levels_above_l0=cfg.max_levels_above_l0)
-            # transitions = cost - 2 M 2^l per level (BASELINE.md §3.5); an isolated row (rate 0,
-            # absorbing) draws nothing and never jumps
-            jumps = 0 if deg[int(r)] == 0 else res["total_jumps"]
-            done_rows.append((time.perf_counter(), jumps, res["total_samples"]))
-            if time.perf_counter() - t0 >= seconds:
-                return
-
-    th = threading.Thread(target=work, daemon=True)
-    th.start()
-    th.join(timeout=seconds + 1.0)
-    got = list(done_rows)
-    if not got:
-        return 0, 0, 0, time.perf_counter() - t0
-    return sum(g[1] for g in got), sum(g[2] for g in got), len(got), got[-1][0] - t0
-
-
-def run_reference(args, cfg, rank, world, r):
-    if rank != 0:
-        return 0
-    from oracle import CSR, Reference, have_reference
-
-    if not have_reference():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libexpmc_ref.so not built"}))
-        return 0
-    threads = os.cpu_count() or 1
-    ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
-    # warm-up: one small component (pages the matrix in, spins up the OpenMP pool); then the
-    # whole timed sample as ONE bounded worker run (an abandoned worker must not overlap a
-    # later timing window), reported per step as its K-th part
-    reference_rows(ref, cfg, cpu_rows(cfg, 0, r), 2.0, threads, 1)
-    tj, ts, tr, tt = reference_rows(ref, cfg, cpu_rows(cfg, args.warmup, r), args.ref_seconds, threads, 1 << 30)
-    value = tj / tt if tr else None
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
-        "scaling": "strong" if r == 0 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": cfg.description, "sample": f"{tr} components (as-shipped mlmc_driver per row)",
-                   "parallelism": f"OpenMP {threads} threads, rank 0 only"},
-        "rows_per_s": tr / tt if tr else None, "samples_per_s": ts / tt if tr else None,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{tr} {cfg.name.upper()} components, as-shipped reference mlmc_driver, {tt:.1f} s"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
-    return 0
-
-
 # ------------------------------------------------------------------------------ our arm
-def main():
-    args = parse()
-    rank, world, local = dist_env()
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_1904_12754_b200 as P
     from paper_1904_12754_b200 import configs
 
     cfg = configs.make_config(args.config)
@@ -302,12 +397,7 @@ def main():
     max_cost = args.max_cost if args.max_cost is not None else default_budget
     sampler = args.sampler or cfg.sampler
     universe = cfg.rows if cfg.rows is not None else np.arange(cfg.a.n, dtype=np.int64)
-    if args.impl == "reference":
-        return run_reference(args, cfg, rank, world, r)
-
-    import torch
-
-    import paper_1904_12754_b200 as P
+    multi = args.multi or ("samples" if cfg.name.startswith(("c3", "c4")) else "rows")
 
     # EXPMC_BENCH_SHARE_DEVICE=1 (functional check of the N > 1 path on a one-GPU box, never a
     # measurement): every rank on cuda:0, host plumbing over gloo.  Row sharding has no
@@ -315,6 +405,10 @@ def main():
     shared = os.environ.get("EXPMC_BENCH_SHARE_DEVICE") == "1"
     if shared:
         local = 0
+        if multi == "samples" and world > 1:
+            multi = "rows"  # NCCL ranks on one device would wait on one another (B200_PROFILING.md)
+    elif local >= P.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but only {P.device_count()} GPU(s) are visible")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -351,7 +445,7 @@ def main():
         ctx.set_full_hold(True)
     if args.log_hold:
         ctx.set_log_hold(True)
-    sample_shard = args.multi == "samples" and world > 1
+    sample_shard = multi == "samples" and world > 1
     if sample_shard:  # every rank runs the same components; chunk g is sampled on rank g % world
         obj = [P.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -361,7 +455,7 @@ def main():
 
     # the batches of every step are built before any timing starts
     batches = [universe[batch_rows(len(universe), s, rank_b, world_b, r)] for s in range(args.warmup + args.steps)]
-    seeds = [configs.row_seeds(b) for b in batches]
+    seeds = [W.row_seeds(b) for b in batches]
 
     def solve(step):
         res, _ = P.mlmc_driver_rows(ctx, cfg.beta, batches[step], seeds[step], opts, want_levels=False)
@@ -400,22 +494,28 @@ def main():
     fine_steps = agg(ctr["fine_steps"])
     rows_done = agg(len(res))
     conv = agg(int(res["converged"].sum()))
-    over = agg(int(res["over_budget"].sum()))
+    overb = res["over_budget"] != 0
+    over = agg(int(overb.sum()))
     total_cost = agg(int(res["total_cost"].sum()))  # every rank takes part in the reduction
-    proj_over = float(res["projected_cost"][res["over_budget"] != 0].max()) if (res["over_budget"] != 0).any() else 0.0
+    proj_over = float(res["projected_cost"][overb].max()) if overb.any() else 0.0
+    # completeness of graph configs: projected model units of the over-budget components, their
+    # sum extrapolated to the whole job, and the GPU time that would take at this run's unit rate
+    proj_sum = agg(float(res["projected_cost"][overb].sum()))
+    proj_full = proj_sum * len(universe) / max(1.0, rows_done)
     value = jumps / (ms * 1e-3)
+    cost_rate = total_cost / (ms * 1e-3)
 
-    # roofline of the dominant kernel (k_sample): algorithmic bytes / summed launch time
-    alg_bytes = ctr["jumps"] * ALG_BYTES_PER_JUMP + ctr["samples"] * ALG_BYTES_PER_SAMPLE
+    # roofline of the dominant kernel (k_sample): algorithmic bytes / summed launch time (CUDA
+    # events on the library stream around every sampler launch, read back by ctx.counters())
+    launches = max(1, ctr["sampler_launches"])
+    alg_bytes = ctr["jumps"] * ALG_BYTES_PER_JUMP
     kern_s = ctr["sampler_ms"] * 1e-3
     achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
     peaks, peak_src = load_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
     cap = load_capture(cfg.name)
-    traffic_rate = cap["bytes_per_ms"] if cap else None
-    launches = max(1, ctr["sampler_launches"])
-    # per launch, like `achieved`: the capture's DRAM bytes per kernel-ms x this run's mean launch length
-    traffic = traffic_rate * ctr["sampler_ms"] / launches if traffic_rate else None
+    mean_launch_ms = ctr["sampler_ms"] / launches
+    traffic = cap["dram_bytes_per_ms"] * mean_launch_ms if cap else None
     gather_l2 = gather_hbm = None
     if rank == 0:
         try:
@@ -423,7 +523,7 @@ def main():
             gather_hbm = P.bench_gather(local, 8 << 30)
         except Exception:
             pass
-    gpu_launches = ctr["kernel_launches"] + 2 * args.steps  # + the L2 flush fill per step (torch)
+    gpu_launches = ctr["kernel_launches"] + args.steps  # + the L2 flush fill per step (torch)
 
     # e2e through the public API from host buffers
     e2e = None
@@ -465,50 +565,54 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            from oracle import CSR, Reference, have_reference
-
-            if have_reference():
-                threads = os.cpu_count() or 1
-                ref = Reference().chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
-                j, smp, done, dt = reference_rows(ref, cfg, cpu_rows(cfg, args.warmup, r),
-                                                  args.ref_seconds, threads, 1 << 30)
-                cpu = {"value": j / dt if done else None, "unit": UNIT, "cores": threads, "kind": "reference",
-                       "sample": f"{done} randomly chosen {cfg.name.upper()} components through the as-shipped reference "
-                                 f"mlmc_driver (OpenMP, {dt:.1f} s)", "rows_per_s": done / dt if done else None,
-                       "sampler_only": sampler_only_rate(ref, cfg, threads)}
+            cpu = cpu_baseline_leg(args, os.cpu_count() or 1)
         except Exception as exc:  # baseline failure must not hide the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
 
     if rank == 0:
+        measured = None
+        if cap:
+            dram_gbs = cap["dram_bytes_per_ms"] / 1e6
+            measured = {"source": cap["source"] + " (ncu --set full, one k_sample launch of this config)",
+                        "dram_gbs": dram_gbs, "dram_frac": dram_gbs / peak, "l2_frac": cap["l2_frac"],
+                        "l1_frac": cap["l1_frac"], "issue_frac": cap["issue_frac"],
+                        "threads_per_inst": cap["threads_per_inst"], "l1_hit": cap["l1_hit"], "l2_hit": cap["l2_hit"]}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if r == 0 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name.upper()}: {cfg.description}; one step = "
-                                   + (f"the whole job (all {cfg.a.n} components) split over the ranks" if r == 0 else
-                                      f"MLMC driver solve of {r} seeded components per rank"),
-                       "components_per_step": int(rows_done / args.steps), "epsilon": cfg.epsilon, "t": cfg.beta,
-                       "l2": f"flushed (256 MB write) before every step; tables {ctx.table_bytes / 1e6:.0f} MB",
-                       "parallelism": (f"samples sharded over {world} ranks, exact NCCL all-reduce of chunk partials"
-                                       if sample_shard else
-                                       f"rows sharded over {world} rank(s), no data-path collective")},
+            "config": W.config_dict(cfg.name),
+            "step": ("the whole job (all components) split over the ranks" if r == 0 else
+                     f"MLMC driver solve of {r} seeded components per rank"),
+            "components_per_step": int(rows_done / args.steps),
+            "l2": f"flushed (256 MB write) before every step; tables {ctx.table_bytes / 1e6:.0f} MB",
+            "parallelism": (f"samples sharded over {world} ranks, exact NCCL all-reduce of chunk partials"
+                            if sample_shard else f"rows sharded over {world} rank(s), no data-path collective"),
             "rows_per_s": rows_done / (ms * 1e-3), "samples_per_s": samples / (ms * 1e-3),
-            "path_steps_per_s": fine_steps / (ms * 1e-3),
-            "cost_units_per_s": total_cost / (ms * 1e-3),
+            "path_steps_per_s": fine_steps / (ms * 1e-3), "cost_units_per_s": cost_rate,
             "converged_rows": int(conv), "rows": int(rows_done), "sampler": sampler,
-            "over_budget_rows": int(over), "max_cost": max_cost, "max_projected_cost_over_budget": proj_over,
+            "completeness": {
+                "converged": int(conv), "over_budget": int(over), "max_cost": max_cost,
+                "over_budget_fraction": over / rows_done if rows_done else 0.0,
+                "max_projected_cost_over_budget": proj_over,
+                "projected_cost_over_budget_sum": proj_sum,
+                "job_components": len(universe),
+                "projected_cost_over_budget_full_job": proj_full,
+                "projected_gpu_hours_full_job": proj_full / cost_rate / 3600.0 * world if cost_rate > 0 else None,
+                "note": "model units the over-budget components need at this eps (driver projection, DESIGN §7b); "
+                        "GPU-hours at this run's cost-unit rate on n_gpus GPUs"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k_sample", "sampler_launches": ctr["sampler_launches"],
-                         "kernel_ms": ctr["sampler_ms"], "step_share": ctr["sampler_ms"] / ms_local,
-                         "alg_bytes_per_launch": alg_bytes / max(1, ctr["sampler_launches"]),
-                         "traffic_source": (cap["source"] + " (ncu --set full of one launch of this config): DRAM "
-                                            "bytes per kernel-ms x this run's mean launch ms") if cap else None,
-                         "alg_bytes": f"{ALG_BYTES_PER_JUMP} B/transition + {ALG_BYTES_PER_SAMPLE} B/sample",
+                         "kernel_ms": ctr["sampler_ms"], "mean_launch_ms": mean_launch_ms,
+                         "step_share": ctr["sampler_ms"] / ms_local,
+                         "alg_bytes": f"{ALG_BYTES_PER_JUMP} B per transition (row record + edge sector); samples "
+                                      "that never leave the entry read no table",
+                         "alg_bytes_per_launch": alg_bytes / launches,
+                         "measured": measured,
+                         "binding_resource": "instruction issue (measured issue_frac)" if cap else None,
                          "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
-                         "issue_active_pct": cap["issue_active_pct"] if cap else None,
-                         "binding_resource": "instruction issue (ncu smsp__issue_active)" if cap else None,
                          "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches), "clocks": clk,
         }
@@ -517,6 +621,19 @@ def main():
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N ranks for --gpus N\n")
+        return 2
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
 
 
 if __name__ == "__main__":
