@@ -318,6 +318,10 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
     int l0 = opt.l0_override >= 0 ? opt.l0_override : initial_level_impl(beta, info.d_max);
     if (lane == EXPMC_LANE_FEM) l0 = std::max(l0, 1);  // the coarse grid must carry a Simpson rule
     const int cap = l0 + opt.max_levels_above_l0;
+    // fewer than two coupled levels: the reference's first iteration throws from bias_estimate
+    // (mlmc.cpp:45-47, 201-235); checked here, before the per-row setup sizes arrays from it
+    if (opt.max_iterations > 0 && nrows > 0 && opt.max_levels_above_l0 < 2)
+        throw Status(EXPMC_EINVAL, "bias estimate needs at least two coupled levels");
     DriverConfig cfg{opt.epsilon, opt.epsilon / std::sqrt(2.0), opt.warmup, opt.max_iterations, opt.max_cost,
                      lane == EXPMC_LANE_FEM};
 
@@ -325,6 +329,7 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
     std::vector<Arena> arenas(static_cast<size_t>(omp_get_max_threads()));
     RowBuffer st_mem(static_cast<size_t>(nrows) * sizeof(RowState));
     RowState* const st = reinterpret_cast<RowState*>(st_mem.p);  // constructed in place below
+    int setup_failed = 0;
 #pragma omp parallel
     {
         tl_arena = &arenas[static_cast<size_t>(omp_get_thread_num())];
@@ -337,12 +342,18 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
         s.l0 = l0;
         s.cap = cap;
         s.top = std::min(l0 + 4, cap);  // mlmc.cpp:201-205
-        s.lv.reserve(8);  // one arena slice each for the common L - l0 < 8
-        s.pending.reserve(8);
-        s.lv.resize(static_cast<uint32_t>(s.top - l0 + 1));
-        for (int i = 0; i <= s.top - l0; ++i) s.pending.emplace_back(i, opt.warmup);
+        try {  // nothing may escape an OpenMP region
+            s.lv.reserve(8);  // one arena slice each for the common L - l0 < 8
+            s.pending.reserve(8);
+            s.lv.resize(static_cast<uint32_t>(s.top - l0 + 1));
+            for (int i = 0; i <= s.top - l0; ++i) s.pending.emplace_back(i, opt.warmup);
+        } catch (...) {
+#pragma omp atomic write
+            setup_failed = 1;
+        }
     }
     }
+    if (setup_failed) throw Status(EXPMC_EINTERNAL, "host allocation failed in the driver setup");
 
     // Per round: (1) every active row's pending extensions become one contiguous slice of a
     // batch, (2) one batched GPU pass, (3) each row applies its slice (extend(), mlmc.cpp:188-199)
@@ -427,6 +438,13 @@ void drive_rows(expmc_ctx* ctx, uint32_t lane, double beta, const expmc_options&
 #pragma omp critical(expmc_driver_error)
                     if (err_code == 0) {
                         err_code = e.code;
+                        err_msg = e.what();
+                    }
+                    s.phase = Phase::done;
+                } catch (const std::exception& e) {  // nothing may escape an OpenMP region
+#pragma omp critical(expmc_driver_error)
+                    if (err_code == 0) {
+                        err_code = EXPMC_EINTERNAL;
                         err_msg = e.what();
                     }
                     s.phase = Phase::done;

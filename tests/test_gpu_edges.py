@@ -145,3 +145,18 @@ def test_event_sampler_multi_window_groups(gpu, monkeypatch):
         assert np.array_equal(out[""][k], out["7"][k]), k
     for k in ("sum", "sum_sq"):
         assert np.allclose(out[""][k], out["7"][k], rtol=1e-12, atol=1e-12 * np.abs(out[""][k]).max()), k
+
+
+def test_driver_too_few_levels_is_invalid_argument(gpu):
+    """max_levels_above_l0 < 2 leaves fewer than two coupled levels: the reference's first driver
+    iteration throws std::invalid_argument from bias_estimate (mlmc.cpp:45-47); here the same
+    error, raised before any per-row state is sized from it (a negative value used to wrap)."""
+    from paper_1904_12754_b200 import configs
+
+    cfg = configs.make_config("c1")
+    with P.Context(cfg.a, cfg.u) as ctx:
+        for mla in (1, 0, -2, -100):
+            with pytest.raises(P.InvalidArgument, match="two coupled levels"):
+                P.mlmc_driver_rows(ctx, cfg.beta, [3, 4], [1003, 1004], P.MlmcOptions(max_levels_above_l0=mla))
+        res, _ = P.mlmc_driver_rows(ctx, cfg.beta, [3], [1003], P.MlmcOptions(max_levels_above_l0=2))
+        assert res["L"][0] <= 2
