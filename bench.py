@@ -501,7 +501,7 @@ def run_ours(args, rank, world, local):
     # completeness of graph configs: projected model units of the over-budget components, their
     # sum extrapolated to the whole job, and the GPU time that would take at this run's unit rate
     proj_sum = agg(float(res["projected_cost"][overb].sum()))
-    proj_full = proj_sum * len(universe) / max(1.0, rows_done)
+    proj_full = proj_sum * len(universe) / max(1.0, rows_done)  # rows_done: every step's components
     value = jumps / (ms * 1e-3)
     cost_rate = total_cost / (ms * 1e-3)
 
@@ -591,12 +591,15 @@ def run_ours(args, rank, world, local):
                             if sample_shard else f"rows sharded over {world} rank(s), no data-path collective"),
             "rows_per_s": rows_done / (ms * 1e-3), "samples_per_s": samples / (ms * 1e-3),
             "path_steps_per_s": fine_steps / (ms * 1e-3), "cost_units_per_s": cost_rate,
-            "converged_rows": int(conv), "rows": int(rows_done), "sampler": sampler,
+            "converged_rows": int(conv), "rows": int(rows_done), "rows_note": "summed over the timed steps",
+            "sampler": sampler,
             "completeness": {
-                "converged": int(conv), "over_budget": int(over), "max_cost": max_cost,
+                "per": "step (the counts are the mean over the timed steps)",
+                "components": int(rows_done / args.steps),
+                "converged": int(conv / args.steps), "over_budget": int(over / args.steps), "max_cost": max_cost,
                 "over_budget_fraction": over / rows_done if rows_done else 0.0,
                 "max_projected_cost_over_budget": proj_over,
-                "projected_cost_over_budget_sum": proj_sum,
+                "projected_cost_over_budget_sum": proj_sum / args.steps,
                 "job_components": len(universe),
                 "projected_cost_over_budget_full_job": proj_full,
                 "projected_gpu_hours_full_job": proj_full / cost_rate / 3600.0 * world if cost_rate > 0 else None,

@@ -48,6 +48,10 @@ extern "C" {
  * against rate * remaining) instead of probability space (1 - u against e^{-rate*remaining},
  * no logarithm); same draws and outcomes up to ulp ties (A/B testing only). */
 #define EXPMC_SAMPLER_FLAG_LOG_HOLD 2u
+/* SCREEN_EACH: the event-driven sampler's chunk kernel tests every sample's first draw for
+ * "never leaves the entry" (one Philox block per sample) instead of locating the chunk's
+ * jumpers by geometric gaps between them (same law; A/B testing only). */
+#define EXPMC_SAMPLER_FLAG_SCREEN_EACH 4u
 
 /* Sampling lanes of the reference's Philox key (mlmc.cpp:94-96).  ENTRY estimates
  * (e^{tA}u)_entry; FORWARD estimates sum_i (e^{tA}u)_i from paths started at a state drawn
@@ -189,6 +193,12 @@ int expmc_ctx_set_load(expmc_ctx* ctx, const double* load);
  * jump_cdf, jump_target [n_edges], sign [n_edges]; any pointer may be NULL. */
 int expmc_ctx_export_tables(const expmc_ctx* ctx, double* d, double* rate, int64_t* row_ptr,
                             double* jump_cdf, int64_t* jump_target, uint8_t* sign);
+/* Alias records of the event-driven sampler (built when EXPMC_SAMPLER_EVENT is selected on a
+ * matrix with non-uniform rows; none otherwise): per edge slot e, prob[e] and the two target
+ * words self[e] / alias[e] (column, or -(column + 1) for a negative entry).  `rows` receives the
+ * number of non-uniform rows; the array pointers may be null.  Test / inspection only; no
+ * reference counterpart (the reference samples from the CDF, chain.cpp:49-58, paths.cpp:57-63). */
+int expmc_ctx_export_alias(const expmc_ctx* ctx, double* prob, int64_t* self, int64_t* alias, uint64_t* rows);
 int expmc_ctx_get_counters(const expmc_ctx* ctx, expmc_counters* out);
 /* Select the path sampler (EXPMC_SAMPLER_REFERENCE / EXPMC_SAMPLER_EVENT) for all later calls. */
 int expmc_ctx_set_sampler(expmc_ctx* ctx, int32_t mode);

@@ -86,6 +86,7 @@ SYMBOLS = [
     ("expmc_ctx_set_vector", C.c_int, [_P, _P]),
     ("expmc_ctx_set_load", C.c_int, [_P, _P]),
     ("expmc_ctx_export_tables", C.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    ("expmc_ctx_export_alias", C.c_int, [_P, _P, _P, _P, C.POINTER(_U64)]),
     ("expmc_ctx_get_counters", C.c_int, [_P, C.POINTER(CountersC)]),
     ("expmc_ctx_reset_counters", C.c_int, [_P]),
     ("expmc_ctx_get_stream", C.c_int, [_P, C.POINTER(_P)]),

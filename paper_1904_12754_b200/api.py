@@ -293,6 +293,13 @@ class Context:
         self._flags = (getattr(self, "_flags", 0) & ~2) | (2 if log else 0)
         _check(L.lib.expmc_ctx_set_sampler_flags(self._h, self._flags))
 
+    def set_screen_each(self, each: bool):
+        """Event sampler, entry mode: test every sample's first draw for "never leaves the
+        entry" (True) instead of locating the chunk's jumpers by geometric gaps (False, the
+        default) -- same law; A/B tests."""
+        self._flags = (getattr(self, "_flags", 0) & ~4) | (4 if each else 0)
+        _check(L.lib.expmc_ctx_set_sampler_flags(self._h, self._flags))
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             L.lib.expmc_ctx_destroy(self._h)
@@ -350,6 +357,19 @@ class Context:
         _check(L.lib.expmc_ctx_export_tables(self._h, _ptr(d), _ptr(rate), _ptr(rp), _ptr(cdf), _ptr(tgt), _ptr(sign)))
         return dict(d=d, rate=rate, row_ptr=rp, jump_cdf=cdf, jump_target=tgt, sign=sign, d_max=self.d_max,
                     d_bar=self.d_bar)
+
+    def alias_tables(self) -> dict | None:
+        """The event sampler's alias records of the non-uniform rows (None when none were built:
+        reference sampler, or every row uniform): per edge slot `prob`, and the target words
+        `self` / `alias` (column, or -(column + 1) for a negative entry)."""
+        rows = C.c_uint64()
+        _check(L.lib.expmc_ctx_export_alias(self._h, None, None, None, C.byref(rows)))
+        if rows.value == 0:
+            return None
+        m = self.n_edges
+        prob, own, alias = np.empty(m), np.empty(m, np.int64), np.empty(m, np.int64)
+        _check(L.lib.expmc_ctx_export_alias(self._h, _ptr(prob), _ptr(own), _ptr(alias), C.byref(rows)))
+        return dict(prob=prob, self=own, alias=alias, rows=int(rows.value))
 
     def counters(self) -> dict:
         c = L.CountersC()

@@ -60,7 +60,10 @@ struct expmc_ctx {
     RowRec* rows = nullptr;
     double* cdf = nullptr;     // per edge, read only for non-uniform rows
     uint32_t* tgt = nullptr;   // per edge: target | sign bit
-    EdgeTables edges() const { return EdgeTables{cdf, tgt}; }
+    AliasRec* alias = nullptr; // per edge, event sampler: alias records of the non-uniform rows
+    bool alias_checked = false;
+    uint64_t alias_rows = 0;   // non-uniform rows (0: every row picks exactly from its degree)
+    EdgeTables edges() const { return EdgeTables{cdf, tgt, alias}; }
 
     // batch staging, two slots so that one batch can be prepared / consumed on the host while
     // the other samples (expmc_b200::batch_launch / batch_finish; the driver's row cohorts)
@@ -202,6 +205,36 @@ void ensure_items(Staging& S, size_t nitems, cudaStream_t st) {
 }
 
 void bind(const expmc_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+// Alias records of the non-uniform rows (event-driven sampler; AliasRec, k_build_alias), built
+// once per context on first selecting the event sampler.  Uniform rows (Laplacians, adjacency
+// matrices) pick exactly from their degree and need none: no memory unless some row is
+// non-uniform.
+void ensure_alias(expmc_ctx* c) {
+    if (c->alias_checked) return;
+    bind(c);
+    unsigned long long* d_count = nullptr;
+    dev_alloc(&d_count, 1, c->stream);
+    launch_count_nonuniform(c->n, c->rows, d_count, c->stream);
+    unsigned long long count = 0;
+    cuda_check(cudaMemcpyAsync(&count, d_count, sizeof count, cudaMemcpyDeviceToHost, c->stream), "D2H count");
+    cuda_check(cudaStreamSynchronize(c->stream), "count non-uniform rows");
+    dev_free(d_count, c->stream);
+    c->alias_rows = count;
+    if (count > 0 && c->nedges > 0) {
+        uint32_t* scratch = nullptr;
+        dev_alloc(&c->alias, c->nedges, c->stream);
+        dev_alloc(&scratch, c->nedges, c->stream);
+        cuda_check(cudaMemsetAsync(c->alias, 0, c->nedges * sizeof(AliasRec), c->stream), "memset alias");  // uniform rows
+        launch_build_alias(c->n, c->rows, c->edges(), c->alias, scratch, c->stream);
+        c->ctr.kernel_launches += 1;
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        dev_free(scratch, c->stream);
+        cuda_check(e, "build alias tables");
+    }
+    c->ctr.kernel_launches += 1;
+    c->alias_checked = true;
+}
 
 // NCCL is resolved at run time, only when sample sharding is requested: the process may already
 // hold a libnccl.so.2 (PyTorch ships its own), and a link-time dependency would bind whichever
@@ -821,7 +854,7 @@ void expmc_ctx_destroy(expmc_ctx* c) {
         }
     }
     for (void* p : {static_cast<void*>(c->rows), static_cast<void*>(c->cdf), static_cast<void*>(c->tgt),
-                    static_cast<void*>(c->d_pf), static_cast<void*>(c->d_pu), static_cast<void*>(c->d_counter),
+                    static_cast<void*>(c->alias), static_cast<void*>(c->d_pf), static_cast<void*>(c->d_pu), static_cast<void*>(c->d_counter),
                     static_cast<void*>(c->d_init_cdf), static_cast<void*>(c->d_init_guide),
                     static_cast<void*>(c->d_load), static_cast<void*>(c->d_dbg)})
         dev_free(p, st);  // back to the device pool, in stream order
@@ -844,7 +877,8 @@ int expmc_ctx_get_info(const expmc_ctx* c, expmc_ctx_info* out) {
         out->d_bar = c->d_bar;
         out->device = c->device;
         out->num_sms = c->num_sms;
-        out->table_bytes = static_cast<uint64_t>(c->n) * sizeof(RowRec) + c->nedges * (sizeof(double) + sizeof(uint32_t));
+        out->table_bytes = static_cast<uint64_t>(c->n) * sizeof(RowRec) + c->nedges * (sizeof(double) + sizeof(uint32_t)) +
+                           (c->alias ? c->nedges * sizeof(AliasRec) : 0);
     });
 }
 
@@ -897,6 +931,27 @@ int expmc_ctx_export_tables(const expmc_ctx* c, double* d, double* rate, int64_t
     });
 }
 
+int expmc_ctx_export_alias(const expmc_ctx* c, double* prob, int64_t* self, int64_t* alias, uint64_t* rows) {
+    return guarded([&] {
+        need(c != nullptr, EXPMC_EINVAL, "null context");
+        if (rows) *rows = c->alias_rows;
+        if (!prob && !self && !alias) return;
+        need(c->alias != nullptr, EXPMC_EINVAL, "no alias table (select the event sampler on a matrix with non-uniform rows)");
+        bind(c);
+        const uint64_t m = c->nedges;
+        double* dp = nullptr;
+        int64_t *ds = nullptr, *da = nullptr;
+        dev_alloc(&dp, m, c->stream); dev_alloc(&ds, m, c->stream); dev_alloc(&da, m, c->stream);
+        launch_export_alias(m, c->alias, dp, ds, da, c->stream);
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        if (e == cudaSuccess && prob) e = cudaMemcpy(prob, dp, m * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && self) e = cudaMemcpy(self, ds, m * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && alias) e = cudaMemcpy(alias, da, m * 8, cudaMemcpyDeviceToHost);
+        for (void* p : {static_cast<void*>(dp), static_cast<void*>(ds), static_cast<void*>(da)}) dev_free(p, c->stream);
+        cuda_check(e, "export alias");
+    });
+}
+
 int expmc_ctx_get_counters(const expmc_ctx* c, expmc_counters* out) {
     return guarded([&] {
         need(c && out, EXPMC_EINVAL, "null argument");
@@ -910,13 +965,16 @@ int expmc_ctx_set_sampler(expmc_ctx* c, int32_t mode) {
         need(mode == EXPMC_SAMPLER_REFERENCE || mode == EXPMC_SAMPLER_EVENT, EXPMC_EINVAL, "unknown sampler mode");
         c->sampler = mode;
         c->sampler_grid = mode == EXPMC_SAMPLER_EVENT ? c->sampler_grid_ed : c->sampler_grid_ref;
+        if (mode == EXPMC_SAMPLER_EVENT) ensure_alias(c);
     });
 }
 
 int expmc_ctx_set_sampler_flags(expmc_ctx* c, uint32_t flags) {
     return guarded([&] {
         need(c != nullptr, EXPMC_EINVAL, "null context");
-        need((flags & ~(EXPMC_SAMPLER_FLAG_FULL_HOLD | EXPMC_SAMPLER_FLAG_LOG_HOLD)) == 0u, EXPMC_EINVAL,
+        need((flags & ~(EXPMC_SAMPLER_FLAG_FULL_HOLD | EXPMC_SAMPLER_FLAG_LOG_HOLD | EXPMC_SAMPLER_FLAG_SCREEN_EACH)) ==
+                 0u,
+             EXPMC_EINVAL,
              "unknown sampler flag");
         c->sampler_flags = flags;
     });

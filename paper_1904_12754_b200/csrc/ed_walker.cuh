@@ -28,6 +28,18 @@
 // event computes, without its log, divide, segment sums and exp.  On C3/C4 (t = 1/lambda)
 // over 95 % of samples never jump.  Draws near the boundary and every later event take the
 // full path.  EXPMC_SAMPLER_FLAG_FULL_HOLD switches the shortcut off (A/B tests).
+//
+// Geometric screening (entry mode, chunk kernel k_sample_grouped): testing every sample's
+// first draw costs a Philox block per sample, and on C3/C4 95 % of them only learn that the
+// sample stays at the entry.  Whether a sample is held is a Bernoulli(p) event with
+// p = P(M < m_safe) = (m_safe - 1) 2^-53, independent across samples, so the chunk's jumpers
+// are located directly: the gaps between consecutive jumpers are Geometric(1 - p),
+// G = floor(log(U) / log(p)), drawn 32 at a time from a per-chunk Philox stream (lane
+// kSkipLane of the item's key, counter = chunk index) and placed by a warp prefix sum.  A
+// listed jumper's first draw must then follow the law of M given M >= m_safe: its own stream's
+// first word is mapped onto [m_safe, 2^53] (kCond, ed_event).  Same path law, one Philox block
+// per 32 gaps instead of per sample.  Used when p > kSkipMinHeld; EXPMC_SAMPLER_FLAG_SCREEN_EACH
+// restores the per-sample screen (A/B tests).
 #pragma once
 
 #ifndef EXPMC_SAMPLER_MINB
@@ -39,6 +51,10 @@
 namespace expmc_b200 {
 
 constexpr uint32_t kFresh = 2u;
+constexpr uint32_t kCond = 4u;        // first draw conditioned on leaving the entry (geometric screen)
+constexpr uint32_t kSkipLane = 5u;    // Philox lane of the per-chunk gap stream (0-3, 6, 7 are taken)
+constexpr double kSkipMinHeld = 0.75; // geometric screening when P(held) exceeds this
+constexpr uint32_t kFlagGrouped = 1u << 31;  // prepare() called by k_sample_grouped (internal flag bit)
 
 struct EdWalker {
     Stream st;
@@ -62,7 +78,9 @@ __device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const
     w.cur = F ? load_row(rows, s0) : ic.r0;  // entry mode: the item's row (EdPolicy::prepare)
     w.state = s0;
     w.sign = 1;
-    w.dconst = 1u | kFresh;
+    // a sample listed by the geometric screen (k_sample_grouped) draws its first hold
+    // conditioned on leaving the entry; otherwise the closed-form first-hold test applies
+    w.dconst = 1u | (ic.skip_scale != 0.0 ? kCond : kFresh);
     w.kcur = 0;
     w.t = 0.0;
     w.acc_a = 0.0;
@@ -95,13 +113,19 @@ __device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const
                                          const EdgeTables& edges, const LogEntry* s_log, unsigned long long& draws,
                                          unsigned long long& jumps) {
     stream_reserve2(w.st);
-    if (w.dconst & kFresh) {
-        w.dconst &= ~kFresh;
-        if ((uint64_t{1} << 53) - (w.st.w0 >> 11) < ic.m_safe) {  // holds past beta at the entry
+    if (w.dconst & (kFresh | kCond)) {
+        if (w.dconst & kCond) {
+            // listed by the geometric screen: M uniform on [m_safe, 2^53] from the first word
+            const uint64_t range = (uint64_t{1} << 53) - ic.m_safe + 1u;
+            const uint64_t m = ic.m_safe + __umul64hi(w.st.w0, range);
+            w.st.w0 = ((uint64_t{1} << 53) - m) << 11;  // K = 2^53 - M
+        } else if ((uint64_t{1} << 53) - (w.st.w0 >> 11) < ic.m_safe) {  // holds past beta at the entry
+            w.dconst &= ~kFresh;
             draws += ic.nsteps;  // ed_segment(0, N) on a non-absorbing row
             w.sign = 0;          // marks the closed-form path for ed_sample / record
             return true;
         }
+        w.dconst &= ~(kFresh | kCond);
     }
     double tjump = INFINITY;
     if (w.cur.rate != 0.0) {
@@ -123,7 +147,7 @@ __device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const
     w.t = tjump;
     ++jumps;
     ++draws;  // the accepted holding-time draw of the jump (paths.cpp:51-54)
-    const uint32_t ts = pick_edge(edges, w.cur.begin, w.cur.deg, stream_pop_bits(w.st));
+    const uint32_t ts = pick_edge<true>(edges, w.cur.begin, w.cur.deg, stream_pop_bits(w.st));
     if (ts & kSignBit) w.sign = -w.sign;
     w.state = ts & kTargetMask;
     w.cur = load_row(rows, w.state);
@@ -210,6 +234,7 @@ struct EdPolicy {
     // The closed-form first hold (header): threshold and stay-at-entry values, once per chunk.
     static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData& ld,
                                                    uint32_t flags) {
+        ic.skip_scale = 0.0;
         if (F) return;
         const Row r = load_row(rows, ic.entry);
         ic.r0 = r;
@@ -232,6 +257,10 @@ struct EdPolicy {
         ed_finish<false>(w, ic, ld, rows, ic.hold_fine, ic.hold_coarse);
         ic.hold_x = ic.base ? ic.hold_fine : 0.0;  // ed_sample's coupled constant-d case
         ic.m_safe = static_cast<uint64_t>(m);
+        // P(held) = #{M in 1..2^53 : M < m_safe} / 2^53, exact in fp64 (m_safe < 2^53)
+        const double p_held = __dmul_rn(static_cast<double>(ic.m_safe - 1u), 0x1.0p-53);
+        if ((flags & kFlagGrouped) && !(flags & EXPMC_SAMPLER_FLAG_SCREEN_EACH) && p_held > kSkipMinHeld)
+            ic.skip_scale = 1.0 / log(p_held);
     }
     static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
                                                  uint64_t s) {

@@ -45,9 +45,22 @@ constexpr uint32_t kDegMask = 0x7FFFFFFFu;
 constexpr uint32_t kSignBit = 0x80000000u;
 constexpr uint32_t kTargetMask = 0x7FFFFFFFu;
 
+// Per-edge-slot alias record of a non-uniform row (Walker / Vose alias method), built on the
+// device for the event-driven sampler (csrc/kernels.cu k_build_alias).  A jump in a row of
+// degree deg draws slot j = floor(v deg) and keeps the slot's own target when the fraction
+// v deg - j is below prob, else takes its alias: one 16-B load instead of a binary search
+// over the row's CDF.  Both target words carry the sign bit like tgt[].
+struct alignas(16) AliasRec {
+    double prob;     // probability of keeping the slot's own target
+    uint32_t self;   // tgt[begin + j]
+    uint32_t alias;  // tgt[begin + alias(j)]
+};
+static_assert(sizeof(AliasRec) == 16, "alias record must be one 128-bit load");
+
 struct EdgeTables {
     const double* cdf;
     const uint32_t* tgt;
+    const AliasRec* alias;  // per edge slot, non-uniform rows only (nullptr: none built)
 };
 
 // One device work item = one run_level request with count > 0.
@@ -159,6 +172,12 @@ void launch_export(int64_t n, const RowRec* rows, double* d, double* rate, int64
                    cudaStream_t s);
 void launch_export_edges(uint64_t e, EdgeTables edges, double* cdf, int64_t* target,
                          uint8_t* sign, cudaStream_t s);
+// alias tables of the non-uniform rows: count them, then build (scratch: one u32 per edge)
+void launch_count_nonuniform(int64_t n, const RowRec* rows, unsigned long long* count, cudaStream_t s);
+void launch_build_alias(int64_t n, const RowRec* rows, EdgeTables edges, AliasRec* alias, uint32_t* scratch,
+                        cudaStream_t s);
+void launch_export_alias(uint64_t e, const AliasRec* alias, double* prob, int64_t* self, int64_t* alias_target,
+                         cudaStream_t s);
 // scans / reductions (CUB): exclusive sum of n u64, max / sum of RowRec::d
 size_t scan_temp_bytes(int64_t n);
 void exclusive_scan_u64(const uint64_t* in, uint64_t* out, int64_t n, void* tmp, size_t tmp_bytes,

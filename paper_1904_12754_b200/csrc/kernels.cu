@@ -236,6 +236,41 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
     }
 }
 
+// Geometric screen of one chunk (ed_walker.cuh): append the chunk's jumpers to the warp's work
+// list wl[nwork..] as (slot << 9) | offset and return the new list length.  Gaps come 32 at a
+// time from the chunk's own Philox stream (lane kSkipLane, counter = absolute chunk index) and
+// are placed by a warp prefix sum.  One accurate log per 32 gaps (libdevice: off the hot path).
+__device__ __forceinline__ uint32_t geometric_screen(const ItemConst& ic, uint64_t chunk, uint32_t cnt, uint32_t slot,
+                                                     uint16_t* wl, uint32_t nwork) {
+    const unsigned full = 0xFFFFFFFFu;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t k3 = (ic.key3 & 0x00FFFFFFu) | (kSkipLane << 24);
+    const uint32_t k0 = static_cast<uint32_t>(ic.seed), k1 = static_cast<uint32_t>(ic.seed >> 32);
+    const double scale = ic.skip_scale;
+    uint32_t pos = 0;
+    for (uint32_t it = 0; pos < cnt; ++it) {  // warp-uniform
+        uint32_t c0 = it * 32u + lane, c1 = static_cast<uint32_t>(chunk), c2 = static_cast<uint32_t>(chunk >> 32), c3 = k3;
+        philox10(c0, c1, c2, c3, k0, k1);
+        const uint64_t k53 = ((static_cast<uint64_t>(c2) << 32) | c3) >> 11;  // rng.hpp:32-35
+        // U = M 2^-53 in (0, 1]; G = floor(log U / log p) >= 0, capped (only G < cnt matters)
+        const double lu = log(__dmul_rn(static_cast<double>((uint64_t{1} << 53) - k53), 0x1.0p-53));
+        const double gf = __dmul_rn(lu, scale);
+        uint32_t incl = (gf < 1048576.0 ? static_cast<uint32_t>(gf) : 1048576u) + 1u;  // gap + 1
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {  // inclusive warp prefix sum
+            const uint32_t y = __shfl_up_sync(full, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        const uint32_t p = pos + incl - 1u;  // this lane's jumper
+        const bool jump = p < cnt;
+        const unsigned need = __ballot_sync(full, jump);
+        if (jump) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>((slot << 9) | p);
+        nwork += __popc(need);
+        pos += __shfl_sync(full, incl, 31);
+    }
+    return nwork;
+}
+
 // Screened event sampler, chunk groups (EdPolicy<false>, sums): a warp claims an aligned group
 // of kGroup consecutive chunks of its window and screens all of an item's chunks in the group before it runs the
 // walker loop, so the few samples that jump (5-10 % on C3/C4) fill the lanes of one walker pass
@@ -248,8 +283,15 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
 #endif
 constexpr uint32_t kGroup = EXPMC_GROUP;
 
+// The grouped kernel runs at 3 blocks per SM (85 registers): its walker loop spills at 64 once
+// the geometric screen shares the kernel (C4 65,536-component step 142 -> 136 ms, C3 1486 ->
+// 1375 ms against 4 blocks per SM; profiles/r02/SUMMARY.md).
+#ifndef EXPMC_GROUPED_MINB
+#define EXPMC_GROUPED_MINB 3
+#endif
+
 template <class P>
-__global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(SamplerArgs a) {
+__global__ void __launch_bounds__(kThreads, EXPMC_GROUPED_MINB) k_sample_grouped(SamplerArgs a) {
     static_assert(P::kScreen && !P::kExtra, "grouped chunks: screened policies only");
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t wid = threadIdx.x >> 5;
@@ -262,7 +304,16 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(Samp
     __syncthreads();
     __shared__ ItemConst s_ic[kWarps];
     ItemConst& ic = s_ic[wid];
-    uint32_t hint = 0;
+    // The portion cursor lives in shared memory, not registers: it is dead during the walker
+    // loop, which needs every register it can get (64 at 4 blocks per SM).
+    struct Cursor {
+        uint64_t gq, ghi;            // the claimed group's first chunk id, end of its window part
+        unsigned long long nsamp;    // samples of the current portion
+        uint32_t j, j0, hint;        // next slot, the portion's first slot, find_item hint
+    };
+    __shared__ Cursor s_cur[kWarps];
+    Cursor& cur = s_cur[wid];
+    if (lane == 0) cur.hint = 0;
     // Groups are aligned blocks of kGroup absolute chunk ids, dealt to the ranks of a sample-
     // sharded run whole (group q on rank q % world): the portions -- and so every chunk
     // partial -- are the same for any GPU count, and the all-reduced window is the one-GPU one.
@@ -273,46 +324,67 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(Samp
         uint32_t gi = 0;
         if (lane == 0) gi = atomicAdd(a.counter, 1u);
         gi = __shfl_sync(full, gi, 0);
-        const uint64_t q = qown + static_cast<uint64_t>(gi) * a.shard_world;
-        const uint64_t gq = q * kGroup;  // first chunk id of the group
-        if (gq >= a.g_end) return;
-        const uint64_t glo = gq > a.g_begin ? gq : a.g_begin;
-        const uint64_t ghi = gq + kGroup < a.g_end ? gq + kGroup : a.g_end;
-        uint32_t j = static_cast<uint32_t>(glo - gq);
-        while (gq + j < ghi) {
-            const uint64_t gp = gq + j;  // first chunk of this portion
-            const uint32_t item = find_item(a.chunk0, a.nitems, gp, hint);
-            hint = item;
+        {
+            const uint64_t gq = (qown + static_cast<uint64_t>(gi) * a.shard_world) * kGroup;  // first chunk id
+            if (gq >= a.g_end) return;
+            const uint64_t glo = gq > a.g_begin ? gq : a.g_begin;
             if (lane == 0) {
-                ItemConst c = load_item(a.items, item);
-                P::prepare(c, a.rows, a.init, a.flags);
-                ic = c;
+                cur.gq = gq;
+                cur.ghi = gq + kGroup < a.g_end ? gq + kGroup : a.g_end;
+                cur.j = static_cast<uint32_t>(glo - gq);
             }
             __syncwarp();
-            const DevItem& it = a.items[item];
-            const uint64_t first = it.first, end = it.first + it.count;
-            const uint64_t item_g1 = a.chunk0[item + 1];
-            // ---- screen the portion: the group's chunks of this item
-            const uint32_t j0 = j;
+        }
+        for (;;) {
             uint32_t nwork = 0, nheld = 0;
-            unsigned long long nsamp = 0;
-            for (; gq + j < ghi; ++j) {
-                const uint64_t g = gq + j;
-                if (g >= item_g1) break;
-                const uint64_t chunk = first / kChunk + (g - a.chunk0[item]);
-                const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
-                const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
-                const uint32_t cnt = hi > lo ? static_cast<uint32_t>(hi - lo) : 0u;  // parallel.hpp:46-49
-                if (lane == 0) s_lo[wid][j] = lo;
-                nsamp += cnt;
-                for (uint32_t q0 = 0; q0 < cnt; q0 += 32u) {
-                    const uint32_t qq = q0 + lane;
-                    const bool valid = qq < cnt;
-                    const bool held = valid && ic.m_safe != 0 && P::screen(ic, lo + qq);
-                    nheld += held;
-                    const unsigned need = __ballot_sync(full, valid && !held);
-                    if (valid && !held) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>((j << 9) | qq);
-                    nwork += __popc(need);
+            {
+                const uint64_t gq = cur.gq, ghi = cur.ghi;
+                uint32_t j = cur.j;
+                if (gq + j >= ghi) break;
+                const uint32_t item = find_item(a.chunk0, a.nitems, gq + j, cur.hint);
+                __syncwarp();
+                if (lane == 0) {
+                    cur.hint = item;
+                    ItemConst c = load_item(a.items, item);
+                    P::prepare(c, a.rows, a.init, a.flags | kFlagGrouped);
+                    ic = c;
+                }
+                __syncwarp();
+                const DevItem& it = a.items[item];
+                const uint64_t first = it.first, end = it.first + it.count;
+                const uint64_t item_g1 = a.chunk0[item + 1];
+                // ---- screen the portion: the group's chunks of this item
+                const uint32_t j0 = j;
+                unsigned long long nsamp = 0;
+                for (; gq + j < ghi; ++j) {
+                    const uint64_t g = gq + j;
+                    if (g >= item_g1) break;
+                    const uint64_t chunk = first / kChunk + (g - a.chunk0[item]);
+                    const uint64_t lo = first > chunk * kChunk ? first : chunk * kChunk;
+                    const uint64_t hi = end < (chunk + 1) * kChunk ? end : (chunk + 1) * kChunk;
+                    const uint32_t cnt = hi > lo ? static_cast<uint32_t>(hi - lo) : 0u;  // parallel.hpp:46-49
+                    if (lane == 0) s_lo[wid][j] = lo;
+                    nsamp += cnt;
+                    if (ic.skip_scale != 0.0) {
+                        const uint32_t n1 = geometric_screen(ic, chunk, cnt, j, wl, nwork);
+                        if (lane == 0) nheld += cnt - (n1 - nwork);
+                        nwork = n1;
+                        continue;
+                    }
+                    for (uint32_t q0 = 0; q0 < cnt; q0 += 32u) {
+                        const uint32_t qq = q0 + lane;
+                        const bool valid = qq < cnt;
+                        const bool held = valid && ic.m_safe != 0 && P::screen(ic, lo + qq);
+                        nheld += held;
+                        const unsigned need = __ballot_sync(full, valid && !held);
+                        if (valid && !held) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>((j << 9) | qq);
+                        nwork += __popc(need);
+                    }
+                }
+                if (lane == 0) {
+                    cur.j0 = j0;
+                    cur.j = j;
+                    cur.nsamp = nsamp;
                 }
             }
             __syncwarp();
@@ -346,7 +418,8 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(Samp
                 }
                 next += __popc(fin);
             }
-            if (lane == 0) cost += nsamp * ic.nsteps;  // the fine steps of every sample
+            __syncwarp();  // the cursor is re-read from shared memory, not held across the loop
+            if (lane == 0) cost += cur.nsamp * ic.nsteps;  // the fine steps of every sample
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 sum = __dadd_rn(sum, __shfl_xor_sync(full, sum, o));
@@ -355,15 +428,17 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample_grouped(Samp
                 jumps += __shfl_xor_sync(full, jumps, o);
             }
             // portion totals on its first chunk, zeros on the rest
-            for (uint32_t t = j0 + lane; t < j; t += 32u) {
-                const uint64_t k = gq + t - a.g_begin;
+            const uint32_t j0 = cur.j0, j1 = cur.j;
+            const uint64_t k0 = cur.gq - a.g_begin;
+            for (uint32_t t = j0 + lane; t < j1; t += 32u) {
+                const uint64_t k = k0 + t;
                 const bool head = t == j0;
                 a.partials.sum[k] = head ? sum : 0.0;
                 a.partials.sum_sq[k] = head ? sum_sq : 0.0;
                 a.partials.cost[k] = head ? cost : 0ull;
                 a.partials.jumps[k] = head ? jumps : 0ull;
             }
-            __syncwarp();  // ic and the list are rewritten by the next portion
+            __syncwarp();  // ic, the cursor and the list are rewritten by the next portion
         }
     }
 }
@@ -746,6 +821,80 @@ __global__ void k_export_edges(uint64_t m, EdgeTables edges, double* cdf, int64_
     if (sign) sign[i] = (t & kSignBit) ? 1 : 0;
 }
 
+// ---- alias tables (event-driven sampler, non-uniform rows; AliasRec in internal.hpp)
+__device__ __forceinline__ bool needs_alias(uint32_t degf) {
+    return !(degf & kUniformRow) && (degf & kDegMask) > 1u;
+}
+
+__global__ void k_count_nonuniform(int64_t n, const RowRec* __restrict__ rows, unsigned long long* count) {
+    unsigned long long c = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        c += needs_alias(rows[i].deg);
+    c = warp_sum_u64(c);
+    if ((threadIdx.x & 31u) == 0 && c) atomicAdd(count, c);
+}
+
+// Vose's alias method, one thread per row, in place over the row's slots: q_j = p_j deg with
+// p_j = cdf_j - cdf_{j-1} (the row's transition probabilities as the reference's CDF stores
+// them, chain.cpp:49-58); slots with q < 1 ("small") and q >= 1 ("large") are kept as two
+// stacks at the two ends of the row's scratch range; each small slot is topped up by the
+// large slot on top of its stack, which gives away 1 - q_s and moves to the small stack when
+// it falls below 1.  Leftovers (rounding) keep their own target with probability 1.  The row's
+// implied law (prob_j + sum_{i: alias(i) = j} (1 - prob_i)) / deg equals p_j to rounding
+// (tests/test_alias.py).  O(deg) per row; hub rows take one thread longer, once per context.
+__global__ void k_build_alias(int64_t n, const RowRec* __restrict__ rows, EdgeTables e, AliasRec* __restrict__ al,
+                              uint32_t* __restrict__ scratch) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t degf = rows[i].deg;
+    if (!needs_alias(degf)) return;
+    const uint32_t b = rows[i].begin, deg = degf & kDegMask;
+    const double fdeg = static_cast<double>(deg);
+    uint32_t ns = 0, nl = 0;
+    double prev = 0.0;
+    for (uint32_t j = 0; j < deg; ++j) {
+        const double c = e.cdf[b + j];
+        const double q = __dmul_rn(__dsub_rn(c, prev), fdeg);
+        prev = c;
+        al[b + j].prob = q;
+        al[b + j].alias = j;
+        if (q < 1.0) scratch[b + ns++] = j;
+        else scratch[b + deg - 1u - nl++] = j;
+    }
+    while (ns > 0u && nl > 0u) {
+        const uint32_t sm = scratch[b + --ns];
+        const uint32_t lg = scratch[b + deg - nl];  // top of the large stack
+        al[b + sm].alias = lg;                       // prob[sm] stays q_sm
+        const double ql = __dsub_rn(__dadd_rn(al[b + lg].prob, al[b + sm].prob), 1.0);
+        al[b + lg].prob = ql;
+        if (ql < 1.0) {
+            --nl;
+            scratch[b + ns++] = lg;
+        }
+    }
+    while (nl > 0u) al[b + scratch[b + deg - nl--]].prob = 1.0;
+    while (ns > 0u) al[b + scratch[b + --ns]].prob = 1.0;
+    for (uint32_t j = 0; j < deg; ++j) {  // slot indices -> target words
+        AliasRec r = al[b + j];
+        r.self = e.tgt[b + j];
+        r.alias = r.prob < 1.0 ? e.tgt[b + r.alias] : r.self;
+        al[b + j] = r;
+    }
+}
+
+__global__ void k_export_alias(uint64_t m, const AliasRec* __restrict__ al, double* prob, int64_t* self,
+                               int64_t* alias_target) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const AliasRec r = al[i];
+    prob[i] = r.prob;
+    // target | sign as a signed word: -(target + 1) for a negative entry
+    self[i] = (r.self & kSignBit) ? -static_cast<int64_t>(r.self & kTargetMask) - 1 : static_cast<int64_t>(r.self);
+    alias_target[i] =
+        (r.alias & kSignBit) ? -static_cast<int64_t>(r.alias & kTargetMask) - 1 : static_cast<int64_t>(r.alias);
+}
+
 // d_max / d_sum: fixed two-level tree (block partials, then one block) -> deterministic.
 constexpr int kRedThreads = 256;
 constexpr int kRedBlocks = 1024;
@@ -947,6 +1096,27 @@ void launch_export_edges(uint64_t m, EdgeTables edges, double* cdf, int64_t* tar
     if (m == 0) return;
     k_export_edges<<<grid_for(static_cast<int64_t>(m), 256), 256, 0, s>>>(m, edges, cdf, target, sign);
     cuda_check(cudaGetLastError(), "k_export_edges launch");
+}
+
+void launch_count_nonuniform(int64_t n, const RowRec* rows, unsigned long long* count, cudaStream_t s) {
+    cuda_check(cudaMemsetAsync(count, 0, sizeof(unsigned long long), s), "memset count");
+    if (n == 0) return;
+    k_count_nonuniform<<<std::min<int64_t>(grid_for(n, 256), 4096), 256, 0, s>>>(n, rows, count);
+    cuda_check(cudaGetLastError(), "k_count_nonuniform launch");
+}
+
+void launch_build_alias(int64_t n, const RowRec* rows, EdgeTables edges, AliasRec* alias, uint32_t* scratch,
+                        cudaStream_t s) {
+    if (n == 0) return;
+    k_build_alias<<<grid_for(n, 128), 128, 0, s>>>(n, rows, edges, alias, scratch);
+    cuda_check(cudaGetLastError(), "k_build_alias launch");
+}
+
+void launch_export_alias(uint64_t m, const AliasRec* alias, double* prob, int64_t* self, int64_t* alias_target,
+                         cudaStream_t s) {
+    if (m == 0) return;
+    k_export_alias<<<grid_for(static_cast<int64_t>(m), 256), 256, 0, s>>>(m, alias, prob, self, alias_target);
+    cuda_check(cudaGetLastError(), "k_export_alias launch");
 }
 
 float bench_gather(uint64_t bytes, int loads_per_thread, int reps, int num_sms, uint64_t* total_loads) {

@@ -137,8 +137,20 @@ __device__ __forceinline__ Row load_row(const RowRec* __restrict__ rows, uint32_
 // does: the choice is the reference's in every case.  Generic rows of degree <= 4 read their
 // CDF with independent loads and count (#{j : cdf_j <= v} == upper_bound on a non-decreasing
 // array); wider rows binary-search.
+//
+// kAlias (event-driven sampler only: its parity is statistical): a non-uniform row with an
+// alias table draws slot j = floor(v deg) = hi64(K 2^11 deg) and keeps its own target iff the
+// fraction lo64(K 2^11 deg) 2^-64 is below prob_j -- one 16-B load, any degree.
+template <bool kAlias = false>
 __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53) {
     const uint32_t deg = degf & kDegMask;
+    if (kAlias && !(degf & kUniformRow) && e.alias != nullptr && deg > 1u) {
+        const uint64_t x = k53 << 11;
+        const uint32_t j = static_cast<uint32_t>(__umul64hi(x, deg));
+        const double f = __dmul_rn(__ull2double_rn((x * deg) >> 11), 0x1.0p-53);
+        const uint4 r = __ldg(reinterpret_cast<const uint4*>(e.alias + begin + j));
+        return f < __hiloint2double(static_cast<int>(r.y), static_cast<int>(r.x)) ? r.z : r.w;
+    }
     uint32_t k = 0;
     bool done = false;
     if ((degf & kUniformRow) && (deg & (deg - 1u)) == 0u) {
@@ -216,7 +228,10 @@ struct ItemConst {
     // reference-order walker: S-mode start value S0 2^53 for steps in rows of rate s0_rate
     double s0_rate;     // -1: no cached rate
     double s0_hold;
-    double smode_max_x; // rate dt below which a fresh step runs in S-mode (-1: T-mode only)
+    union {
+        double smode_max_x; // reference-order walker: rate dt below which a fresh step runs in S-mode (-1: T-mode only)
+        double skip_scale;  // event walker: 1 / log P(M < m_safe) < 0, jumpers located by geometric gaps
+    };                      //   (0: off; EdPolicy::prepare always writes it)
     Row r0;             // entry mode: the entry's row record and its fresh-step hold (the
     double h0;          //   restart of every sample reads them from here, not from the tables)
     double ea_key;      // base level: e^{ea_key} = ea_val, the exponent of a path that keeps the

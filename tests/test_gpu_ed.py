@@ -107,6 +107,7 @@ def test_ed_closed_form_first_hold_is_exact(gpu, level, base):
     u = rng.uniform(-1.0, 1.0, n)
     rows = np.array([0, 3, 7, 11, 39])
     with P.Context(a, u, sampler="event") as c:
+        c.set_screen_each(True)  # per-sample screen: the same draws as the full first event
         for beta in (0.05, 0.7):
             c.set_full_hold(False)
             fast = c.sample_debug(beta, rows[:, None].repeat(400, 1).ravel(), level, base,
@@ -132,3 +133,36 @@ def test_ed_closed_form_first_hold_is_exact(gpu, level, base):
                 mc[full_hold] = [P.mc_single_entry(c, int(e), 0.05, 0.05 / 8, 30_000, 9 + int(e)) for e in rows]
             for x, y in zip(mc[False], mc[True]):
                 assert (x.estimate, x.std_error, x.wall_cost, x.jumps) == (y.estimate, y.std_error, y.wall_cost, y.jumps)
+
+
+@pytest.mark.parametrize("level,base", [(0, 1), (3, 1), (1, 0), (4, 0)])
+def test_ed_geometric_screen_matches_per_sample_screen(gpu, level, base):
+    """The chunk kernel's geometric screen (jumpers located by Geometric gaps, their first draw
+    conditioned on leaving the entry; ed_walker.cuh) has the per-sample screen's law: level
+    means, mean unit cost and mean jumps agree at 4 combined SE on rows where most samples are
+    held (the screen is on), and the held count is exact in expectation."""
+    rng = np.random.default_rng(11)
+    n = 60
+    dense = np.where(rng.random((n, n)) < 0.08, rng.uniform(-1.0, 1.0, (n, n)), 0.0)
+    np.fill_diagonal(dense, rng.uniform(-1.5, 0.5, n))
+    a = P.SparseMatrix.from_dense(dense)
+    u = rng.uniform(-1.0, 1.0, n)
+    rows = np.array([0, 5, 17, 31, 44, 59])
+    m = 400_000
+    out = {}
+    for each in (False, True):
+        with P.Context(a, u, sampler="event") as c:
+            c.set_screen_each(each)
+            # first index not chunk-aligned: the first chunk is partial
+            out[each] = c.run_level_batch(0.08, rows, level, base, 100, m, 300 + rows)
+    g, e = out[False], out[True]
+    for k in range(len(rows)):
+        mg, me = g["sum"][k] / m, e["sum"][k] / m
+        vg = max(g["sum_sq"][k] / m - mg * mg, 0.0)
+        ve = max(e["sum_sq"][k] / m - me * me, 0.0)
+        se = math.sqrt((vg + ve) / m)
+        assert abs(mg - me) <= 4 * se + 1e-15, (rows[k], mg, me, se)
+        for key in ("jumps", "cost"):
+            # per-sample counts: Poisson-like, variance <= mean * (max per-sample count) -- a loose SE
+            a_, b_ = float(g[key][k]), float(e[key][k])
+            assert abs(a_ - b_) <= 4 * math.sqrt(2 * max(a_, b_) * (1 << (level + 2))) + 1, (key, rows[k], a_, b_)
