@@ -165,5 +165,6 @@ def make_config(name: str) -> Config:
         u = 2.0 * philox_first_uniform(VECTOR_SEED, 0, np.arange(a.n, dtype=np.uint64), 6) - 1.0
         return Config(name, a, u, 0.1, 1e-4,
                       f"3D 7-point convection-diffusion {g}^3 (cell Peclet 10 along x: off-diagonals +6/-4/1), "
-                      "t=0.1, v uniform [-1,1), eps=1e-4, 5 MLMC levels", max_levels_above_l0=4)
+                      "t=0.1, v uniform [-1,1), eps=1e-4, 5 MLMC levels", max_levels_above_l0=4,
+                      sampler="event")  # alias picks on its non-uniform rows (tests/test_alias.py)
     raise ValueError(f"unknown config {name!r}")

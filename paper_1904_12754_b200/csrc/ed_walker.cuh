@@ -209,6 +209,15 @@ struct RefPolicy {
                                                     const RowRec* rows, double&) {
         return walker_sample<F>(w, ic, ld, rows);
     }
+    static constexpr bool kDefer = true;  // sample() split into end_record() + value()
+    static __device__ __forceinline__ void end_record(const W& w, const ItemConst& ic, double& a, double& b,
+                                                      uint32_t& se) {
+        walker_end_record(w, ic, a, b, se);
+    }
+    static __device__ __forceinline__ double value(double a, double b, uint32_t se, const ItemConst& ic,
+                                                   const LaneData& ld, const RowRec* rows) {
+        return walker_value<F>(a, b, se, ic, ld, rows);
+    }
     static __device__ __forceinline__ void record(const W& w, const ItemConst& ic, const LaneData& ld,
                                                   const RowRec* rows, SampleOut& o) {
         walker_finish<F>(w, ic, ld, rows, o.fine, o.coarse);
@@ -221,6 +230,7 @@ struct RefPolicy {
 template <bool F>
 struct EdPolicy {
     using W = EdWalker;
+    static constexpr bool kDefer = false;
     static constexpr bool kExtra = false;
     static constexpr bool kScreen = !F;  // entry mode: all samples start in ic.entry
     // The first event's closed-form test alone: block 0 of the sample's stream, first word.

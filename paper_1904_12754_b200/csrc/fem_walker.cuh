@@ -134,6 +134,7 @@ __device__ __forceinline__ double fem_finish(const FemWalker& f, const ItemConst
 // the event-driven sampler has nothing to skip).
 struct FemPolicy {
     using W = FemWalker;
+    static constexpr bool kDefer = false;
     static constexpr bool kExtra = true;
     static constexpr bool kScreen = false;
     static __device__ __forceinline__ bool screen(const ItemConst&, uint64_t) { return false; }

@@ -88,10 +88,24 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+#ifndef EXPMC_DEFER
+#define EXPMC_DEFER 0
+#endif
+constexpr uint32_t kQueue = 64;  // deferred-finish ring per warp (pending < 32 + 32)
+
 template <class P, bool W>
 __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs a) {
     const uint32_t lane = threadIdx.x & 31u;
     const unsigned full = 0xFFFFFFFFu;
+    // Deferred finish (reference-order sums): a finishing lane queues its end record in shared
+    // memory and restarts at once; the values are computed 32 at a time by the whole warp
+    // instead of by the ~1/3 of the lanes that finish in a given trip.
+    constexpr bool kDefer = P::kDefer && !W && EXPMC_DEFER;
+    __shared__ double s_qa[kDefer ? kWarps * kQueue : 1], s_qb[kDefer ? kWarps * kQueue : 1];
+    __shared__ uint32_t s_qs[kDefer ? kWarps * kQueue : 1];
+    double* const qa = s_qa + (kDefer ? (threadIdx.x >> 5) * kQueue : 0);
+    double* const qb = s_qb + (kDefer ? (threadIdx.x >> 5) * kQueue : 0);
+    uint32_t* const qs = s_qs + (kDefer ? (threadIdx.x >> 5) * kQueue : 0);
     __shared__ double s_x[W ? kWarps * kChunk : 1];
     double* const wx = s_x + (W ? (threadIdx.x >> 5) * kChunk : 0);
     // screened policies: the chunk's slots that need the full walker, ascending
@@ -177,18 +191,29 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
             active = true;
         }
         uint32_t next = nwork < 32u ? nwork : 32u;
+        uint32_t qh = 0, qn = 0;  // deferred finish: ring head and pending records (warp-uniform)
         while (__any_sync(full, active)) {
             const bool done = active && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps);
             const unsigned fin = __ballot_sync(full, done);
             if (done) {
-                double ex;
-                const double x = P::sample(w, ic, a.init, a.rows, ex);
-                if constexpr (W) {
-                    wx[my] = x;
+                if constexpr (kDefer) {
+                    double ra, rb;
+                    uint32_t se;
+                    P::end_record(w, ic, ra, rb, se);
+                    const uint32_t slot = (qh + qn + __popc(fin & lanemask_lt())) & (kQueue - 1u);
+                    qa[slot] = ra;
+                    qb[slot] = rb;
+                    qs[slot] = se;
                 } else {
-                    sum = __dadd_rn(sum, x);
-                    sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
-                    if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
+                    double ex;
+                    const double x = P::sample(w, ic, a.init, a.rows, ex);
+                    if constexpr (W) {
+                        wx[my] = x;
+                    } else {
+                        sum = __dadd_rn(sum, x);
+                        sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
+                        if constexpr (P::kExtra) extra = __dadd_rn(extra, ex);
+                    }
                 }
                 const uint32_t mine = next + __popc(fin & lanemask_lt());
                 if (mine < nwork) {
@@ -199,6 +224,29 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
                 }
             }
             next += __popc(fin);
+            if constexpr (kDefer) {
+                qn += __popc(fin);
+                if (qn >= 32u) {  // a converged pass over 32 records
+                    __syncwarp();
+                    const uint32_t slot = (qh + lane) & (kQueue - 1u);
+                    const double x = P::value(qa[slot], qb[slot], qs[slot], ic, a.init, a.rows);
+                    sum = __dadd_rn(sum, x);
+                    sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
+                    qh = (qh + 32u) & (kQueue - 1u);
+                    qn -= 32u;
+                    __syncwarp();  // the slots are rewritten by later finishes
+                }
+            }
+        }
+        if constexpr (kDefer) {  // drain the ring
+            __syncwarp();
+            if (lane < qn) {
+                const uint32_t slot = (qh + lane) & (kQueue - 1u);
+                const double x = P::value(qa[slot], qb[slot], qs[slot], ic, a.init, a.rows);
+                sum = __dadd_rn(sum, x);
+                sum_sq = __dadd_rn(sum_sq, __dmul_rn(x, x));
+            }
+            __syncwarp();
         }
         if constexpr (W) {  // WelfordAcc::add over the chunk in sample order (parallel.hpp:86-92)
             __syncwarp();

@@ -470,6 +470,27 @@ __device__ __forceinline__ double walker_sample(const Walker& w, const ItemConst
     return __dsub_rn(__dmul_rn(uf, dexp(__dadd_rn(acc_a, acc_b))), __dmul_rn(uf, ea));
 }
 
+// Deferred finish (k_sample, EXPMC_DEFER): the finishing lane records only its last step's sums
+// and its packed end (state | sign bit); the value -- walker_sample's arithmetic, same operation
+// order -- is computed later from that record by a converged pass of the warp.
+__device__ __forceinline__ void walker_end_record(const Walker& w, const ItemConst& ic, double& a, double& b,
+                                                  uint32_t& se) {
+    last_step_sums(w, ic, a, b);
+    se = w.state | (w.sign < 0 ? kSignBit : 0u);
+}
+
+template <bool F>
+__device__ __forceinline__ double walker_value(double acc_a, double acc_b, uint32_t se, const ItemConst& ic,
+                                               const LaneData& fi, const RowRec* __restrict__ rows) {
+    if (!ic.base && acc_b == 0.0) return 0.0;
+    const double sg = (se & kSignBit) ? -1.0 : 1.0;
+    const double u_end = terminal_factor<F>(ic, fi, rows, se & kTargetMask);
+    const double ea = ic.base && acc_a == ic.ea_key ? ic.ea_val : exp_or_one(acc_a);
+    if (ic.base) return __dmul_rn(__dmul_rn(sg, ea), u_end);
+    const double uf = __dmul_rn(sg, u_end);
+    return __dsub_rn(__dmul_rn(uf, dexp(__dadd_rn(acc_a, acc_b))), __dmul_rn(uf, ea));
+}
+
 __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items, uint32_t i) {
     const DevItem it = items[i];
     ItemConst ic;

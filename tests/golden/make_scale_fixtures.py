@@ -12,8 +12,9 @@ pref(1e6, 5, seed 1) (netgen.cpp:61-107); R-MAT = the product's host generator (
 has none), handed to the reference as a CSR.  beta = 1/lambda from workloads.power_iteration.
 Every component runs the reference mlmc_driver (mlmc.cpp:170-260) with its OWN default options
 (eps = 1e-3, warmup 1000, max_levels_above_l0 30, no cost budget), row seed 1000 + row, one
-single-threaded process per component (results are bitwise thread-count independent,
-parallel.hpp:16-19), `--procs` at a time.  A component whose reference run exceeds `--cap`
+process per component (results are bitwise thread-count independent, parallel.hpp:16-19): light
+components single-threaded, `--procs` at a time; components of degree >= --heavy-degree one at a
+time on `--procs` threads, lightest first.  A component whose reference run exceeds `--cap`
 seconds is recorded as `timed_out` (the reference has no budget; SURVEY §7 hub rows run for
 hours) and is not a parity case.  The matrix is pinned by a hash of its CSR.
 """
@@ -101,12 +102,20 @@ def choose_rows(name, deg, count, per_stratum, seed=20260420):
     return np.asarray(rows, np.int64)[order], np.asarray(strata, np.int32)[order]
 
 
-def run_rows(chain, u, beta, rows, procs, cap):
-    """Fork one single-threaded child per component, `procs` at a time, each killed after `cap` s."""
+def run_rows(chain, u, beta, rows, procs, cap, threads=1, give_up=0):
+    """Fork one child per component (`threads` OpenMP threads in the reference's run_level),
+    `procs` at a time, each killed after `cap` s.  give_up > 0: after that many consecutive
+    timeouts the remaining rows (ascending degree: heavier still) are recorded as timed out
+    without running."""
     out = {}
     todo = list(rows)
+    streak = 0
     live = {}  # pid -> (row, read fd, start)
     while todo or live:
+        if give_up and streak >= give_up:
+            for r in todo:
+                out[int(r)] = {"timed_out": True, "seconds": 0.0, "skipped": True}
+            todo = []
         while todo and len(live) < procs:
             r = int(todo.pop(0))
             rd, wr = os.pipe()
@@ -114,7 +123,7 @@ def run_rows(chain, u, beta, rows, procs, cap):
             if pid == 0:  # child
                 os.close(rd)
                 try:
-                    (res,) = chain.driver_rows(u, beta, [r], [W.ROW_SEED_BASE + r], threads=1)
+                    (res,) = chain.driver_rows(u, beta, [r], [W.ROW_SEED_BASE + r], threads=threads)
                     res["levels"] = [dict(level=int(x["level"]), sum=float(x["sum"]).hex(),
                                           sum_sq=float(x["sum_sq"]).hex(), samples=int(x["samples"]),
                                           cost=int(x["cost"])) for x in res["levels"]]
@@ -136,6 +145,7 @@ def run_rows(chain, u, beta, rows, procs, cap):
                 res = pickle.loads(data) if data else {"error": "no output"}
                 res["seconds"] = time.time() - t0
                 out[r] = res
+                streak = 0
                 del live[pid]
                 print(f"row {r}: {time.time() - t0:.1f}s cost {res.get('total_cost', -1):.3g} L {res.get('L')}",
                       flush=True)
@@ -144,6 +154,7 @@ def run_rows(chain, u, beta, rows, procs, cap):
                 os.waitpid(pid, 0)
                 os.close(rd)
                 out[r] = {"timed_out": True, "seconds": cap}
+                streak += 1
                 del live[pid]
                 print(f"row {r}: timed out", flush=True)
     return out
@@ -156,13 +167,23 @@ def main():
     p.add_argument("--per-stratum", type=int, default=48, help="graphs: components per degree stratum")
     p.add_argument("--procs", type=int, default=os.cpu_count() or 1)
     p.add_argument("--cap", type=float, default=900.0, help="seconds per component")
+    p.add_argument("--heavy-degree", type=int, default=50,
+                   help="graphs: components of at least this degree run one at a time on all threads, "
+                        "in ascending degree, giving up after --give-up consecutive timeouts")
+    p.add_argument("--give-up", type=int, default=4)
     a = p.parse_args()
     t0 = time.time()
     chain, u, beta, (rp, col, val), meta = problem(a.config)
     deg = np.diff(rp)
     print(f"problem built in {time.time() - t0:.0f}s: n={deg.size} nnz={rp[-1]} beta={beta!r}", flush=True)
     rows, strata = choose_rows(a.config, deg, a.count, a.per_stratum)
-    res = run_rows(chain, u, beta, rows, a.procs, a.cap)
+    if strata is None:
+        res = run_rows(chain, u, beta, rows, a.procs, a.cap)
+    else:  # light components in parallel, then the heavy ones on all threads, lightest first
+        light = [int(r) for r in rows if deg[r] < a.heavy_degree]
+        heavy = sorted((int(r) for r in rows if deg[r] >= a.heavy_degree), key=lambda r: (deg[r], r))
+        res = run_rows(chain, u, beta, light, a.procs, a.cap)
+        res.update(run_rows(chain, u, beta, heavy, 1, a.cap, threads=a.procs, give_up=a.give_up))
     out = {"generator": "tests/golden/make_scale_fixtures.py (reference mlmc_driver via oracle/_ref)",
            "config": a.config, **meta, "beta": float(beta).hex(), "n": int(deg.size), "nnz": int(rp[-1]),
            "csr_sha256": csr_hash(rp, col, val), "epsilon": 1e-3, "cap_seconds": a.cap,
@@ -174,6 +195,7 @@ def main():
         if x.get("timed_out") or "error" in x:
             rec["timed_out"] = True
             rec["error"] = x.get("error")
+            rec["skipped"] = bool(x.get("skipped", False))
         else:
             rec.update(estimate=float(x["estimate"]).hex(), statistical_error=float(x["statistical_error"]).hex(),
                        bias_estimate=float(x["bias_estimate"]).hex(), l0=int(x["l0"]), L=int(x["L"]),

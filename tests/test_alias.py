@@ -70,13 +70,13 @@ def test_no_alias_for_uniform_rows(gpu):
 
 @pytest.mark.parametrize("level_offset,base", [(0, 1), (1, 0), (2, 0), (3, 0)])
 def test_event_alias_matches_reference_order_c5(gpu, level_offset, base):
-    """C5 operator family at 32^3 (7-point conv-diff, cell Peclet 10: off-diagonals +6/-4/1,
+    """C5 operator family at 64^3 (7-point conv-diff, cell Peclet 10: off-diagonals +6/-4/1,
     t = 0.1): level means of the event sampler (alias picks) vs the reference-order sampler
     (CDF picks, the reference draw for draw) on interior, face and corner components."""
-    cfg = configs.make_config("c5-32")
-    g = 32
+    cfg = configs.make_config("c5-64")
+    g = 64
     idx = lambda x, y, z: (z * g + y) * g + x  # noqa: E731
-    rows = np.array([idx(16, 16, 16), idx(0, 5, 9), idx(31, 31, 31), idx(0, 0, 0), idx(7, 20, 31), idx(31, 1, 14)])
+    rows = np.array([idx(32, 32, 32), idx(0, 5, 9), idx(63, 63, 63), idx(0, 0, 0), idx(7, 40, 63), idx(63, 1, 14)])
     with P.Context(cfg.a, cfg.u) as c:
         l0 = P.initial_level(cfg.beta, c.d_max)
     level = l0 + level_offset

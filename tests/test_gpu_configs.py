@@ -4,7 +4,9 @@ C5 (3-D convection-diffusion: non-uniform rows, mixed signs, degree 6 -> the CDF
 path) runs the reference-order sampler: per-sample and per-driver parity with the oracle is
 exact.  C3 (Barabasi-Albert, the reference's pref) and C4 (R-MAT) run the event-driven sampler
 they are configured with: every component within 3 combined standard errors of the reference
-driver (Binomial tail allowed) and the RMS rule against the deterministic e^{beta A} 1.
+driver -- exceedances consistent with Binomial(n, 0.0027) (tail probability >= 1e-3) -- and the
+RMS rule against the deterministic e^{beta A} 1.  The configured sizes and eps are pinned against
+the reference driver in tests/test_gpu_scale_parity.py.
 """
 import math
 
@@ -14,6 +16,7 @@ import pytest
 import paper_1904_12754_b200 as P
 from paper_1904_12754_b200 import configs
 from oracle import CSR
+from scipy.stats import binom
 
 pytestmark = pytest.mark.gpu
 
@@ -57,7 +60,7 @@ def test_c5_small_exact_parity(gpu, oracle_lib):
         assert float(res["estimate"][k]) == pytest.approx(e["estimate"], rel=1e-10, abs=1e-12)
 
 
-def _statistical_check(cfg, rows, eps, oracle_lib, max_fail_frac=0.1):
+def _statistical_check(cfg, rows, eps, oracle_lib):
     with P.Context(cfg.a, cfg.u, sampler=cfg.sampler) as ctx:
         res, _ = P.mlmc_driver_rows(ctx, cfg.beta, rows, configs.row_seeds(rows), P.MlmcOptions(epsilon=eps))
     och = oracle_lib.chain(_csr(cfg.a))
@@ -66,7 +69,8 @@ def _statistical_check(cfg, rows, eps, oracle_lib, max_fail_frac=0.1):
     se_r = np.array([r["statistical_error"] for r in ref])
     z = np.abs(res["estimate"] - est_r) / np.sqrt(res["statistical_error"] ** 2 + se_r ** 2 + 1e-300)
     assert res["converged"].all()
-    assert np.mean(z > 3) <= max_fail_frac, z
+    k = int(np.sum(z > 3))
+    assert k == 0 or binom.sf(k - 1, len(z), 0.0027) >= 1e-3, (k, len(z), z)
     exact = oracle_lib.dense_expmv(_csr(cfg.a), cfg.u, cfg.beta)[rows]
     err = res["estimate"] - exact
     assert math.sqrt(float(np.mean(err ** 2))) <= eps
@@ -78,7 +82,7 @@ def test_c3_small_ba_statistical(gpu, oracle_lib):
     assert cfg.sampler == "event"
     deg = np.diff(cfg.a.row_ptr)
     order = np.argsort(deg)
-    rows = np.sort(np.r_[order[:: len(order) // 24][:24], order[-200]])  # degree-stratified, no top hubs
+    rows = np.sort(np.r_[order[:: len(order) // 24][:24], order[-200], order[-20]])  # degree-stratified + hubs
     _statistical_check(cfg, rows, 1e-2, oracle_lib)
 
 
