@@ -106,7 +106,7 @@ __device__ __forceinline__ bool fem_event(FemWalker& f, const ItemConst& ic, con
         f.e1 = e[1];
     }
     if (--w.left == 0) return true;
-    w.hold = fresh_hold(ic, w.cur.rate);
+    set_hold(w, fresh_hold(ic, w.cur.rate));
     return false;
 }
 

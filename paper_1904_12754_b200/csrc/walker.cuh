@@ -282,11 +282,21 @@ struct Walker {
     int32_t sign;
     uint32_t half;         // coupled: 0 before the pair's middle node, 1 after
     double hold;           // S-mode (> 0): e^{-rate*remaining} 2^53; T-mode (<= 0): -remaining
+#if EXPMC_PROD
+    double thr;            // product form: S-mode hold = prod (1 - u_j) over the step's jumps and
+                           //   thr = S0 2^53 of the step; jump iff hold m > thr (no divide)
+#endif
     double acc_a, acc_b;   // single: expo; coupled: coarse, delta
     double d0, d1;         // d[s0], d[s1]
     uint64_t left;         // fine steps not yet completed, the current one included (counts down:
                            //   the step-end test needs no item constant)
 };
+
+#ifndef EXPMC_PROD
+#define EXPMC_PROD 0
+#endif
+struct Walker;
+__device__ __forceinline__ void set_hold(Walker& w, double h);
 
 // Start value of a fresh fine step in a row of the given rate (paths.cpp:95-96).
 __device__ __forceinline__ double fresh_hold(const ItemConst& ic, double rate) {
@@ -317,6 +327,17 @@ __device__ __forceinline__ void prepare_hold(ItemConst& ic, const RowRec* __rest
     }
 }
 
+// A fresh step's hold (fresh_hold's value): the product form keeps S0 2^53 as the threshold and
+// starts the product at 1.
+__device__ __forceinline__ void set_hold(Walker& w, double h) {
+#if EXPMC_PROD
+    w.thr = h;
+    w.hold = h > 0.0 ? 1.0 : h;
+#else
+    w.hold = h;
+#endif
+}
+
 template <bool F>
 __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                              uint64_t sample) {
@@ -324,10 +345,10 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
     const uint32_t s0 = draw_start<F>(w.st, ic, fi);
     if (!F) {  // entry mode: the item's cached start (prepare_hold; +3 % on C2)
         w.cur = ic.r0;
-        w.hold = ic.h0;
+        set_hold(w, ic.h0);
     } else {
         w.cur = load_row(rows, s0);
-        w.hold = fresh_hold(ic, w.cur.rate);
+        set_hold(w, fresh_hold(ic, w.cur.rate));
     }
     w.state = s0;
     w.sign = 1;
@@ -354,25 +375,43 @@ __device__ __forceinline__ bool walker_hold(Walker& w, const RowRec* __restrict_
         const bool smode = w.hold > 0.0;
         double e = 0.0;
         bool jump;
+#if EXPMC_PROD
+        double t = 0.0;
+        if (smode) {
+            t = __dmul_rn(w.hold, m);  // prod (1 - u_j) (1 - u) 2^53
+            jump = t > w.thr;          // (1 - u) > S0 / prod (1 - u_j) = S  <=>  u < q
+        } else {
+#else
         if (smode) {
             jump = m > w.hold;  // 1 - u > S  <=>  u < q
         } else {
+#endif
             // T-mode: E = -log1p(-u) = -log(m 2^-53) (fastmath.cuh: <= 1 ulp), jump iff E < rate * remaining
             e = -fast_log(m, -53, s_log, c_log_poly);
             jump = e < __dmul_rn(w.cur.rate, -w.hold);
         }
         if (jump) {
+#if EXPMC_PROD
+            // S-mode: the product times (1 - u), exact rescale; T-mode: -(remaining - E / rate) (paths.cpp:54)
+            double h1 = smode ? __dmul_rn(t, 0x1.0p-53) : -__dsub_rn(-w.hold, fast_div(e, w.cur.rate));
+#else
             // S-mode: S / (1 - u) (scaled); T-mode: -(remaining - E / rate) (paths.cpp:54)
             const double q = fast_div(smode ? __dmul_rn(w.hold, 0x1.0p53) : e, smode ? m : w.cur.rate);
             double h1 = smode ? q : -__dsub_rn(-w.hold, q);
+#endif
             ++jumps;
             const double rate0 = w.cur.rate;
             const uint32_t ts = pick_edge(edges, w.cur.begin, w.cur.deg, stream_pop_bits(w.st));
             if (ts & kSignBit) w.sign = -w.sign;
             w.state = ts & kTargetMask;
             w.cur = load_row(rows, w.state);
+#if EXPMC_PROD
+            if (smode && w.cur.rate != rate0)  // to T-mode: S 2^53 = S0 2^53 / prod, -remaining = log(S) / rate
+                h1 = fast_div(fast_log(fast_div(w.thr, h1), -53, s_log, c_log_poly), rate0);
+#else
             if (smode && w.cur.rate != rate0)  // S-mode needs one rate per step: to T-mode
                 h1 = fast_div(fast_log(h1, -53, s_log, c_log_poly), rate0);  // -remaining = log(S) / rate
+#endif
             w.hold = h1;
             // remaining <= 0: rounding pushed past the boundary, the step ends (paths.cpp:67)
             step_done = !(smode ? h1 != 0.0 : h1 < 0.0);
@@ -410,7 +449,7 @@ __device__ __forceinline__ bool walker_event(Walker& w, const ItemConst& ic, con
         w.half = 0u;
     }
     --w.left;
-    w.hold = fresh_hold(ic, w.cur.rate);  // next fine step: fresh holding interval of length dt (paths.cpp:95-96)
+    set_hold(w, fresh_hold(ic, w.cur.rate));  // next fine step: fresh holding interval of length dt (paths.cpp:95-96)
     return false;
 }
 
