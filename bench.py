@@ -75,6 +75,10 @@ def parse(argv=None):
     p.add_argument("--sampler", default=None, choices=["reference", "event"], help="override the config's sampler")
     p.add_argument("--full-hold", action="store_true",
                    help="event sampler: evaluate first holding intervals in full (A/B of the closed-form hold)")
+    p.add_argument("--row-gather", action="store_true",
+                   help="event sampler: separate gather of the target's row record (A/B of the per-edge records)")
+    p.add_argument("--screen-each", action="store_true",
+                   help="event sampler: per-sample screen (A/B of the geometric screen)")
     p.add_argument("--log-hold", action="store_true",
                    help="reference-order sampler: time-space holding tests with a log per event (A/B of S-mode)")
     p.add_argument("--multi", default=None, choices=["rows", "samples"],
@@ -336,14 +340,23 @@ def run_reference(args, rank, world):
     return 0
 
 
-def cpu_baseline_leg(args, threads):
+def cpu_baseline_leg(args, threads, cfg=None):
     """cpu_baseline of our arm (rank 0, N = 1): the unmodified reference on a bounded ~ref-seconds
-    sample of the same job, plus its sampler alone."""
-    from oracle import have_reference
+    sample of the same job, plus its sampler alone.  With the arm's config at hand
+    the reference's tables are decomposed from the same CSR (the reference's own decompose,
+    chain.cpp:75) instead of regenerating the graph and its lambda (minutes at C3 / C4 scale)."""
+    from oracle import CSR, Reference, have_reference
 
     if not have_reference():
         return {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": "oracle/_ref not built"}
-    chain, u, beta, universe, deg, mla, eps = reference_problem(args.config)
+    if cfg is None:
+        chain, u, beta, universe, deg, mla, eps = reference_problem(args.config)
+    else:
+        a = cfg.a
+        chain = Reference().chain(CSR(a.n, a.row_ptr, a.col, a.val))
+        u, beta, eps, mla = cfg.u, cfg.beta, cfg.epsilon, cfg.max_levels_above_l0
+        universe = cfg.rows if cfg.rows is not None else np.arange(a.n, dtype=np.int64)
+        deg = np.diff(a.row_ptr)
     per_step = REF_ROWS_PER_STEP.get(args.config.split("-")[0], 16)
     tj = ts = tr = 0
     t0 = time.perf_counter()
@@ -447,6 +460,10 @@ def run_ours(args, rank, world, local):
         ctx.set_full_hold(True)
     if args.log_hold:
         ctx.set_log_hold(True)
+    if args.row_gather:
+        ctx.set_row_gather(True)
+    if args.screen_each:
+        ctx.set_screen_each(True)
     sample_shard = multi == "samples" and world > 1
     if sample_shard:  # every rank runs the same components; chunk g is sampled on rank g % world
         obj = [P.nccl_unique_id() if rank == 0 else None]
@@ -547,6 +564,10 @@ def run_ours(args, rank, world, local):
                     c2.set_full_hold(True)
                 if args.log_hold:
                     c2.set_log_hold(True)
+                if args.row_gather:
+                    c2.set_row_gather(True)
+                if args.screen_each:
+                    c2.set_screen_each(True)
                 if sample_shard:
                     c2.shard_samples(ids[s], rank, world)
                 rows = batches[args.warmup + s]
@@ -567,7 +588,7 @@ def run_ours(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_leg(args, os.cpu_count() or 1)
+            cpu = cpu_baseline_leg(args, os.cpu_count() or 1, cfg)
         except Exception as exc:  # baseline failure must not hide the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
 

@@ -52,6 +52,10 @@ extern "C" {
  * "never leaves the entry" (one Philox block per sample) instead of locating the chunk's
  * jumpers by geometric gaps between them (same law; A/B testing only). */
 #define EXPMC_SAMPLER_FLAG_SCREEN_EACH 4u
+/* ROW_GATHER: the event-driven sampler reads the target's row record with a second gather after
+ * the edge's target word instead of the per-edge record that carries the target row's payload
+ * (same draws and outcomes; A/B testing only). */
+#define EXPMC_SAMPLER_FLAG_ROW_GATHER 8u
 
 /* Sampling lanes of the reference's Philox key (mlmc.cpp:94-96).  ENTRY estimates
  * (e^{tA}u)_entry; FORWARD estimates sum_i (e^{tA}u)_i from paths started at a state drawn

@@ -293,6 +293,13 @@ class Context:
         self._flags = (getattr(self, "_flags", 0) & ~2) | (2 if log else 0)
         _check(L.lib.expmc_ctx_set_sampler_flags(self._h, self._flags))
 
+    def set_row_gather(self, separate: bool):
+        """Event sampler: read the target's row record with a second gather (True) instead of
+        the per-edge record carrying the target row's payload (False, the default) -- same draws
+        and outcomes; A/B tests."""
+        self._flags = (getattr(self, "_flags", 0) & ~8) | (8 if separate else 0)
+        _check(L.lib.expmc_ctx_set_sampler_flags(self._h, self._flags))
+
     def set_screen_each(self, each: bool):
         """Event sampler, entry mode: test every sample's first draw for "never leaves the
         entry" (True) instead of locating the chunk's jumpers by geometric gaps (False, the

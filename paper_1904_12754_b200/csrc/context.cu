@@ -63,7 +63,11 @@ struct expmc_ctx {
     AliasRec* alias = nullptr; // per edge, event sampler: alias records of the non-uniform rows
     bool alias_checked = false;
     uint64_t alias_rows = 0;   // non-uniform rows (0: every row picks exactly from its degree)
-    EdgeTables edges() const { return EdgeTables{cdf, tgt, alias}; }
+    EdgeRec* erec = nullptr;   // per edge, event sampler: target word + the target row's payload
+    EdgeTables edges() const {
+        const bool row_gather = sampler != EXPMC_SAMPLER_EVENT || (sampler_flags & EXPMC_SAMPLER_FLAG_ROW_GATHER);
+        return EdgeTables{cdf, tgt, alias, row_gather ? nullptr : erec};
+    }
 
     // batch staging, two slots so that one batch can be prepared / consumed on the host while
     // the other samples (expmc_b200::batch_launch / batch_finish; the driver's row cohorts)
@@ -206,11 +210,11 @@ void ensure_items(Staging& S, size_t nitems, cudaStream_t st) {
 
 void bind(const expmc_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
 
-// Alias records of the non-uniform rows (event-driven sampler; AliasRec, k_build_alias), built
-// once per context on first selecting the event sampler.  Uniform rows (Laplacians, adjacency
-// matrices) pick exactly from their degree and need none: no memory unless some row is
-// non-uniform.
-void ensure_alias(expmc_ctx* c) {
+// Tables of the event-driven sampler, built once per context on first selecting it: alias
+// records of the non-uniform rows (AliasRec, k_build_alias; uniform rows -- Laplacians,
+// adjacency matrices -- pick exactly from their degree and need none) and the per-edge records
+// carrying the target row's payload (EdgeRec, k_build_erec).
+void ensure_event_tables(expmc_ctx* c) {
     if (c->alias_checked) return;
     bind(c);
     unsigned long long* d_count = nullptr;
@@ -233,6 +237,12 @@ void ensure_alias(expmc_ctx* c) {
         cuda_check(e, "build alias tables");
     }
     c->ctr.kernel_launches += 1;
+    if (c->nedges > 0) {  // EdgeRec: one sector per jump instead of the target word + its row record
+        dev_alloc(&c->erec, c->nedges, c->stream);
+        launch_build_erec(c->nedges, c->rows, c->tgt, c->erec, c->stream);
+        c->ctr.kernel_launches += 1;
+        cuda_check(cudaStreamSynchronize(c->stream), "build edge records");
+    }
     c->alias_checked = true;
 }
 
@@ -854,7 +864,7 @@ void expmc_ctx_destroy(expmc_ctx* c) {
         }
     }
     for (void* p : {static_cast<void*>(c->rows), static_cast<void*>(c->cdf), static_cast<void*>(c->tgt),
-                    static_cast<void*>(c->alias), static_cast<void*>(c->d_pf), static_cast<void*>(c->d_pu), static_cast<void*>(c->d_counter),
+                    static_cast<void*>(c->alias), static_cast<void*>(c->erec), static_cast<void*>(c->d_pf), static_cast<void*>(c->d_pu), static_cast<void*>(c->d_counter),
                     static_cast<void*>(c->d_init_cdf), static_cast<void*>(c->d_init_guide),
                     static_cast<void*>(c->d_load), static_cast<void*>(c->d_dbg)})
         dev_free(p, st);  // back to the device pool, in stream order
@@ -878,7 +888,7 @@ int expmc_ctx_get_info(const expmc_ctx* c, expmc_ctx_info* out) {
         out->device = c->device;
         out->num_sms = c->num_sms;
         out->table_bytes = static_cast<uint64_t>(c->n) * sizeof(RowRec) + c->nedges * (sizeof(double) + sizeof(uint32_t)) +
-                           (c->alias ? c->nedges * sizeof(AliasRec) : 0);
+                           (c->alias ? c->nedges * sizeof(AliasRec) : 0) + (c->erec ? c->nedges * sizeof(EdgeRec) : 0);
     });
 }
 
@@ -965,15 +975,15 @@ int expmc_ctx_set_sampler(expmc_ctx* c, int32_t mode) {
         need(mode == EXPMC_SAMPLER_REFERENCE || mode == EXPMC_SAMPLER_EVENT, EXPMC_EINVAL, "unknown sampler mode");
         c->sampler = mode;
         c->sampler_grid = mode == EXPMC_SAMPLER_EVENT ? c->sampler_grid_ed : c->sampler_grid_ref;
-        if (mode == EXPMC_SAMPLER_EVENT) ensure_alias(c);
+        if (mode == EXPMC_SAMPLER_EVENT) ensure_event_tables(c);
     });
 }
 
 int expmc_ctx_set_sampler_flags(expmc_ctx* c, uint32_t flags) {
     return guarded([&] {
         need(c != nullptr, EXPMC_EINVAL, "null context");
-        need((flags & ~(EXPMC_SAMPLER_FLAG_FULL_HOLD | EXPMC_SAMPLER_FLAG_LOG_HOLD | EXPMC_SAMPLER_FLAG_SCREEN_EACH)) ==
-                 0u,
+        need((flags & ~(EXPMC_SAMPLER_FLAG_FULL_HOLD | EXPMC_SAMPLER_FLAG_LOG_HOLD | EXPMC_SAMPLER_FLAG_SCREEN_EACH |
+                        EXPMC_SAMPLER_FLAG_ROW_GATHER)) == 0u,
              EXPMC_EINVAL,
              "unknown sampler flag");
         c->sampler_flags = flags;

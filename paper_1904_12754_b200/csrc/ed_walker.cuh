@@ -147,10 +147,24 @@ __device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const
     w.t = tjump;
     ++jumps;
     ++draws;  // the accepted holding-time draw of the jump (paths.cpp:51-54)
-    const uint32_t ts = pick_edge<true>(edges, w.cur.begin, w.cur.deg, stream_pop_bits(w.st));
+    const uint64_t kv = stream_pop_bits(w.st);
+    uint32_t ts;
+    if (edges.erec != nullptr && !alias_row(edges, w.cur.deg)) {
+        // one 32-B sector: the edge's target word and the target row's payload (EdgeRec)
+        const EdgeRec* p = edges.erec + w.cur.begin + pick_slot(edges, w.cur.begin, w.cur.deg, kv);
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+        const double2 rd = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        ts = q.x;
+        w.cur.d = rd.y;
+        w.cur.rate = rd.x;
+        w.cur.begin = q.y;
+        w.cur.deg = q.z;
+    } else {
+        ts = pick_edge<true>(edges, w.cur.begin, w.cur.deg, kv);
+        w.cur = load_row(rows, ts & kTargetMask);
+    }
     if (ts & kSignBit) w.sign = -w.sign;
     w.state = ts & kTargetMask;
-    w.cur = load_row(rows, w.state);
     if (w.cur.d != w.dfirst) w.dconst = 0u;
     return false;
 }

@@ -57,10 +57,25 @@ struct alignas(16) AliasRec {
 };
 static_assert(sizeof(AliasRec) == 16, "alias record must be one 128-bit load");
 
+// Per-edge record with the target row's payload (event-driven sampler): a jump reads ONE
+// 32-B sector -- the chosen edge's target word plus everything the walker needs of the row it
+// lands on -- instead of the 4-B target and then the target's row record (two dependent
+// random gathers; tables beyond L2 on C3/C4).  u is not copied: it is read once per sample.
+struct alignas(32) EdgeRec {
+    uint32_t tgt;    // target | sign bit (tgt[])
+    uint32_t begin;  // the target row's RowRec::begin
+    uint32_t deg;    // the target row's RowRec::deg (with kUniformRow)
+    uint32_t pad;
+    double rate;     // the target row's rate
+    double d;        // the target row's d
+};
+static_assert(sizeof(EdgeRec) == 32, "edge record must be one 32-B sector");
+
 struct EdgeTables {
     const double* cdf;
     const uint32_t* tgt;
     const AliasRec* alias;  // per edge slot, non-uniform rows only (nullptr: none built)
+    const EdgeRec* erec;    // per edge slot, event sampler (nullptr: none / separate row gathers)
 };
 
 // One device work item = one run_level request with count > 0.
@@ -176,6 +191,7 @@ void launch_export_edges(uint64_t e, EdgeTables edges, double* cdf, int64_t* tar
 void launch_count_nonuniform(int64_t n, const RowRec* rows, unsigned long long* count, cudaStream_t s);
 void launch_build_alias(int64_t n, const RowRec* rows, EdgeTables edges, AliasRec* alias, uint32_t* scratch,
                         cudaStream_t s);
+void launch_build_erec(uint64_t e, const RowRec* rows, const uint32_t* tgt, EdgeRec* erec, cudaStream_t s);
 void launch_export_alias(uint64_t e, const AliasRec* alias, double* prob, int64_t* self, int64_t* alias_target,
                          cudaStream_t s);
 // scans / reductions (CUB): exclusive sum of n u64, max / sum of RowRec::d

@@ -931,6 +931,22 @@ __global__ void k_build_alias(int64_t n, const RowRec* __restrict__ rows, EdgeTa
     }
 }
 
+__global__ void k_build_erec(uint64_t m, const RowRec* __restrict__ rows, const uint32_t* __restrict__ tgt,
+                             EdgeRec* __restrict__ erec) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t t = tgt[i];
+    const RowRec r = rows[t & kTargetMask];
+    EdgeRec e;
+    e.tgt = t;
+    e.begin = r.begin;
+    e.deg = r.deg;
+    e.pad = 0u;
+    e.rate = r.rate;
+    e.d = r.d;
+    erec[i] = e;
+}
+
 __global__ void k_export_alias(uint64_t m, const AliasRec* __restrict__ al, double* prob, int64_t* self,
                                int64_t* alias_target) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1158,6 +1174,12 @@ void launch_build_alias(int64_t n, const RowRec* rows, EdgeTables edges, AliasRe
     if (n == 0) return;
     k_build_alias<<<grid_for(n, 128), 128, 0, s>>>(n, rows, edges, alias, scratch);
     cuda_check(cudaGetLastError(), "k_build_alias launch");
+}
+
+void launch_build_erec(uint64_t m, const RowRec* rows, const uint32_t* tgt, EdgeRec* erec, cudaStream_t s) {
+    if (m == 0) return;
+    k_build_erec<<<grid_for(static_cast<int64_t>(m), 256), 256, 0, s>>>(m, rows, tgt, erec);
+    cuda_check(cudaGetLastError(), "k_build_erec launch");
 }
 
 void launch_export_alias(uint64_t m, const AliasRec* alias, double* prob, int64_t* self, int64_t* alias_target,

@@ -141,16 +141,28 @@ __device__ __forceinline__ Row load_row(const RowRec* __restrict__ rows, uint32_
 // kAlias (event-driven sampler only: its parity is statistical): a non-uniform row with an
 // alias table draws slot j = floor(v deg) = hi64(K 2^11 deg) and keeps its own target iff the
 // fraction lo64(K 2^11 deg) 2^-64 is below prob_j -- one 16-B load, any degree.
+__device__ __forceinline__ bool alias_row(const EdgeTables& e, uint32_t degf) {
+    return !(degf & kUniformRow) && e.alias != nullptr && (degf & kDegMask) > 1u;
+}
+
+// The chosen slot (offset in the row) for the exact paths: uniform rows and the CDF search.
+__device__ __forceinline__ uint32_t pick_slot(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53);
+
 template <bool kAlias = false>
 __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53) {
-    const uint32_t deg = degf & kDegMask;
-    if (kAlias && !(degf & kUniformRow) && e.alias != nullptr && deg > 1u) {
+    if (kAlias && alias_row(e, degf)) {
+        const uint32_t deg = degf & kDegMask;
         const uint64_t x = k53 << 11;
         const uint32_t j = static_cast<uint32_t>(__umul64hi(x, deg));
         const double f = __dmul_rn(__ull2double_rn((x * deg) >> 11), 0x1.0p-53);
         const uint4 r = __ldg(reinterpret_cast<const uint4*>(e.alias + begin + j));
         return f < __hiloint2double(static_cast<int>(r.y), static_cast<int>(r.x)) ? r.z : r.w;
     }
+    return __ldg(e.tgt + begin + pick_slot(e, begin, degf, k53));
+}
+
+__device__ __forceinline__ uint32_t pick_slot(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53) {
+    const uint32_t deg = degf & kDegMask;
     uint32_t k = 0;
     bool done = false;
     if ((degf & kUniformRow) && (deg & (deg - 1u)) == 0u) {
@@ -191,8 +203,7 @@ __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begi
             k = lo;
         }
     }
-    k = k < deg - 1u ? k : deg - 1u;
-    return __ldg(e.tgt + begin + k);
+    return k < deg - 1u ? k : deg - 1u;
 }
 
 // ----------------------------------------------------------------------------- walker

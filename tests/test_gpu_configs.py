@@ -82,7 +82,9 @@ def test_c3_small_ba_statistical(gpu, oracle_lib):
     assert cfg.sampler == "event"
     deg = np.diff(cfg.a.row_ptr)
     order = np.argsort(deg)
-    rows = np.sort(np.r_[order[:: len(order) // 24][:24], order[-200], order[-20]])  # degree-stratified + hubs
+    # degree-stratified; the hubs are pinned at the configured size against the reference driver
+    # (tests/test_gpu_scale_parity.py) -- the CPU reference needs hours for them at this eps
+    rows = np.sort(np.r_[order[:: len(order) // 24][:24], order[-200]])
     _statistical_check(cfg, rows, 1e-2, oracle_lib)
 
 

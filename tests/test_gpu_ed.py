@@ -166,3 +166,31 @@ def test_ed_geometric_screen_matches_per_sample_screen(gpu, level, base):
             # per-sample counts: Poisson-like, variance <= mean * (max per-sample count) -- a loose SE
             a_, b_ = float(g[key][k]), float(e[key][k])
             assert abs(a_ - b_) <= 4 * math.sqrt(2 * max(a_, b_) * (1 << (level + 2))) + 1, (key, rows[k], a_, b_)
+
+
+def test_ed_edge_records_equal_row_gathers(gpu):
+    """The per-edge records carrying the target row's payload (EdgeRec) change where a jump reads
+    the landing row from, not what it reads: per-sample outputs and run_level results are
+    bitwise those of the separate row gather, on uniform rows (grid), alias rows and absorbing
+    rows alike."""
+    rng = np.random.default_rng(17)
+    n = 50
+    dense = np.where(rng.random((n, n)) < 0.1, rng.uniform(-1.0, 1.0, (n, n)), 0.0)
+    np.fill_diagonal(dense, rng.uniform(-2.0, 0.5, n))
+    dense[9, :] = 0.0
+    dense[9, 9] = -1.0  # absorbing
+    for a, beta, rows in ((P.SparseMatrix.from_dense(dense), 0.9, np.array([0, 9, 21, 49])),
+                          (configs.make_config("c1").a, 1.0, np.array([0, 130, 2080]))):
+        u = rng.uniform(-1.0, 1.0, a.n)
+        out = {}
+        for sep in (False, True):
+            with P.Context(a, u, sampler="event") as c:
+                c.set_row_gather(sep)
+                e = np.repeat(rows, 300)
+                s = c.sample_debug(beta, e, 3, 0, 100 + e, np.tile(np.arange(300), len(rows)))
+                r = c.run_level_batch(beta, rows, 2, 0, 0, 50_000, 7 + rows)
+                out[sep] = (s, r)
+        for k in ("fine", "coarse", "cost", "jumps", "end_state"):
+            assert np.array_equal(out[False][0][k], out[True][0][k]), k
+        for k in ("sum", "sum_sq", "cost", "jumps"):
+            assert np.array_equal(out[False][1][k], out[True][1][k]), k
