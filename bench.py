@@ -54,7 +54,10 @@ import workloads as W  # noqa: E402  (numpy only: safe for the reference arm)
 
 METRIC = "random-walk transitions/sec and exp(tA)v rows/sec at target ε; % gather roofline"
 UNIT = "transitions/s"
-ALG_BYTES_PER_JUMP = 64  # destination row record (32-B sector: d, rate, u, begin, deg) + edge-record sector
+# algorithmic bytes per transition: reference-order sampler (and the event sampler with separate
+# row gathers) = the edge's target sector + the destination row record (32-B sector: d, rate, u,
+# begin, deg); event sampler = one 32-B EdgeRec carrying the target row's payload
+ALG_BYTES_PER_JUMP = {"reference": 64, "event": 32}
 PROFILE_DIR = os.path.join(ROOT, "profiles", "r02")
 # reference-arm components per step (as-shipped driver, all host cores): ~1-3 s per step on 16 cores
 REF_ROWS_PER_STEP = {"c1": 64, "c2": 32, "c3": 1, "c4": 1, "c5": 1}
@@ -369,15 +372,18 @@ def cpu_baseline_leg(args, threads, cfg=None):
     return {"value": tj / dt, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"{tr} {args.config.upper()} components through the as-shipped reference mlmc_driver "
                       f"(OpenMP, {dt:.1f} s)", "rows_per_s": tr / dt,
-            "sampler_only": sampler_only_rate(chain, u, beta, universe, threads)}
+            "sampler_only": sampler_only_rate(chain, u, beta, universe, threads, deg)}
 
 
-def sampler_only_rate(chain, u, beta, universe, threads, seconds=4.0):
+def sampler_only_rate(chain, u, beta, universe, threads, deg, seconds=4.0):
     """The reference's sampler without the driver: one large run_level per level (its
     LevelSampler table is built once per call, so the O(n) construction is amortised), OpenMP on all
-    cores.  transitions = cost - 2 M 2^l.  Level 0 (base) and level 2 (coupled), ~seconds/2 each."""
+    cores.  transitions = cost - 2 M 2^l, exact when no visited row is absorbing: the row is the
+    first of the fixed permutation with degree >= 2 (a symmetric graph's walk from it never meets
+    an isolated row).  Level 0 (base) and level 2 (coupled), ~seconds/2 each."""
     out = {}
-    row = int(universe[len(universe) // 2])
+    perm = perm_rows(len(universe))
+    row = int(next(universe[k] for k in perm if deg[universe[k]] >= 2))
     for level, base in ((0, True), (2, False)):
         m = 1 << 16
         while True:  # grow the sample until one call takes ~seconds / 2
@@ -389,7 +395,7 @@ def sampler_only_rate(chain, u, beta, universe, threads, seconds=4.0):
             m = int(m * min(16.0, max(2.0, (seconds / 2) / max(dt, 1e-3))))
         jumps = r["cost"] - 2 * m * (1 << level)
         out[f"level{level}"] = {"transitions_per_s": jumps / dt, "samples_per_s": m / dt, "samples": m,
-                                "seconds": dt}
+                                "seconds": dt, "row": row}
     return out
 
 
@@ -527,7 +533,8 @@ def run_ours(args, rank, world, local):
     # roofline of the dominant kernel (k_sample): algorithmic bytes / summed launch time (CUDA
     # events on the library stream around every sampler launch, read back by ctx.counters())
     launches = max(1, ctr["sampler_launches"])
-    alg_bytes = ctr["jumps"] * ALG_BYTES_PER_JUMP
+    bytes_per_jump = 64 if sampler == "reference" or args.row_gather else ALG_BYTES_PER_JUMP["event"]
+    alg_bytes = ctr["jumps"] * bytes_per_jump
     kern_s = ctr["sampler_ms"] * 1e-3
     achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
     peaks, peak_src = load_peaks()
@@ -630,14 +637,22 @@ def run_ours(args, rank, world, local):
                         "GPU-hours at this run's cost-unit rate on n_gpus GPUs"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_sample", "sampler_launches": ctr["sampler_launches"],
+                         "kernel": "k_sample_grouped" if sampler == "event" else "k_sample",
+                         "sampler_launches": ctr["sampler_launches"],
                          "kernel_ms": ctr["sampler_ms"], "mean_launch_ms": mean_launch_ms,
                          "step_share": ctr["sampler_ms"] / ms_local,
-                         "alg_bytes": f"{ALG_BYTES_PER_JUMP} B per transition (row record + edge sector); samples "
+                         "alg_bytes": f"{bytes_per_jump} B per transition ("
+                                      + ("row record + edge sector" if bytes_per_jump == 64 else
+                                         "one edge record with the target row's payload; + <= 1 sector per "
+                                         "jumping sample for u[end], not counted")
+                                      + "); samples "
                                       "that never leave the entry read no table",
                          "alg_bytes_per_launch": alg_bytes / launches,
                          "measured": measured,
-                         "binding_resource": "instruction issue (measured issue_frac)" if cap else None,
+                         "binding_resource": (None if not cap else
+                                              "instruction issue (measured issue_frac)" if cap["issue_frac"] >= 0.7 else
+                                              "random-gather latency (issue_frac below 0.7, L2 hit "
+                                              f"{cap['l2_hit']:.2f}; tables beyond L2)"),
                          "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
                          "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches), "clocks": clk,

@@ -11,7 +11,7 @@
 // SIMT shape: a warp advances 32 independent paths one EVENT per loop trip (one pass of
 // evolve_common's for(;;) body).  Each event has exactly one call site for every expensive
 // operation -- one Philox block (the stream keeps a 3-word queue so one refill per event is
-// always enough for the u and v draws) and one divide (the holding test runs in probability
+// always enough for the u and v draws) and no divide (the holding test runs in probability
 // space, see below) -- so a diverged warp pays each of them at most once per trip.
 #pragma once
 
@@ -20,6 +20,12 @@
 
 #include "fastmath.cuh"
 #include "internal.hpp"
+
+// Product-form probability-space holding test (see walker_hold): 1 = on (default since round 2,
+// C2 kernel -1.9 %), 0 = the round-1 divide form (A/B builds).
+#ifndef EXPMC_PROD
+#define EXPMC_PROD 1
+#endif
 
 namespace expmc_b200 {
 
@@ -210,10 +216,13 @@ __device__ __forceinline__ uint32_t pick_slot(const EdgeTables& e, uint32_t begi
 // Holding-interval test.  The reference decides "no jump in the rest of the interval" by
 // u >= q with q = -expm1(-rate*remaining) (paths.cpp:53, 68, 90) and, on a jump, spends
 // E = -log1p(-u) of the interval (paths.cpp:54).  With 1 - u = M 2^-53 exactly (M = 2^53 - K),
-// u < q is 1 - u > S, S = e^{-rate*remaining}: the walker carries S itself ("S-mode", scaled by
-// 2^53: hold = S 2^53, compared with the integer M) and a jump multiplies it by 1/(1 - u)
-// (e^{-rate (remaining - E/rate)} = S / (1 - u)) -- one correctly-rounded-to-1-ulp divide, no
-// logarithm, no exponential.  A fresh step starts from S0 = e^{-rate dt}, cached per item for
+// u < q is 1 - u > S, S = e^{-rate*remaining}: the walker works in probability space ("S-mode")
+// with no logarithm and no exponential.  After jumps with draws u_1..u_k in the current step,
+// S = S0 / prod_j (1 - u_j) (e^{-rate (remaining - E/rate)} = S / (1 - u)), so the test is
+// prod_j (1 - u_j) (1 - u) 2^53 > S0 2^53: the walker keeps the product (hold, starts at 1) and
+// the step's S0 2^53 (thr) -- one multiply per event and none of round 1's divides per jump
+// ("product form", EXPMC_PROD; EXPMC_PROD=0 keeps hold = S 2^53 and divides by 1 - u per jump).
+// A fresh step starts from S0 = e^{-rate dt}, cached per item for
 // the entry row's rate (every interior row of C1/C2/C5 shares it).  When a jump changes the
 // rate, the rest of the step continues in time space ("T-mode", hold = -remaining with
 // remaining = -log(S)/rate, then the reference's log-space test E < rate*remaining per event);
@@ -292,7 +301,8 @@ struct Walker {
     uint32_t state;
     int32_t sign;
     uint32_t half;         // coupled: 0 before the pair's middle node, 1 after
-    double hold;           // S-mode (> 0): e^{-rate*remaining} 2^53; T-mode (<= 0): -remaining
+    double hold;           // S-mode (> 0): prod (1 - u_j) (EXPMC_PROD) or e^{-rate*remaining} 2^53;
+                           //   T-mode (<= 0): -remaining
 #if EXPMC_PROD
     double thr;            // product form: S-mode hold = prod (1 - u_j) over the step's jumps and
                            //   thr = S0 2^53 of the step; jump iff hold m > thr (no divide)
@@ -303,9 +313,6 @@ struct Walker {
                            //   the step-end test needs no item constant)
 };
 
-#ifndef EXPMC_PROD
-#define EXPMC_PROD 0
-#endif
 struct Walker;
 __device__ __forceinline__ void set_hold(Walker& w, double h);
 
