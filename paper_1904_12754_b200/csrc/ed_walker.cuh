@@ -241,6 +241,36 @@ struct RefPolicy {
     }
 };
 
+// Level-0 items of the entry lane (base level, nsteps == 1): the reference-order walker
+// without step bookkeeping (Walker0).  A batch's level-0 items are launched with this policy,
+// the rest with RefPolicy (context.cu: sample_launch).
+#ifndef EXPMC_B0_MINB
+#define EXPMC_B0_MINB EXPMC_SAMPLER_MINB
+#endif
+struct RefPolicy0 {
+    using W = Walker0;
+    static constexpr bool kDefer = false;
+    static constexpr bool kExtra = false;
+    static constexpr bool kScreen = false;
+    static __device__ __forceinline__ bool screen(const ItemConst&, uint64_t) { return false; }
+    static constexpr int kMinBlocks = EXPMC_B0_MINB;
+    static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData&, uint32_t flags) {
+        prepare_hold(ic, rows, flags);
+    }
+    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData&, const RowRec*, uint64_t s) {
+        walker0_start(w, ic, s);
+    }
+    static __device__ __forceinline__ bool event(W& w, const ItemConst&, const LaneData&, const RowRec* rows,
+                                                 const EdgeTables& e, const LogEntry* lg, unsigned long long& dr,
+                                                 unsigned long long& j) {
+        return walker_hold(w, rows, e, lg, dr, j);  // the step's end is the sample's end
+    }
+    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const LaneData&,
+                                                    const RowRec* rows, double&) {
+        return walker0_sample(w, ic, rows);
+    }
+};
+
 template <bool F>
 struct EdPolicy {
     using W = EdWalker;

@@ -151,8 +151,9 @@ struct SamplerArgs {
     const DevItem* items;
     const uint64_t* chunk0;  // nitems + 1, exclusive prefix of chunk counts
     uint32_t nitems;
-    uint64_t g_begin, g_end;  // global chunk window of this launch
-    ChunkPartials partials;   // [g_end - g_begin] each
+    uint64_t g_begin, g_end;  // global chunk range of this launch
+    uint64_t part_base;       // chunk g's partial is partials[g - part_base] (the window's first chunk)
+    ChunkPartials partials;   // one per chunk of the window
     LaneData init;
     unsigned int* counter;    // dynamic chunk counter, zeroed before launch
     uint32_t shard_rank;      // sample sharding: this launch samples the chunks g with
@@ -160,7 +161,8 @@ struct SamplerArgs {
     uint32_t flags;           // EXPMC_SAMPLER_FLAG_*
 };
 
-void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s);
+// level0: every item of the launch is an entry-lane base level with one fine step (RefPolicy0)
+void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s, bool level0 = false);
 void launch_sampler_welford(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s);
 void launch_combine_welford(const uint64_t* chunk0, const DevItem* items, uint32_t nitems, uint64_t g_begin,
                             uint64_t g_end, const ChunkPartials& partials, Partial* totals, cudaStream_t s);

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
             jumps += __shfl_xor_sync(full, jumps, o);
         }
         if (lane == 0) {
-            const uint64_t k = g - a.g_begin;
+            const uint64_t k = g - a.part_base;
             a.partials.sum[k] = sum;
             a.partials.sum_sq[k] = sum_sq;
             if constexpr (P::kExtra) a.partials.extra[k] = extra;
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, EXPMC_GROUPED_MINB) k_sample_grouped
             }
             // portion totals on its first chunk, zeros on the rest
             const uint32_t j0 = cur.j0, j1 = cur.j;
-            const uint64_t k0 = cur.gq - a.g_begin;
+            const uint64_t k0 = cur.gq - a.part_base;
             for (uint32_t t = j0 + lane; t < j1; t += 32u) {
                 const uint64_t k = k0 + t;
                 const bool head = t == j0;
@@ -1067,7 +1067,7 @@ int sampler_blocks_per_sm(int mode) {
 // Entry and forward mode are separate instantiations: a batch is one lane, and the entry-mode
 // kernel (the hot path) carries no trace of the forward start draw.
 template <bool W>
-void launch_sampler_t(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s) {
+void launch_sampler_t(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s, bool level0) {
     if constexpr (!W) {
         if (lane == EXPMC_LANE_FEM) {
             k_sample<FemPolicy, false><<<grid, kThreads, 0, s>>>(a);
@@ -1081,18 +1081,19 @@ void launch_sampler_t(const SamplerArgs& a, int grid, int mode, uint32_t lane, c
         else k_sample_grouped<EdPolicy<false>><<<grid, kThreads, 0, s>>>(a);
     } else {
         if (lane == EXPMC_LANE_FORWARD) k_sample<RefPolicy<true>, W><<<grid, kThreads, 0, s>>>(a);
+        else if (!W && level0) k_sample<RefPolicy0, false><<<grid, kThreads, 0, s>>>(a);
         else k_sample<RefPolicy<false>, W><<<grid, kThreads, 0, s>>>(a);
     }
     cuda_check(cudaGetLastError(), "k_sample launch");
 }
 
-void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s) {
-    launch_sampler_t<false>(a, grid, mode, lane, s);
+void launch_sampler(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s, bool level0) {
+    launch_sampler_t<false>(a, grid, mode, lane, s, level0);
 }
 
 void launch_sampler_welford(const SamplerArgs& a, int grid, int mode, uint32_t lane, cudaStream_t s) {
     if (lane == EXPMC_LANE_FEM) throw Status(EXPMC_ENOTIMPL, "classical MC has no fem lane");
-    launch_sampler_t<true>(a, grid, mode, lane, s);
+    launch_sampler_t<true>(a, grid, mode, lane, s, false);
 }
 
 void launch_combine_welford(const uint64_t* chunk0, const DevItem* items, uint32_t nitems, uint64_t g_begin,

@@ -313,8 +313,6 @@ struct Walker {
                            //   the step-end test needs no item constant)
 };
 
-struct Walker;
-__device__ __forceinline__ void set_hold(Walker& w, double h);
 
 // Start value of a fresh fine step in a row of the given rate (paths.cpp:95-96).
 __device__ __forceinline__ double fresh_hold(const ItemConst& ic, double rate) {
@@ -347,7 +345,8 @@ __device__ __forceinline__ void prepare_hold(ItemConst& ic, const RowRec* __rest
 
 // A fresh step's hold (fresh_hold's value): the product form keeps S0 2^53 as the threshold and
 // starts the product at 1.
-__device__ __forceinline__ void set_hold(Walker& w, double h) {
+template <class WK>
+__device__ __forceinline__ void set_hold(WK& w, double h) {
 #if EXPMC_PROD
     w.thr = h;
     w.hold = h > 0.0 ? 1.0 : h;
@@ -381,7 +380,8 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
 // on a jump, the neighbour draw.  Returns true when the holding interval ends the fine step.
 // Exponential draws and jumps are counted straight into the caller's accumulators (cost =
 // draws + fine steps, paths.hpp:22-23; the fine steps are added when the sample ends).
-__device__ __forceinline__ bool walker_hold(Walker& w, const RowRec* __restrict__ rows, const EdgeTables& edges,
+template <class WK>
+__device__ __forceinline__ bool walker_hold(WK& w, const RowRec* __restrict__ rows, const EdgeTables& edges,
                                             const LogEntry* s_log, unsigned long long& draws,
                                             unsigned long long& jumps) {
     stream_reserve2(w.st);  // the event's only Philox call site
@@ -546,6 +546,38 @@ __device__ __forceinline__ double walker_value(double acc_a, double acc_b, uint3
     if (ic.base) return __dmul_rn(__dmul_rn(sg, ea), u_end);
     const double uf = __dmul_rn(sg, u_end);
     return __dsub_rn(__dmul_rn(uf, dexp(__dadd_rn(acc_a, acc_b))), __dmul_rn(uf, ea));
+}
+
+// ----------------------------------------------------------------------------- level 0
+// Base level with one fine step (l = l0 = 0: every C1/C2 component's first and largest level;
+// ~80 % of C2's loop trips).  The sample ends with the step, so the walker needs none of the
+// step bookkeeping -- no accumulators, d0/d1, pair half or step count (11 registers of
+// Walker): expo = dt 0.5 (d[entry] + d[end]) (paths.cpp:108-110), value = sign e^expo u[end]
+// (paths.cpp:112), the same operations in the same order as walker_event + walker_sample.
+struct Walker0 {
+    Stream st;
+    Row cur;
+    uint32_t state;
+    int32_t sign;
+    double hold;
+#if EXPMC_PROD
+    double thr;
+#endif
+};
+
+__device__ __forceinline__ void walker0_start(Walker0& w, const ItemConst& ic, uint64_t sample) {
+    stream_init(w.st, ic.seed, sample, ic.key3);
+    w.cur = ic.r0;
+    set_hold(w, ic.h0);
+    w.state = ic.entry;
+    w.sign = 1;
+}
+
+__device__ __forceinline__ double walker0_sample(const Walker0& w, const ItemConst& ic, const RowRec* __restrict__ rows) {
+    const double a = __dadd_rn(0.0, __dmul_rn(ic.half_dt, __dadd_rn(ic.r0.d, w.cur.d)));  // last_step_sums
+    const double sg = static_cast<double>(w.sign);
+    const double ea = a == ic.ea_key ? ic.ea_val : exp_or_one(a);
+    return __dmul_rn(__dmul_rn(sg, ea), __ldg(&rows[w.state].u));
 }
 
 __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items, uint32_t i) {

@@ -160,3 +160,43 @@ def test_driver_too_few_levels_is_invalid_argument(gpu):
                 P.mlmc_driver_rows(ctx, cfg.beta, [3, 4], [1003, 1004], P.MlmcOptions(max_levels_above_l0=mla))
         res, _ = P.mlmc_driver_rows(ctx, cfg.beta, [3], [1003], P.MlmcOptions(max_levels_above_l0=2))
         assert res["L"][0] <= 2
+
+
+def test_level0_items_split_launch_bitwise(gpu):
+    """Reference-order batches sample their level-0 items (base level, one fine step) with the
+    step-free walker in a launch of their own (context.cu sample_launch, RefPolicy0): a batch
+    mixing level-0 and coupled items of several levels, with empty requests and partial first
+    chunks, returns bitwise what each request returns alone -- in one window and across many."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, paper_1904_12754_b200 as P
+from paper_1904_12754_b200 import configs
+cfg = configs.make_config("c1")
+rng = np.random.default_rng(4)
+k = 40
+entry = rng.integers(0, cfg.a.n, k)
+level = rng.integers(0, 4, k)
+base = np.where(level == 0, 1, rng.integers(0, 2, k))
+base[level > 0] = 0
+base[::7] = 1  # base levels above 0 too (nsteps > 1: the general walker)
+first = rng.integers(0, 3000, k).astype(np.uint64)
+count = rng.integers(0, 5000, k).astype(np.uint64)
+count[::9] = 0
+seed = 1000 + entry
+with P.Context(cfg.a, cfg.u) as c:
+    both = c.run_level_batch(cfg.beta, entry, level, base, first, count, seed)
+    for i in range(k):
+        one = c.run_level_batch(cfg.beta, entry[i], level[i], base[i], first[i], count[i], seed[i])
+        for f in ("sum", "sum_sq", "samples", "cost", "jumps"):
+            assert both[f][i] == one[f][0], (i, f)
+print("ok")
+'''
+    import os
+    for window in (None, "7"):
+        env = dict(os.environ)
+        if window:
+            env["EXPMC_WINDOW_CHUNKS"] = window
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
