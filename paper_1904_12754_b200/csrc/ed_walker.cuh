@@ -256,6 +256,9 @@ struct RefPolicy0 {
     static constexpr int kMinBlocks = EXPMC_B0_MINB;
     static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData&, uint32_t flags) {
         prepare_hold(ic, rows, flags);
+#if EXPMC_RKEYS
+        set_round_keys(ic.seed);  // lane 0; k_sample's __syncwarp publishes it with the item constants
+#endif
     }
     static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData&, const RowRec*, uint64_t s) {
         walker0_start(w, ic, s);

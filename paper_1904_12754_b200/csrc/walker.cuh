@@ -102,7 +102,8 @@ __device__ __forceinline__ void stream_reserve2(Stream& s) {
 }
 
 // The 53-bit integer K of the next uniform v = K 2^-53 (rng.hpp:34-35).
-__device__ __forceinline__ uint64_t stream_pop_bits(Stream& s) {
+template <class ST>
+__device__ __forceinline__ uint64_t stream_pop_bits(ST& s) {
     const uint64_t bits = s.w0;
     s.w0 = s.w1;
     s.w1 = s.w2;
@@ -114,6 +115,74 @@ __device__ __forceinline__ double to_uniform(uint64_t k53) { return __dmul_rn(__
 
 // next_uniform: 53 random bits -> [0,1) exactly as rng.hpp:35.
 __device__ __forceinline__ double stream_pop(Stream& s) { return to_uniform(stream_pop_bits(s)); }
+
+// Keyless stream (EXPMC_RKEYS): the Weyl key schedule of the warp's item seed is precomputed once
+// per chunk into shared memory (g_round_keys, one 80-B table per warp), and a refill reads the
+// ten (k0, k1) round-key pairs with five 128-bit shared loads instead of adding the key
+// increments (18 integer adds per block) -- and the stream holds no key registers.
+#ifndef EXPMC_RKEYS
+#define EXPMC_RKEYS 1
+#endif
+__shared__ uint4 g_round_keys[8][5];  // [warp of a 256-thread block][pair of rounds]
+
+__device__ __forceinline__ void set_round_keys(uint64_t seed) {  // lane 0, then __syncwarp()
+    uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+    uint4* t = g_round_keys[threadIdx.x >> 5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        t[r] = make_uint4(k0, k1, k0 + 0x9E3779B9u, k1 + 0xBB67AE85u);
+        k0 += 2u * 0x9E3779B9u;
+        k1 += 2u * 0xBB67AE85u;
+    }
+}
+
+struct StreamRK {
+    uint32_t c1, c2, c3;   // counter words 1..3 (the key comes from g_round_keys)
+    uint32_t block;
+    uint64_t w0, w1, w2;
+    uint32_t n;
+};
+
+__device__ __forceinline__ void stream_init(StreamRK& s, uint64_t sample, uint32_t key3) {
+    s.c1 = static_cast<uint32_t>(sample);
+    s.c2 = static_cast<uint32_t>(sample >> 32);
+    s.c3 = key3;
+    s.block = 0;
+    s.n = 0;
+}
+
+__device__ __forceinline__ void stream_reserve2(StreamRK& s) {
+    if (s.n < 2u) {
+        uint32_t c0 = s.block++, c1 = s.c1, c2 = s.c2, c3 = s.c3;
+        const uint4* t = g_round_keys[threadIdx.x >> 5];
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const uint4 k = t[r];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // rng.hpp:44-62, round keys (k.x, k.y) then (k.z, k.w)
+                const uint32_t ka = h ? k.z : k.x, kb = h ? k.w : k.y;
+                const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c0;
+                const uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c2;
+                const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ ka;
+                const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ kb;
+                c1 = static_cast<uint32_t>(p1);
+                c3 = static_cast<uint32_t>(p0);
+                c0 = n0;
+                c2 = n2;
+            }
+        }
+        const uint64_t first = (static_cast<uint64_t>(c2) << 32) | c3;
+        const uint64_t second = (static_cast<uint64_t>(c0) << 32) | c1;
+        if (s.n == 0u) {
+            s.w0 = first;
+            s.w1 = second;
+        } else {
+            s.w1 = first;
+            s.w2 = second;
+        }
+        s.n += 2u;
+    }
+}
 
 // ----------------------------------------------------------------------------- tables
 struct Row {  // u_i is not kept in registers: walker_finish reloads it for the end state
@@ -555,7 +624,11 @@ __device__ __forceinline__ double walker_value(double acc_a, double acc_b, uint3
 // Walker): expo = dt 0.5 (d[entry] + d[end]) (paths.cpp:108-110), value = sign e^expo u[end]
 // (paths.cpp:112), the same operations in the same order as walker_event + walker_sample.
 struct Walker0 {
+#if EXPMC_RKEYS
+    StreamRK st;
+#else
     Stream st;
+#endif
     Row cur;
     uint32_t state;
     int32_t sign;
@@ -566,7 +639,11 @@ struct Walker0 {
 };
 
 __device__ __forceinline__ void walker0_start(Walker0& w, const ItemConst& ic, uint64_t sample) {
+#if EXPMC_RKEYS
+    stream_init(w.st, sample, ic.key3);
+#else
     stream_init(w.st, ic.seed, sample, ic.key3);
+#endif
     w.cur = ic.r0;
     set_hold(w, ic.h0);
     w.state = ic.entry;
