@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
     __shared__ ItemConst s_ic[kWarps];  // per-warp item constants: read at use, not held in registers
     ItemConst& ic = s_ic[threadIdx.x >> 5];
     uint32_t hint = 0;
+    uint32_t prepared = 0xFFFFFFFFu;  // the item whose constants ic holds (chunks of an item come in runs)
     // sample sharding: this GPU owns the chunks g = own0 + k * world of the window
     const uint64_t rem = a.g_begin % a.shard_world;
     const uint64_t own0 = a.g_begin + (a.shard_rank + a.shard_world - rem) % a.shard_world;
@@ -129,13 +130,14 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
 
         const uint32_t item = find_item(a.chunk0, a.nitems, g, hint);
         hint = item;
-        {
+        if (item != prepared) {  // warp-uniform
             if (lane == 0) {
                 ItemConst c = load_item(a.items, item);
                 P::prepare(c, a.rows, a.init, a.flags);
                 ic = c;
             }
             __syncwarp();
+            prepared = item;
         }
         const DevItem& it = a.items[item];
         const uint64_t first = it.first, end = it.first + it.count;

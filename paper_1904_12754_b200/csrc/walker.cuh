@@ -123,6 +123,11 @@ __device__ __forceinline__ double stream_pop(Stream& s) { return to_uniform(stre
 #ifndef EXPMC_RKEYS
 #define EXPMC_RKEYS 1
 #endif
+// EXPMC_QEND: the reference-order walker reads u and v in place and advances its word queue once
+// at the event's end instead of shifting it on every pop (A/B builds).
+#ifndef EXPMC_QEND
+#define EXPMC_QEND 1
+#endif
 __shared__ uint4 g_round_keys[8][5];  // [warp of a 256-thread block][pair of rounds]
 
 __device__ __forceinline__ void set_round_keys(uint64_t seed) {  // lane 0, then __syncwarp()
@@ -456,7 +461,11 @@ __device__ __forceinline__ bool walker_hold(WK& w, const RowRec* __restrict__ ro
     stream_reserve2(w.st);  // the event's only Philox call site
     bool step_done = true;
     if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
+#if EXPMC_QEND
+        const uint64_t k53 = w.st.w0 >> 11;  // u; consumed with v (on a jump) at the event's end
+#else
         const uint64_t k53 = stream_pop_bits(w.st);
+#endif
         ++draws;
         const double m = __ull2double_rn((uint64_t{1} << 53) - k53);  // (1 - u) 2^53, exact
         const bool smode = w.hold > 0.0;
@@ -488,7 +497,11 @@ __device__ __forceinline__ bool walker_hold(WK& w, const RowRec* __restrict__ ro
 #endif
             ++jumps;
             const double rate0 = w.cur.rate;
+#if EXPMC_QEND
+            const uint32_t ts = pick_edge(edges, w.cur.begin, w.cur.deg, w.st.w1 >> 11);
+#else
             const uint32_t ts = pick_edge(edges, w.cur.begin, w.cur.deg, stream_pop_bits(w.st));
+#endif
             if (ts & kSignBit) w.sign = -w.sign;
             w.state = ts & kTargetMask;
             w.cur = load_row(rows, w.state);
@@ -503,6 +516,12 @@ __device__ __forceinline__ bool walker_hold(WK& w, const RowRec* __restrict__ ro
             // remaining <= 0: rounding pushed past the boundary, the step ends (paths.cpp:67)
             step_done = !(smode ? h1 != 0.0 : h1 < 0.0);
         }
+#if EXPMC_QEND
+        // the queue advances once per event: by u, or by u and v after a jump
+        w.st.w0 = jump ? w.st.w2 : w.st.w1;
+        w.st.w1 = w.st.w2;
+        w.st.n -= jump ? 2u : 1u;
+#endif
     }
     return step_done;
 }
