@@ -56,8 +56,9 @@ constexpr uint32_t kSkipLane = 5u;    // Philox lane of the per-chunk gap stream
 constexpr double kSkipMinHeld = 0.75; // geometric screening when P(held) exceeds this
 constexpr uint32_t kFlagGrouped = 1u << 31;  // prepare() called by k_sample_grouped (internal flag bit)
 
-struct EdWalker {
-    Stream st;
+template <class ST>
+struct EdWalkerT {
+    ST st;
     Row cur;
     uint32_t state;
     int32_t sign;
@@ -69,11 +70,22 @@ struct EdWalker {
     double acc_b;      // doubled-weight sum of d: delta (coupled)
     double dfirst;
 };
+using EdWalker = EdWalkerT<Stream>;
+// k_sample_grouped's walker: the Philox key schedule comes from the warp's round-key table
+// (g_round_keys, one item per warp at a time), so the stream holds no key registers.
+using EdWalkerRK = EdWalkerT<StreamRK>;
 
-template <bool F>
-__device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
+__device__ __forceinline__ void ed_stream_init(Stream& st, const ItemConst& ic, uint64_t sample) {
+    stream_init(st, ic.seed, sample, ic.key3);
+}
+__device__ __forceinline__ void ed_stream_init(StreamRK& st, const ItemConst& ic, uint64_t sample) {
+    stream_init(st, sample, ic.key3);
+}
+
+template <bool F, class WK>
+__device__ __forceinline__ void ed_start(WK& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                          uint64_t sample) {
-    stream_init(w.st, ic.seed, sample, ic.key3);
+    ed_stream_init(w.st, ic, sample);
     const uint32_t s0 = draw_start<F>(w.st, ic, fi);
     w.cur = F ? load_row(rows, s0) : ic.r0;  // entry mode: the item's row (EdPolicy::prepare)
     w.state = s0;
@@ -89,7 +101,8 @@ __device__ __forceinline__ void ed_start(EdWalker& w, const ItemConst& ic, const
 }
 
 // Boundaries [ka, kb] (ka <= kb <= N) all see the current state.
-__device__ __forceinline__ void ed_segment(EdWalker& w, const ItemConst& ic, uint64_t ka, uint64_t kb,
+template <class WK>
+__device__ __forceinline__ void ed_segment(WK& w, const ItemConst& ic, uint64_t ka, uint64_t kb,
                                            unsigned long long& draws) {
     const uint64_t n = kb - ka + 1;
     const int64_t ends = static_cast<int64_t>(ka == 0) + static_cast<int64_t>(kb == ic.nsteps);
@@ -109,7 +122,8 @@ __device__ __forceinline__ void ed_segment(EdWalker& w, const ItemConst& ic, uin
 }
 
 // One holding interval: draw its length, assign the boundaries it covers, jump (or finish).
-__device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+template <class WK>
+__device__ __forceinline__ bool ed_event(WK& w, const ItemConst& ic, const RowRec* __restrict__ rows,
                                          const EdgeTables& edges, const LogEntry* s_log, unsigned long long& draws,
                                          unsigned long long& jumps) {
     stream_reserve2(w.st);
@@ -169,8 +183,8 @@ __device__ __forceinline__ bool ed_event(EdWalker& w, const ItemConst& ic, const
     return false;
 }
 
-template <bool F>
-__device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
+template <bool F, class WK>
+__device__ __forceinline__ void ed_finish(const WK& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows,
                                           double& fine, double& coarse) {
     const double sg = static_cast<double>(w.sign);
     const double u_end = terminal_factor<F>(ic, fi, rows, w.state);
@@ -188,8 +202,8 @@ __device__ __forceinline__ void ed_finish(const EdWalker& w, const ItemConst& ic
     }
 }
 
-template <bool F>
-__device__ __forceinline__ double ed_sample(const EdWalker& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows) {
+template <bool F, class WK>
+__device__ __forceinline__ double ed_sample(const WK& w, const ItemConst& ic, const LaneData& fi, const RowRec* __restrict__ rows) {
     if (w.sign == 0) return ic.hold_x;
     if (!ic.base && w.dconst) return 0.0;
     double fine, coarse;
@@ -344,6 +358,29 @@ struct EdPolicy {
         }
         o.integ_f = o.integ_c = 0.0;
         o.end_state = w.state;
+    }
+};
+
+// The grouped kernel's entry-mode policy: EdPolicy<false> with the keyless stream (the round-key
+// table is written by prepare(), lane 0, and published by the kernel's __syncwarp).
+struct EdPolicyG : EdPolicy<false> {
+    using W = EdWalkerRK;
+    static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData& ld, uint32_t flags) {
+        EdPolicy<false>::prepare(ic, rows, ld, flags);
+        set_round_keys(ic.seed);
+    }
+    static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
+                                                 uint64_t s) {
+        ed_start<false>(w, ic, ld, rows, s);
+    }
+    static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const LaneData&, const RowRec* rows,
+                                                 const EdgeTables& e, const LogEntry* lg, unsigned long long& dr,
+                                                 unsigned long long& j) {
+        return ed_event(w, ic, rows, e, lg, dr, j);
+    }
+    static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const LaneData& ld,
+                                                    const RowRec* rows, double&) {
+        return ed_sample<false>(w, ic, ld, rows);
     }
 };
 

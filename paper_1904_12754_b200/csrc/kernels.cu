@@ -1058,7 +1058,7 @@ int sampler_blocks_per_sm(int mode) {
     if (mode == kSamplerFem)
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<FemPolicy, false>, kThreads, 0), "occupancy");
     else if (mode == EXPMC_SAMPLER_EVENT)
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_grouped<EdPolicy<false>>, kThreads, 0),
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample_grouped<EdPolicyG>, kThreads, 0),
                    "occupancy");
     else
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sample<RefPolicy<false>, false>, kThreads, 0),
@@ -1080,7 +1080,7 @@ void launch_sampler_t(const SamplerArgs& a, int grid, int mode, uint32_t lane, c
     if (mode == EXPMC_SAMPLER_EVENT) {
         if (lane == EXPMC_LANE_FORWARD) k_sample<EdPolicy<true>, W><<<grid, kThreads, 0, s>>>(a);
         else if constexpr (W) k_sample<EdPolicy<false>, W><<<grid, kThreads, 0, s>>>(a);
-        else k_sample_grouped<EdPolicy<false>><<<grid, kThreads, 0, s>>>(a);
+        else k_sample_grouped<EdPolicyG><<<grid, kThreads, 0, s>>>(a);
     } else {
         if (lane == EXPMC_LANE_FORWARD) k_sample<RefPolicy<true>, W><<<grid, kThreads, 0, s>>>(a);
         else if (!W && level0) k_sample<RefPolicy0, false><<<grid, kThreads, 0, s>>>(a);

@@ -339,8 +339,8 @@ struct ItemConst {
 
 // sample_initial (paths.cpp:32-36): the path's first draw picks the start state by
 // upper_bound over the CDF of u -- an exact binary search over the same fp64 CDF.
-template <bool F>
-__device__ __forceinline__ uint32_t draw_start(Stream& st, const ItemConst& ic, const LaneData& fi) {
+template <bool F, class ST>
+__device__ __forceinline__ uint32_t draw_start(ST& st, const ItemConst& ic, const LaneData& fi) {
     if (!F) return ic.entry;
     stream_reserve2(st);
     const uint64_t k53 = stream_pop_bits(st);

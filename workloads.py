@@ -146,9 +146,17 @@ def _segmented_sequential_sum(v, row_ptr, n):
     sdeg = deg[order]
     start = row_ptr[:-1][order]
     acc = np.zeros(n)
-    for k in range(int(sdeg[0])):
+    band = min(int(sdeg[0]), 256)  # positions summed across rows; the few wider rows continue below
+    for k in range(band):
         cnt = int(np.searchsorted(-sdeg, -k, side="left"))  # rows with deg > k form a prefix
         acc[:cnt] += v[start[:cnt] + k]
+    wide = int(np.searchsorted(-sdeg, -band, side="left"))  # rows with deg > band
+    for i in range(wide):  # sequential continuation: acc + v[band] + v[band + 1] + ...
+        b0 = int(start[i]) + band
+        seg = np.empty(int(sdeg[i]) - band + 1)
+        seg[0] = acc[i]
+        seg[1:] = v[b0:int(start[i]) + int(sdeg[i])]
+        acc[i] = np.cumsum(seg)[-1]
     out[order] = acc
     return out
 
