@@ -33,6 +33,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+static_assert(kWarps <= 8, "g_round_keys (walker.cuh) holds one round-key table per warp of a 256-thread block");
 
 __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ chunk0, uint32_t nitems,
                                               uint64_t g, uint32_t hint) {

@@ -73,7 +73,9 @@ def test_workload_inputs_match_the_product_generators():
     n, rp, col, val = W.convdiff3d(12)
     a = configs.gen_convdiff3d(12, 10.0, 0)
     assert np.array_equal(rp, a.row_ptr) and np.array_equal(col, a.col) and np.array_equal(val, a.val)
-    for a in (configs.gen_ba(5000, 5, 1), configs.gen_rmat(12, 16), a):
+    wide = configs.gen_rmat(15, 16)  # rows wider than the position band (the sequential continuation)
+    assert np.diff(wide.row_ptr).max() > 256
+    for a in (configs.gen_ba(5000, 5, 1), configs.gen_rmat(12, 16), a, wide):
         assert W.power_iteration(a.n, a.row_ptr, a.col, a.val) == configs.power_iteration(a, 50)
     assert np.array_equal(W.seeded_rows(1 << 16, 1000), configs.seeded_rows(1 << 16, 1000))
     assert np.array_equal(W.row_seeds([0, 5]), configs.row_seeds([0, 5]))
