@@ -102,7 +102,7 @@ def choose_rows(name, deg, count, per_stratum, seed=20260420):
     return np.asarray(rows, np.int64)[order], np.asarray(strata, np.int32)[order]
 
 
-def run_rows(chain, u, beta, rows, procs, cap, threads=1, give_up=0):
+def run_rows(chain, u, beta, rows, procs, cap, threads=1, give_up=0, journal=None):
     """Fork one child per component (`threads` OpenMP threads in the reference's run_level),
     `procs` at a time, each killed after `cap` s.  give_up > 0: after that many consecutive
     timeouts the remaining rows (ascending degree: heavier still) are recorded as timed out
@@ -146,6 +146,9 @@ def run_rows(chain, u, beta, rows, procs, cap, threads=1, give_up=0):
                 res["seconds"] = time.time() - t0
                 out[r] = res
                 streak = 0
+                if journal:  # progress survives an interrupted run (--resume)
+                    with open(journal, "ab") as jf:
+                        pickle.dump((r, res), jf)
                 del live[pid]
                 print(f"row {r}: {time.time() - t0:.1f}s cost {res.get('total_cost', -1):.3g} L {res.get('L')}",
                       flush=True)
@@ -155,6 +158,9 @@ def run_rows(chain, u, beta, rows, procs, cap, threads=1, give_up=0):
                 os.close(rd)
                 out[r] = {"timed_out": True, "seconds": cap}
                 streak += 1
+                if journal:
+                    with open(journal, "ab") as jf:
+                        pickle.dump((r, out[r]), jf)
                 del live[pid]
                 print(f"row {r}: timed out", flush=True)
     return out
@@ -171,19 +177,34 @@ def main():
                    help="graphs: components of at least this degree run one at a time on all threads, "
                         "in ascending degree, giving up after --give-up consecutive timeouts")
     p.add_argument("--give-up", type=int, default=4)
+    p.add_argument("--resume", action="store_true", help="skip components already in the run's journal")
     a = p.parse_args()
     t0 = time.time()
     chain, u, beta, (rp, col, val), meta = problem(a.config)
     deg = np.diff(rp)
     print(f"problem built in {time.time() - t0:.0f}s: n={deg.size} nnz={rp[-1]} beta={beta!r}", flush=True)
     rows, strata = choose_rows(a.config, deg, a.count, a.per_stratum)
+    journal = os.path.join("/tmp", f"scale_{a.config}.journal")
+    res = {}
+    if a.resume and os.path.exists(journal):
+        with open(journal, "rb") as jf:
+            while True:
+                try:
+                    r, x = pickle.load(jf)
+                except EOFError:
+                    break
+                res[int(r)] = x
+        print(f"resumed {len(res)} components from {journal}", flush=True)
+    elif os.path.exists(journal):
+        os.remove(journal)
+    todo = [int(r) for r in rows if int(r) not in res]
     if strata is None:
-        res = run_rows(chain, u, beta, rows, a.procs, a.cap)
+        res.update(run_rows(chain, u, beta, todo, a.procs, a.cap, journal=journal))
     else:  # light components in parallel, then the heavy ones on all threads, lightest first
-        light = [int(r) for r in rows if deg[r] < a.heavy_degree]
-        heavy = sorted((int(r) for r in rows if deg[r] >= a.heavy_degree), key=lambda r: (deg[r], r))
-        res = run_rows(chain, u, beta, light, a.procs, a.cap)
-        res.update(run_rows(chain, u, beta, heavy, 1, a.cap, threads=a.procs, give_up=a.give_up))
+        light = [r for r in todo if deg[r] < a.heavy_degree]
+        heavy = sorted((r for r in todo if deg[r] >= a.heavy_degree), key=lambda r: (deg[r], r))
+        res.update(run_rows(chain, u, beta, light, a.procs, a.cap, journal=journal))
+        res.update(run_rows(chain, u, beta, heavy, 1, a.cap, threads=a.procs, give_up=a.give_up, journal=journal))
     out = {"generator": "tests/golden/make_scale_fixtures.py (reference mlmc_driver via oracle/_ref)",
            "config": a.config, **meta, "beta": float(beta).hex(), "n": int(deg.size), "nnz": int(rp[-1]),
            "csr_sha256": csr_hash(rp, col, val), "epsilon": 1e-3, "cap_seconds": a.cap,
