@@ -378,9 +378,9 @@ def cpu_baseline_leg(args, threads, cfg=None):
 def sampler_only_rate(chain, u, beta, universe, threads, deg, seconds=4.0):
     """The reference's sampler without the driver: one large run_level per level (its
     LevelSampler table is built once per call, so the O(n) construction is amortised), OpenMP on all
-    cores.  transitions = cost - 2 M 2^l, exact when no visited row is absorbing: the row is the
-    first of the fixed permutation with degree >= 2 (a symmetric graph's walk from it never meets
-    an isolated row).  Level 0 (base) and level 2 (coupled), ~seconds/2 each."""
+    cores.  transitions = the jumps run_level counts (RunLevelStats::jumps); the row is the first
+    of the fixed permutation with degree >= 2.  Level 0 (base) and level 2 (coupled), ~seconds/2
+    each."""
     out = {}
     perm = perm_rows(len(universe))
     row = int(next(universe[k] for k in perm if deg[universe[k]] >= 2))
@@ -393,7 +393,7 @@ def sampler_only_rate(chain, u, beta, universe, threads, deg, seconds=4.0):
             if dt >= seconds / 4 or m >= (1 << 34):
                 break
             m = int(m * min(16.0, max(2.0, (seconds / 2) / max(dt, 1e-3))))
-        jumps = r["cost"] - 2 * m * (1 << level)
+        jumps = int(r["jumps"])
         out[f"level{level}"] = {"transitions_per_s": jumps / dt, "samples_per_s": m / dt, "samples": m,
                                 "seconds": dt, "row": row}
     return out

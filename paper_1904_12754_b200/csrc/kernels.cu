@@ -291,15 +291,20 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
 // list wl[nwork..] as (slot << 9) | offset and return the new list length.  Gaps come 32 at a
 // time from the chunk's own Philox stream (lane kSkipLane, counter = absolute chunk index) and
 // are placed by a warp prefix sum.  One accurate log per 32 gaps (libdevice: off the hot path).
-__device__ __forceinline__ uint32_t geometric_screen(const ItemConst& ic, uint64_t chunk, uint32_t cnt, uint32_t slot,
-                                                     uint16_t* wl, uint32_t nwork) {
+__device__ __forceinline__ uint32_t geometric_screen(const ItemConst& ic, uint64_t chunk, uint32_t off, uint32_t cnt,
+                                                     uint32_t slot, uint16_t* wl, uint32_t nwork) {
     const unsigned full = 0xFFFFFFFFu;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t k3 = (ic.key3 & 0x00FFFFFFu) | (kSkipLane << 24);
     const uint32_t k0 = static_cast<uint32_t>(ic.seed), k1 = static_cast<uint32_t>(ic.seed >> 32);
     const double scale = ic.skip_scale;
+    // Positions are offsets in the WHOLE chunk (sample chunk*512 + p): a chunk that run_level
+    // extensions split (samples [lo, hi) of it now, the rest in a later call) must see the same
+    // jumper set in both calls, so the gaps are always laid from the chunk's first sample and
+    // this call keeps the jumpers in [off, off + cnt).  Listed entries are offsets from lo.
+    const uint32_t end = off + cnt;
     uint32_t pos = 0;
-    for (uint32_t it = 0; pos < cnt; ++it) {  // warp-uniform
+    for (uint32_t it = 0; pos < end; ++it) {  // warp-uniform
         uint32_t c0 = it * 32u + lane, c1 = static_cast<uint32_t>(chunk), c2 = static_cast<uint32_t>(chunk >> 32), c3 = k3;
         philox10(c0, c1, c2, c3, k0, k1);
         const uint64_t k53 = ((static_cast<uint64_t>(c2) << 32) | c3) >> 11;  // rng.hpp:32-35
@@ -313,9 +318,9 @@ __device__ __forceinline__ uint32_t geometric_screen(const ItemConst& ic, uint64
             if (lane >= static_cast<uint32_t>(o)) incl += y;
         }
         const uint32_t p = pos + incl - 1u;  // this lane's jumper
-        const bool jump = p < cnt;
+        const bool jump = p >= off && p < end;
         const unsigned need = __ballot_sync(full, jump);
-        if (jump) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>((slot << 9) | p);
+        if (jump) wl[nwork + __popc(need & lanemask_lt())] = static_cast<uint16_t>((slot << 9) | (p - off));
         nwork += __popc(need);
         pos += __shfl_sync(full, incl, 31);
     }
@@ -417,7 +422,8 @@ __global__ void __launch_bounds__(kThreads, EXPMC_GROUPED_MINB) k_sample_grouped
                     if (lane == 0) s_lo[wid][j] = lo;
                     nsamp += cnt;
                     if (ic.skip_scale != 0.0) {
-                        const uint32_t n1 = geometric_screen(ic, chunk, cnt, j, wl, nwork);
+                        const uint32_t n1 = geometric_screen(ic, chunk, static_cast<uint32_t>(lo - chunk * kChunk), cnt, j,
+                                                             wl, nwork);
                         if (lane == 0) nheld += cnt - (n1 - nwork);
                         nwork = n1;
                         continue;

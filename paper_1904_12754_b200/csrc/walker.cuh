@@ -156,26 +156,31 @@ __device__ __forceinline__ void stream_init(StreamRK& s, uint64_t sample, uint32
     s.n = 0;
 }
 
+// Philox4x32-10 with the warp's precomputed round keys (rng.hpp:44-62).
+__device__ __forceinline__ void philox10_rk(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3) {
+    const uint4* t = g_round_keys[threadIdx.x >> 5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        const uint4 k = t[r];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // round keys (k.x, k.y) then (k.z, k.w)
+            const uint32_t ka = h ? k.z : k.x, kb = h ? k.w : k.y;
+            const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c0;
+            const uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c2;
+            const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ ka;
+            const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ kb;
+            c1 = static_cast<uint32_t>(p1);
+            c3 = static_cast<uint32_t>(p0);
+            c0 = n0;
+            c2 = n2;
+        }
+    }
+}
+
 __device__ __forceinline__ void stream_reserve2(StreamRK& s) {
     if (s.n < 2u) {
         uint32_t c0 = s.block++, c1 = s.c1, c2 = s.c2, c3 = s.c3;
-        const uint4* t = g_round_keys[threadIdx.x >> 5];
-#pragma unroll
-        for (int r = 0; r < 5; ++r) {
-            const uint4 k = t[r];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {  // rng.hpp:44-62, round keys (k.x, k.y) then (k.z, k.w)
-                const uint32_t ka = h ? k.z : k.x, kb = h ? k.w : k.y;
-                const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c0;
-                const uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c2;
-                const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ ka;
-                const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ kb;
-                c1 = static_cast<uint32_t>(p1);
-                c3 = static_cast<uint32_t>(p0);
-                c0 = n0;
-                c2 = n2;
-            }
-        }
+        philox10_rk(c0, c1, c2, c3);
         const uint64_t first = (static_cast<uint64_t>(c2) << 32) | c3;
         const uint64_t second = (static_cast<uint64_t>(c0) << 32) | c1;
         if (s.n == 0u) {
@@ -188,6 +193,47 @@ __device__ __forceinline__ void stream_reserve2(StreamRK& s) {
         s.n += 2u;
     }
 }
+
+// One-step stream (level-0 walker, EXPMC_EV0).  A level-0 sample is one fine step, and a step
+// ends at its first non-jump draw: the sample consumes u_1 v_1 u_2 v_2 ... u_k (a jump draws u
+// and v, paths.cpp:52-57; the final u, or an absorbing row, ends it).  Block b of the stream
+// holds (first, second) = (u_{b+1}, v_{b+1}) in consumption order (rng.hpp:32-36, 63-65), so
+// every event starts on a fresh block: one unconditional Philox call per event, no word queue
+// (the queue's bookkeeping and its divergent refill branch are gone).  Same words, same order.
+#ifndef EXPMC_EV0
+#define EXPMC_EV0 1
+#endif
+#if EXPMC_EV0 && !EXPMC_QEND
+#error "EXPMC_EV0 reads u and v in place (EXPMC_QEND)"
+#endif
+struct StreamEv {
+    uint32_t c1, c2, c3;
+    uint32_t block;
+    uint64_t w0, w1;  // this event's u and v words
+};
+
+__device__ __forceinline__ void stream_init(StreamEv& s, uint64_t sample, uint32_t key3) {
+    s.c1 = static_cast<uint32_t>(sample);
+    s.c2 = static_cast<uint32_t>(sample >> 32);
+    s.c3 = key3;
+    s.block = 0;
+}
+
+__device__ __forceinline__ void stream_reserve2(StreamEv& s) {
+    uint32_t c0 = s.block++, c1 = s.c1, c2 = s.c2, c3 = s.c3;
+    philox10_rk(c0, c1, c2, c3);
+    s.w0 = (static_cast<uint64_t>(c2) << 32) | c3;
+    s.w1 = (static_cast<uint64_t>(c0) << 32) | c1;
+}
+
+// The event's words are consumed: advance the queue by u, or by u and v after a jump.
+template <class ST>
+__device__ __forceinline__ void stream_advance(ST& s, bool jump) {
+    s.w0 = jump ? s.w2 : s.w1;
+    s.w1 = s.w2;
+    s.n -= jump ? 2u : 1u;
+}
+__device__ __forceinline__ void stream_advance(StreamEv&, bool) {}  // the next event refills
 
 // ----------------------------------------------------------------------------- tables
 struct Row {  // u_i is not kept in registers: walker_finish reloads it for the end state
@@ -518,9 +564,7 @@ __device__ __forceinline__ bool walker_hold(WK& w, const RowRec* __restrict__ ro
         }
 #if EXPMC_QEND
         // the queue advances once per event: by u, or by u and v after a jump
-        w.st.w0 = jump ? w.st.w2 : w.st.w1;
-        w.st.w1 = w.st.w2;
-        w.st.n -= jump ? 2u : 1u;
+        stream_advance(w.st, jump);
 #endif
     }
     return step_done;
@@ -643,7 +687,9 @@ __device__ __forceinline__ double walker_value(double acc_a, double acc_b, uint3
 // Walker): expo = dt 0.5 (d[entry] + d[end]) (paths.cpp:108-110), value = sign e^expo u[end]
 // (paths.cpp:112), the same operations in the same order as walker_event + walker_sample.
 struct Walker0 {
-#if EXPMC_RKEYS
+#if EXPMC_RKEYS && EXPMC_EV0
+    StreamEv st;
+#elif EXPMC_RKEYS
     StreamRK st;
 #else
     Stream st;

@@ -194,3 +194,29 @@ def test_ed_edge_records_equal_row_gathers(gpu):
             assert np.array_equal(out[False][0][k], out[True][0][k]), k
         for k in ("sum", "sum_sq", "cost", "jumps"):
             assert np.array_equal(out[False][1][k], out[True][1][k]), k
+
+
+@pytest.mark.parametrize("level,base", [(0, 1), (2, 0)])
+def test_ed_geometric_screen_is_split_invariant(gpu, level, base):
+    """The driver extends a level in pieces (run_level(first, additional), mlmc.cpp:188-199), so a
+    chunk can be sampled partly in one call and partly in the next.  The geometric screen lays its
+    gaps from the chunk's first sample in every call, so the jumper set -- and with it every
+    sample's path -- does not depend on where the calls split: jumps and costs are exactly those
+    of one call over the same samples, sums equal up to summation order.  (Before this rule a split
+    chunk re-used its first gaps for the second piece: correlated samples across extensions.)"""
+    rng = np.random.default_rng(23)
+    n = 60
+    dense = np.where(rng.random((n, n)) < 0.08, rng.uniform(-1.0, 1.0, (n, n)), 0.0)
+    np.fill_diagonal(dense, rng.uniform(-1.5, 0.5, n))
+    a = P.SparseMatrix.from_dense(dense)
+    u = rng.uniform(-1.0, 1.0, n)
+    rows = np.array([0, 5, 17, 31, 44, 59])
+    total = 100_000
+    with P.Context(a, u, sampler="event") as c:
+        one = c.run_level_batch(0.08, rows, level, base, 0, total, 300 + rows)
+        parts = [c.run_level_batch(0.08, rows, level, base, f, k, 300 + rows)
+                 for f, k in ((0, 1000), (1000, 37), (1037, 50_000 - 1037), (50_000, total - 50_000))]
+    for key in ("cost", "jumps"):
+        assert np.array_equal(one[key], sum(p[key] for p in parts)), key
+    for key in ("sum", "sum_sq"):
+        np.testing.assert_allclose(sum(p[key] for p in parts), one[key], rtol=1e-11, atol=1e-13)
