@@ -550,7 +550,10 @@ class RefChain(_Chain):
         self.be._check(self.be.lib.ref_run_level(self.h, _ptr(u), _I64(entry), _D(beta), _INT(level), _INT(int(base)),
                                                  _U64(first), _U64(count), _U64(seed), _INT(threads), C.byref(s),
                                                  C.byref(s2), C.byref(m), C.byref(c)))
-        return dict(sum=s.value, sum_sq=s2.value, samples=m.value, cost=c.value)
+        # the reference's RunLevelStats has no jump counter: every fine step of a non-absorbing row ends
+        # with one rejected draw, so cost = (jumps + M 2^l) + M 2^l (paths.hpp:22-23, paths.cpp:50-53)
+        return dict(sum=s.value, sum_sq=s2.value, samples=m.value, cost=c.value,
+                    jumps=max(0, c.value - 2 * m.value * (1 << level)))
 
     def driver_rows(self, u, beta, rows, row_seeds, max_levels=40, **opt):
         rows = np.ascontiguousarray(rows, np.int64)
