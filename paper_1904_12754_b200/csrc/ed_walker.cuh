@@ -72,7 +72,7 @@ struct EdWalkerT {
 };
 using EdWalker = EdWalkerT<Stream>;
 // k_sample_grouped's walker: the Philox key schedule comes from the warp's round-key table
-// (g_round_keys, one item per warp at a time), so the stream holds no key registers.
+// (ItemConst::rk, one item per warp at a time), so the stream holds no key registers.
 using EdWalkerRK = EdWalkerT<StreamRK>;
 
 __device__ __forceinline__ void ed_stream_init(Stream& st, const ItemConst& ic, uint64_t sample) {
@@ -126,7 +126,7 @@ template <class WK>
 __device__ __forceinline__ bool ed_event(WK& w, const ItemConst& ic, const RowRec* __restrict__ rows,
                                          const EdgeTables& edges, const LogEntry* s_log, unsigned long long& draws,
                                          unsigned long long& jumps) {
-    stream_reserve2(w.st);
+    stream_reserve2(w.st, ic.rk);
     if (w.dconst & (kFresh | kCond)) {
         if (w.dconst & kCond) {
             // listed by the geometric screen: M uniform on [m_safe, 2^53] from the first word
@@ -271,16 +271,20 @@ struct RefPolicy0 {
     static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData&, uint32_t flags) {
         prepare_hold(ic, rows, flags);
 #if EXPMC_RKEYS
-        set_round_keys(ic.seed);  // lane 0; k_sample's __syncwarp publishes it with the item constants
+        set_round_keys(ic.rk, ic.seed);  // lane 0; k_sample's __syncwarp publishes it with the item constants
 #endif
     }
     static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData&, const RowRec*, uint64_t s) {
         walker0_start(w, ic, s);
     }
-    static __device__ __forceinline__ bool event(W& w, const ItemConst&, const LaneData&, const RowRec* rows,
+    static __device__ __forceinline__ bool event(W& w, const ItemConst& ic, const LaneData&, const RowRec* rows,
                                                  const EdgeTables& e, const LogEntry* lg, unsigned long long& dr,
                                                  unsigned long long& j) {
-        return walker_hold(w, rows, e, lg, dr, j);  // the step's end is the sample's end
+#if EXPMC_L0TUNE
+        return walker0_event(w, ic, rows, e, lg, dr, j);  // the step's end is the sample's end
+#else
+        return walker_hold(w, rows, e, lg, dr, j, ic.rk);
+#endif
     }
     static __device__ __forceinline__ double sample(const W& w, const ItemConst& ic, const LaneData&,
                                                     const RowRec* rows, double&) {
@@ -367,7 +371,7 @@ struct EdPolicyG : EdPolicy<false> {
     using W = EdWalkerRK;
     static __device__ __forceinline__ void prepare(ItemConst& ic, const RowRec* rows, const LaneData& ld, uint32_t flags) {
         EdPolicy<false>::prepare(ic, rows, ld, flags);
-        set_round_keys(ic.seed);
+        set_round_keys(ic.rk, ic.seed);
     }
     static __device__ __forceinline__ void start(W& w, const ItemConst& ic, const LaneData& ld, const RowRec* rows,
                                                  uint64_t s) {

@@ -33,7 +33,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-static_assert(kWarps <= 8, "g_round_keys (walker.cuh) holds one round-key table per warp of a 256-thread block");
 
 __device__ __forceinline__ uint32_t find_item(const uint64_t* __restrict__ chunk0, uint32_t nitems,
                                               uint64_t g, uint32_t hint) {
@@ -184,19 +183,25 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
             }
         }
         typename P::W w;
-        bool active = false;
-        uint32_t my = 0;  // the running sample's slot in the chunk
+        // The running sample's slot in the chunk; kIdle: the lane has no sample (no separate flag:
+        // a bool kept across the loop costs byte-permute instructions on every trip).
+        constexpr uint32_t kIdle = 0xFFFFFFFFu;
+        uint32_t my = kIdle;
+        // A chunk's samples share their upper 32 index bits (chunks are 512-aligned), so sample
+        // lo + my is (lo's upper word, lo's lower word + my) without a carry: the stream's second
+        // counter word is chunk-invariant.
+        const uint64_t lo_hi = lo & 0xFFFFFFFF00000000ull;
+        const uint32_t lo_lo = static_cast<uint32_t>(lo);
         // Lanes start work entries 0..31; a lane whose sample ends takes the next unstarted
         // entry in the same divergent section as its finish (one ballot per trip).
         if (lane < nwork) {
             my = listed ? wl[lane] : lane;
-            P::start(w, ic, a.init, a.rows, lo + my);
-            active = true;
+            P::start(w, ic, a.init, a.rows, lo_hi | (lo_lo + my));
         }
         uint32_t next = nwork < 32u ? nwork : 32u;
         uint32_t qh = 0, qn = 0;  // deferred finish: ring head and pending records (warp-uniform)
-        while (__any_sync(full, active)) {
-            const bool done = active && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps);
+        while (__any_sync(full, my != kIdle)) {
+            const bool done = my != kIdle && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps);
             const unsigned fin = __ballot_sync(full, done);
             if (done) {
                 if constexpr (kDefer) {
@@ -221,9 +226,9 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
                 const uint32_t mine = next + __popc(fin & lanemask_lt());
                 if (mine < nwork) {
                     my = listed ? wl[mine] : mine;
-                    P::start(w, ic, a.init, a.rows, lo + my);
+                    P::start(w, ic, a.init, a.rows, lo_hi | (lo_lo + my));
                 } else {
-                    active = false;
+                    my = kIdle;
                 }
             }
             next += __popc(fin);

@@ -101,6 +101,8 @@ __device__ __forceinline__ void stream_reserve2(Stream& s) {
     }
 }
 
+__device__ __forceinline__ void stream_reserve2(Stream& s, const uint4*) { stream_reserve2(s); }  // keyed stream: no table
+
 // The 53-bit integer K of the next uniform v = K 2^-53 (rng.hpp:34-35).
 template <class ST>
 __device__ __forceinline__ uint64_t stream_pop_bits(ST& s) {
@@ -117,9 +119,11 @@ __device__ __forceinline__ double to_uniform(uint64_t k53) { return __dmul_rn(__
 __device__ __forceinline__ double stream_pop(Stream& s) { return to_uniform(stream_pop_bits(s)); }
 
 // Keyless stream (EXPMC_RKEYS): the Weyl key schedule of the warp's item seed is precomputed once
-// per chunk into shared memory (g_round_keys, one 80-B table per warp), and a refill reads the
-// ten (k0, k1) round-key pairs with five 128-bit shared loads instead of adding the key
-// increments (18 integer adds per block) -- and the stream holds no key registers.
+// per item into the warp's item constants in shared memory (ItemConst::rk, 80 B), and a refill
+// reads the ten (k0, k1) round-key pairs with five 128-bit shared loads instead of adding the key
+// increments (18 integer adds per block) -- and the stream holds no key registers.  The table
+// sits in ItemConst so that its address is the item-constant pointer the loop already holds
+// (a table of its own cost six address instructions per Philox block).
 #ifndef EXPMC_RKEYS
 #define EXPMC_RKEYS 1
 #endif
@@ -128,11 +132,8 @@ __device__ __forceinline__ double stream_pop(Stream& s) { return to_uniform(stre
 #ifndef EXPMC_QEND
 #define EXPMC_QEND 1
 #endif
-__shared__ uint4 g_round_keys[8][5];  // [warp of a 256-thread block][pair of rounds]
-
-__device__ __forceinline__ void set_round_keys(uint64_t seed) {  // lane 0, then __syncwarp()
+__device__ __forceinline__ void set_round_keys(uint4* t, uint64_t seed) {  // t = ItemConst::rk (prepare, lane 0)
     uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
-    uint4* t = g_round_keys[threadIdx.x >> 5];
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
         t[r] = make_uint4(k0, k1, k0 + 0x9E3779B9u, k1 + 0xBB67AE85u);
@@ -142,7 +143,7 @@ __device__ __forceinline__ void set_round_keys(uint64_t seed) {  // lane 0, then
 }
 
 struct StreamRK {
-    uint32_t c1, c2, c3;   // counter words 1..3 (the key comes from g_round_keys)
+    uint32_t c1, c2, c3;   // counter words 1..3 (the key comes from ItemConst::rk)
     uint32_t block;
     uint64_t w0, w1, w2;
     uint32_t n;
@@ -157,8 +158,7 @@ __device__ __forceinline__ void stream_init(StreamRK& s, uint64_t sample, uint32
 }
 
 // Philox4x32-10 with the warp's precomputed round keys (rng.hpp:44-62).
-__device__ __forceinline__ void philox10_rk(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3) {
-    const uint4* t = g_round_keys[threadIdx.x >> 5];
+__device__ __forceinline__ void philox10_rk(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, const uint4* t) {
 #pragma unroll
     for (int r = 0; r < 5; ++r) {
         const uint4 k = t[r];
@@ -177,10 +177,10 @@ __device__ __forceinline__ void philox10_rk(uint32_t& c0, uint32_t& c1, uint32_t
     }
 }
 
-__device__ __forceinline__ void stream_reserve2(StreamRK& s) {
+__device__ __forceinline__ void stream_reserve2(StreamRK& s, const uint4* rk) {
     if (s.n < 2u) {
         uint32_t c0 = s.block++, c1 = s.c1, c2 = s.c2, c3 = s.c3;
-        philox10_rk(c0, c1, c2, c3);
+        philox10_rk(c0, c1, c2, c3, rk);
         const uint64_t first = (static_cast<uint64_t>(c2) << 32) | c3;
         const uint64_t second = (static_cast<uint64_t>(c0) << 32) | c1;
         if (s.n == 0u) {
@@ -206,6 +206,13 @@ __device__ __forceinline__ void stream_reserve2(StreamRK& s) {
 #if EXPMC_EV0 && !EXPMC_QEND
 #error "EXPMC_EV0 reads u and v in place (EXPMC_QEND)"
 #endif
+// EXPMC_L0TUNE: the level-0 walker's own event function (walker0_event) instead of walker_hold.
+#ifndef EXPMC_L0TUNE
+#define EXPMC_L0TUNE 1
+#endif
+#if EXPMC_L0TUNE && !(EXPMC_RKEYS && EXPMC_EV0 && EXPMC_PROD)
+#error "EXPMC_L0TUNE is written for the one-block-per-event keyless stream and the product form"
+#endif
 struct StreamEv {
     uint32_t c1, c2, c3;
     uint32_t block;
@@ -219,9 +226,9 @@ __device__ __forceinline__ void stream_init(StreamEv& s, uint64_t sample, uint32
     s.block = 0;
 }
 
-__device__ __forceinline__ void stream_reserve2(StreamEv& s) {
+__device__ __forceinline__ void stream_reserve2(StreamEv& s, const uint4* rk) {
     uint32_t c0 = s.block++, c1 = s.c1, c2 = s.c2, c3 = s.c3;
-    philox10_rk(c0, c1, c2, c3);
+    philox10_rk(c0, c1, c2, c3, rk);
     s.w0 = (static_cast<uint64_t>(c2) << 32) | c3;
     s.w1 = (static_cast<uint64_t>(c0) << 32) | c1;
 }
@@ -252,6 +259,21 @@ __device__ __forceinline__ Row load_row(const RowRec* __restrict__ rows, uint32_
     return r;
 }
 
+// load_row with the record's address formed by one 32 x 32 -> 64-bit multiply-add (the compiler
+// otherwise splits the masked state's shift over six instructions).
+__device__ __forceinline__ Row load_row_at(const RowRec* __restrict__ rows, uint32_t i) {
+    uint64_t p;
+    asm("mad.wide.u32 %0, %1, 32, %2;" : "=l"(p) : "r"(i), "l"(reinterpret_cast<uint64_t>(rows)));
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const uint2 b = __ldg(reinterpret_cast<const uint2*>(p) + 3);
+    Row r;
+    r.d = a.x;
+    r.rate = a.y;
+    r.begin = b.x;
+    r.deg = b.y;
+    return r;
+}
+
 // Neighbour choice (paths.cpp:57-65): k = upper_bound(cdf[begin:begin+deg], v) clamped to
 // deg-1, then (target, sign) = tgt[begin + k].  Returns the packed target|sign word.
 //
@@ -272,7 +294,9 @@ __device__ __forceinline__ bool alias_row(const EdgeTables& e, uint32_t degf) {
 }
 
 // The chosen slot (offset in the row) for the exact paths: uniform rows and the CDF search.
+// pick_slot_np2 is pick_slot for a row that is not (uniform with a power-of-two degree).
 __device__ __forceinline__ uint32_t pick_slot(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53);
+__device__ __forceinline__ uint32_t pick_slot_np2(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53);
 
 template <bool kAlias = false>
 __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53) {
@@ -289,14 +313,19 @@ __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begi
 
 __device__ __forceinline__ uint32_t pick_slot(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53) {
     const uint32_t deg = degf & kDegMask;
-    uint32_t k = 0;
-    bool done = false;
     if ((degf & kUniformRow) && (deg & (deg - 1u)) == 0u) {
         // power-of-two degree 2^p (every interior row of a 2-D Laplacian: 4): cdf_j = (j+1) 2^-p
-        // and v 2^p = K 2^(p-53) are exact, so upper_bound = K >> (53 - p), no boundary case
-        k = static_cast<uint32_t>(k53 >> (53 - (31 - __clz(deg))));
-        done = true;
-    } else if (degf & kUniformRow) {
+        // and v 2^p = K 2^(p-53) are exact, so upper_bound = K >> (53 - p) <= deg - 1, no boundary case
+        return static_cast<uint32_t>(k53 >> (53 - (31 - __clz(deg))));
+    }
+    return pick_slot_np2(e, begin, degf, k53);
+}
+
+__device__ __forceinline__ uint32_t pick_slot_np2(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53) {
+    const uint32_t deg = degf & kDegMask;
+    uint32_t k = 0;
+    bool done = false;
+    if (degf & kUniformRow) {
         // t = fl(v deg) is within deg 2^-53 of v deg; a fractional part at least 2 deg 2^-53 away
         // from 0 and 1 puts v deg at least deg 2^-53 from every integer: floor(t) is then the
         // exact upper_bound and the boundary condition above holds.
@@ -374,6 +403,7 @@ struct ItemConst {
     };                      //   (0: off; EdPolicy::prepare always writes it)
     Row r0;             // entry mode: the entry's row record and its fresh-step hold (the
     double h0;          //   restart of every sample reads them from here, not from the tables)
+    double hold0;       // level-0 walker: the restart's hold (product form: 1 in S-mode, else h0)
     double ea_key;      // base level: e^{ea_key} = ea_val, the exponent of a path that keeps the
     double ea_val;      //   entry's d (every interior path of C5) -- one exp per chunk, not per sample
     // event-driven entry mode: closed-form first holding interval (EdPolicy::prepare)
@@ -381,6 +411,7 @@ struct ItemConst {
     double hold_fine;   // that path's (fine, coarse) and run_level sample x
     double hold_coarse;
     double hold_x;
+    uint4 rk[5];        // keyless streams: the item seed's Philox round keys (set_round_keys)
 };
 
 // sample_initial (paths.cpp:32-36): the path's first draw picks the start state by
@@ -388,7 +419,7 @@ struct ItemConst {
 template <bool F, class ST>
 __device__ __forceinline__ uint32_t draw_start(ST& st, const ItemConst& ic, const LaneData& fi) {
     if (!F) return ic.entry;
-    stream_reserve2(st);
+    stream_reserve2(st, ic.rk);
     const uint64_t k53 = stream_pop_bits(st);
     const double v = to_uniform(k53);
     // the draw's guide bucket bounds the search (context.cu: ensure_forward_init)
@@ -455,6 +486,11 @@ __device__ __forceinline__ void prepare_hold(ItemConst& ic, const RowRec* __rest
         }
     }
     ic.h0 = fresh_hold(ic, ic.r0.rate);
+#if EXPMC_PROD
+    ic.hold0 = ic.h0 > 0.0 ? 1.0 : ic.h0;  // set_hold(w, h0)
+#else
+    ic.hold0 = ic.h0;
+#endif
     if (ic.base && ic.nsteps <= 64u) {  // walker_event / last_step_sums on a constant-d path
         double a = 0.0;
         for (uint64_t k = 0; k < ic.nsteps; ++k) a = __dadd_rn(a, __dmul_rn(ic.half_dt, __dadd_rn(ic.r0.d, ic.r0.d)));
@@ -503,8 +539,8 @@ __device__ __forceinline__ void walker_start(Walker& w, const ItemConst& ic, con
 template <class WK>
 __device__ __forceinline__ bool walker_hold(WK& w, const RowRec* __restrict__ rows, const EdgeTables& edges,
                                             const LogEntry* s_log, unsigned long long& draws,
-                                            unsigned long long& jumps) {
-    stream_reserve2(w.st);  // the event's only Philox call site
+                                            unsigned long long& jumps, const uint4* rk = nullptr) {
+    stream_reserve2(w.st, rk);  // the event's only Philox call site (rk: keyless streams)
     bool step_done = true;
     if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
 #if EXPMC_QEND
@@ -696,7 +732,11 @@ struct Walker0 {
 #endif
     Row cur;
     uint32_t state;
+#if EXPMC_L0TUNE
+    uint32_t sign;  // kSignBit when the path's sign is -1, else 0
+#else
     int32_t sign;
+#endif
     double hold;
 #if EXPMC_PROD
     double thr;
@@ -710,16 +750,100 @@ __device__ __forceinline__ void walker0_start(Walker0& w, const ItemConst& ic, u
     stream_init(w.st, ic.seed, sample, ic.key3);
 #endif
     w.cur = ic.r0;
-    set_hold(w, ic.h0);
     w.state = ic.entry;
+#if EXPMC_L0TUNE
+    w.thr = ic.h0;  // set_hold(w, ic.h0), the product's start value prepared per item
+    w.hold = ic.hold0;
+    w.sign = 0u;
+#else
+    set_hold(w, ic.h0);
     w.sign = 1;
+#endif
 }
 
+#if EXPMC_L0TUNE
+// walker_hold for the level-0 walker, the same tests and values with the instruction count of
+// the common case cut (C2: uniform rows of degree 4, one rate, S-mode):
+//   * one Philox block per event, u = (c2, c3), v = (c0, c1) (StreamEv), round keys read through
+//     the item-constant pointer;
+//   * uniform row of degree 2^p: upper_bound = K >> (53 - p) = v word >> (64 - p), one funnel
+//     shift of the v word's high half; the (uniform, power of two) test is one and-not on
+//     deg ^ kUniformRow; table addresses from 32-bit indices;
+//   * the sign is kept as a sign bit and xor-ed with the target word's;
+//   * the step-end tests leave the common path: an S-mode jump that keeps the rate leaves
+//     hold = prod (1 - u_j) 2^0 > 0 (t > thr >= 2^-942), never the boundary case h1 == 0.
+__device__ __forceinline__ bool walker0_event(Walker0& w, const ItemConst& ic, const RowRec* __restrict__ rows,
+                                              const EdgeTables& edges, const LogEntry* s_log,
+                                              unsigned long long& draws, unsigned long long& jumps) {
+    uint32_t c0 = w.st.block++, c1 = w.st.c1, c2 = w.st.c2, c3 = w.st.c3;
+    philox10_rk(c0, c1, c2, c3, ic.rk);
+    bool done = true;
+    if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
+        ++draws;
+        const uint64_t k53 = ((static_cast<uint64_t>(c2) << 32) | c3) >> 11;  // u (rng.hpp:32-35)
+        const double m = __ull2double_rn((uint64_t{1} << 53) - k53);           // (1 - u) 2^53, exact
+        const bool smode = w.hold > 0.0;
+        double t = 0.0, e = 0.0;
+        bool jump;
+        if (smode) {
+            t = __dmul_rn(w.hold, m);  // prod (1 - u_j) (1 - u) 2^53
+            jump = t > w.thr;          // u < q
+        } else {
+            e = -fast_log(m, -53, s_log, c_log_poly);
+            jump = e < __dmul_rn(w.cur.rate, -w.hold);
+        }
+        if (jump) {
+            ++jumps;
+            // S-mode: the product times (1 - u), exact rescale, > 0; T-mode: -(remaining - E / rate) (paths.cpp:54)
+            double h1 = smode ? __dmul_rn(t, 0x1.0p-53) : -__dsub_rn(-w.hold, fast_div(e, w.cur.rate));
+            const uint32_t degf = w.cur.deg;
+            const uint32_t x = degf ^ kUniformRow;  // uniform row: its degree; other rows: bit 31 set
+            uint32_t k;
+            if ((x & (x - 1u)) == 0u)  // uniform, degree 2^p (deg >= 1 in a row with rate > 0)
+                k = __funnelshift_rc(c0, 0u, 1u + static_cast<uint32_t>(__clz(x)));  // c0 >> (32 - p); 0 for p = 0
+            else
+                k = pick_slot_np2(edges, w.cur.begin, degf, ((static_cast<uint64_t>(c0) << 32) | c1) >> 11);
+            const uint32_t ts = __ldg(edges.tgt + static_cast<uint32_t>(w.cur.begin + k));
+            w.sign ^= ts & kSignBit;
+            w.state = ts & kTargetMask;
+            w.cur = load_row_at(rows, w.state);  // the old row is dead here: the record loads in place
+            done = false;
+            if (smode) {
+                // S-mode lasts while the rate is the entry's (the sample's only fresh hold is the
+                // entry's, walker0_start): a jump to another rate continues in T-mode,
+                // S 2^53 = S0 2^53 / prod, -remaining = log(S) / rate
+                const double rate0 = ic.r0.rate;
+                if (w.cur.rate != rate0) {
+                    h1 = fast_div(fast_log(fast_div(w.thr, h1), -53, s_log, c_log_poly), rate0);
+                    done = h1 == 0.0;
+                }
+            } else {
+                done = !(h1 < 0.0);  // remaining <= 0: rounding pushed past the boundary (paths.cpp:67)
+            }
+            w.hold = h1;
+        }
+    }
+    return done;
+}
+#endif
+
 __device__ __forceinline__ double walker0_sample(const Walker0& w, const ItemConst& ic, const RowRec* __restrict__ rows) {
+#if EXPMC_L0TUNE
+    // a path that ends in a row with the entry's d has a == ea_key (the same sum of the same terms)
+    double ea = ic.ea_val;
+    if (w.cur.d != ic.r0.d) {
+        const double a = __dmul_rn(ic.half_dt, __dadd_rn(ic.r0.d, w.cur.d));  // last_step_sums; 0 + a == a for every test below
+        ea = a == ic.ea_key ? ic.ea_val : exp_or_one(a);
+    }
+    // (sign e^a) u[end]: the sign bit xor-ed into e^a is the product by +-1
+    const double sea = __hiloint2double(__double2hiint(ea) ^ static_cast<int>(w.sign), __double2loint(ea));
+    return __dmul_rn(sea, __ldg(&rows[w.state].u));
+#else
     const double a = __dadd_rn(0.0, __dmul_rn(ic.half_dt, __dadd_rn(ic.r0.d, w.cur.d)));  // last_step_sums
     const double sg = static_cast<double>(w.sign);
     const double ea = a == ic.ea_key ? ic.ea_val : exp_or_one(a);
     return __dmul_rn(__dmul_rn(sg, ea), __ldg(&rows[w.state].u));
+#endif
 }
 
 __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items, uint32_t i) {
@@ -743,6 +867,7 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.smode_max_x = kSModeMaxX;
     ic.r0 = Row{0.0, 0.0, 0u, 0u};
     ic.h0 = 0.0;
+    ic.hold0 = 0.0;
     ic.ea_key = 0.0;  // exp_or_one(0) = 1
     ic.ea_val = 1.0;
     return ic;
