@@ -7,7 +7,15 @@ product's host generators and pinned to the fixtures by a SHA-256 of their CSR a
 
 Rules (north_star):
   * statistical: |x_gpu - x_ref| <= 3 sqrt(SE_gpu^2 + SE_ref^2) on every component, up to a count of
-    exceedances consistent with Binomial(n, 0.0027) (tail probability >= 1e-3);
+    exceedances consistent with Binomial(n, p) (tail probability >= 1e-3).  p = 0.0027 (the normal
+    tail) on C2.  On the graph configs the REFERENCE ITSELF does not meet that p against a rerun of
+    itself with other row seeds (C3: 9-14 of 355 components beyond 3 combined SE, 3-4 %, with no
+    bias -- the driver's reported SE comes from sample variances of heavy-tailed level
+    corrections and understates the spread), so there p is the reference's own seed-to-seed
+    exceedance rate, from tests/golden/scale_<name>_reseed.json (scripts/scale_diag.py: the
+    reference-order sampler -- the reference draw for draw, as this file asserts -- rerun with
+    shifted row seeds), the estimates must be unbiased (mean signed z within 4 sd / sqrt(n)) and
+    the z distribution must match the reference's own (two-sample Kolmogorov-Smirnov);
   * reference-order sampler (draw for draw the reference): identical decision sequences (same l0,
     L, samples per level, cost) on >= 99 % of the components and equal estimates there;
   * event-driven sampler (statistically equivalent paths): the statistical rule, plus
@@ -87,12 +95,53 @@ def _same_decisions(res, lv, done):
     return same
 
 
-def _statistical(res, est, se, label):
+def _statistical(res, est, se, label, p=P_3SE):
     z = np.abs(res["estimate"] - est) / np.sqrt(res["statistical_error"] ** 2 + se ** 2)
     k = int(np.sum(z > 3.0))
-    print(f"{label}: {len(z)} components, {k} beyond 3 combined SE (expected {P_3SE * len(z):.2f}), max z {z.max():.2f}")
-    assert binomial_consistent(k, len(z)), (k, len(z), np.sort(z)[-8:])
+    print(f"{label}: {len(z)} components, {k} beyond 3 combined SE (expected {p * len(z):.2f}), max z {z.max():.2f}")
+    assert binomial_consistent(k, len(z), p=p), (k, len(z), np.sort(z)[-8:])
     return z
+
+
+def _reference_null(name, rows, est, se):
+    """The reference's own seed-to-seed z values on these components (the reseed fixture): signed
+    z of every pair of reference runs (the CPU reference's fixture and the reference-order
+    sampler's shifted-seed runs), and the pooled rate of |z| > 3."""
+    fx = _fixture(f"{name}_reseed")
+    assert fx["rows"] == rows.tolist()
+    runs = [(est, se)]
+    for key, r in fx["runs"].items():
+        if key.startswith("reference_") and key != "reference_0":
+            runs.append((np.array([float.fromhex(x) for x in r["estimate"]]),
+                         np.array([float.fromhex(x) for x in r["statistical_error"]])))
+    assert len(runs) >= 2
+    # the shift-0 reference-order run IS the fixture (the reference draw for draw)
+    r0 = fx["runs"]["reference_0"]
+    assert np.mean(np.abs(np.array([float.fromhex(x) for x in r0["estimate"]]) - est) <= 1e-10 * np.abs(est)) >= 0.99
+    zs = []
+    for i in range(len(runs)):
+        for j in range(i + 1, len(runs)):
+            zs.append((runs[i][0] - runs[j][0]) / np.sqrt(runs[i][1] ** 2 + runs[j][1] ** 2))
+    zs = np.concatenate(zs)
+    return zs, float(np.mean(np.abs(zs) > 3.0))
+
+
+def _statistical_vs_null(res, est, se, label, znull, p_null):
+    """The statistical rule with the reference's own exceedance rate, plus unbiasedness and equality
+    of the z distributions (module docstring)."""
+    from scipy.stats import ks_2samp
+
+    sz = (res["estimate"] - est) / np.sqrt(res["statistical_error"] ** 2 + se ** 2)
+    n = len(sz)
+    k = int(np.sum(np.abs(sz) > 3.0))
+    ks = ks_2samp(np.abs(sz), np.abs(znull))
+    print(f"{label}: {n} components, {k} beyond 3 combined SE; the reference against its own reruns: "
+          f"{p_null * n:.1f} expected ({p_null:.4f}, nominal {P_3SE}); mean signed z {sz.mean():+.3f} "
+          f"(sd {sz.std():.2f}), KS p-value vs the reference's own |z| {ks.pvalue:.3f}")
+    assert binomial_consistent(k, n, p=max(p_null, P_3SE)), (k, n, p_null)
+    assert abs(sz.mean()) <= 4.0 * sz.std() / math.sqrt(n), sz.mean()
+    assert ks.pvalue >= 1e-3, ks
+    return np.abs(sz)
 
 
 def test_c2_full_size_vs_reference_driver(gpu):
@@ -133,9 +182,10 @@ def test_graph_full_size_vs_reference_driver(gpu, name):
             print(f"  stratum {fx['strata'][s]}: the reference finished none of {len(rs)} within "
                   f"{fx['cap_seconds']} s ({sum(bool(r.get('skipped')) for r in rs)} not attempted after "
                   f"consecutive timeouts of lighter components)")
+    znull, p_null = _reference_null(name, rows, est, se)
     res_e, _ = _solve(cfg, rows, "event")
     assert res_e["converged"].mean() >= 0.99
-    z = _statistical(res_e, est, se, f"{name} event sampler")
+    z = _statistical_vs_null(res_e, est, se, f"{name} event sampler", znull, p_null)
     for s in sorted(set(strata.tolist())):
         m = strata == s
         print(f"  stratum {fx['strata'][s]}: {m.sum()} components, max z {z[m].max():.2f}")
@@ -144,7 +194,7 @@ def test_graph_full_size_vs_reference_driver(gpu, name):
     print(f"{name} reference-order sampler: identical decision sequences on {same.mean():.4f}")
     assert same.mean() >= 0.99
     assert np.allclose(res_r["estimate"][same], est[same], rtol=1e-10, atol=1e-13)
-    _statistical(res_r, est, se, f"{name} reference-order sampler")
+    _statistical(res_r, est, se, f"{name} reference-order sampler", p=max(p_null, P_3SE))
 
 
 def test_c3_event_vs_reference_order_level_means(gpu):
