@@ -22,13 +22,16 @@ namespace expmc_b200 {
 
 // ----------------------------------------------------------------------------- HBM layout
 // Packed row record: everything a walker needs when it lands on a row, in ONE 32-B sector
-// (the reference reads rate/d/row_ptr/u from four SoA arrays, chain.hpp:31-35).
+// (the reference reads rate/d/row_ptr/u from four SoA arrays, chain.hpp:31-35), as two 16-B
+// halves: what a JUMP needs (rate, begin, deg: one 128-bit load) and what the END of a fine step
+// or of the path needs (d, u: one 128-bit load).  The level-0 walker reads exactly one half per
+// event; the others read the first half and d (load_row, walker.cuh).
 struct alignas(32) RowRec {
-    double d;        // a_ii + rate_i                     (chain.cpp:47-48)
     double rate;     // sum_{j != i} |a_ij|               (chain.cpp:39-46)
-    double u;        // u_i, the terminal factor           (paths.cpp:112,138)
     uint32_t begin;  // first edge of the row
     uint32_t deg;    // bits 0-30: number of chain edges; bit 31: kUniformRow
+    double d;        // a_ii + rate_i                     (chain.cpp:47-48)
+    double u;        // u_i, the terminal factor           (paths.cpp:112,138)
 };
 static_assert(sizeof(RowRec) == 32, "row record must be one 32-B sector");
 

@@ -249,29 +249,25 @@ struct Row {  // u_i is not kept in registers: walker_finish reloads it for the 
 };
 
 __device__ __forceinline__ Row load_row(const RowRec* __restrict__ rows, uint32_t i) {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(rows + i));
-    const uint2 b = __ldg(reinterpret_cast<const uint2*>(rows + i) + 3);
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(rows + i));  // rate, begin, deg
     Row r;
-    r.d = a.x;
-    r.rate = a.y;
-    r.begin = b.x;
-    r.deg = b.y;
+    r.d = __ldg(&rows[i].d);
+    r.rate = __hiloint2double(static_cast<int>(a.y), static_cast<int>(a.x));
+    r.begin = a.z;
+    r.deg = a.w;
     return r;
 }
 
-// load_row with the record's address formed by one 32 x 32 -> 64-bit multiply-add (the compiler
-// otherwise splits the masked state's shift over six instructions).
-__device__ __forceinline__ Row load_row_at(const RowRec* __restrict__ rows, uint32_t i) {
+// The jump half of a row record (rate, begin, deg) with its address formed by one 32 x 32 -> 64-bit
+// multiply-add (the compiler otherwise splits the masked state's shift over six instructions);
+// the level-0 walker reads d only when the path ends (walker0_sample).
+__device__ __forceinline__ void load_row_jump(const RowRec* __restrict__ rows, uint32_t i, Row& r) {
     uint64_t p;
     asm("mad.wide.u32 %0, %1, 32, %2;" : "=l"(p) : "r"(i), "l"(reinterpret_cast<uint64_t>(rows)));
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    const uint2 b = __ldg(reinterpret_cast<const uint2*>(p) + 3);
-    Row r;
-    r.d = a.x;
-    r.rate = a.y;
-    r.begin = b.x;
-    r.deg = b.y;
-    return r;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+    r.rate = __hiloint2double(static_cast<int>(a.y), static_cast<int>(a.x));
+    r.begin = a.z;
+    r.deg = a.w;
 }
 
 // Neighbour choice (paths.cpp:57-65): k = upper_bound(cdf[begin:begin+deg], v) clamped to
@@ -806,7 +802,7 @@ __device__ __forceinline__ bool walker0_event(Walker0& w, const ItemConst& ic, c
             const uint32_t ts = __ldg(edges.tgt + static_cast<uint32_t>(w.cur.begin + k));
             w.sign ^= ts & kSignBit;
             w.state = ts & kTargetMask;
-            w.cur = load_row_at(rows, w.state);  // the old row is dead here: the record loads in place
+            load_row_jump(rows, w.state, w.cur);  // the old row is dead here: the half record loads in place
             done = false;
             if (smode) {
                 // S-mode lasts while the rate is the entry's (the sample's only fresh hold is the
@@ -829,15 +825,17 @@ __device__ __forceinline__ bool walker0_event(Walker0& w, const ItemConst& ic, c
 
 __device__ __forceinline__ double walker0_sample(const Walker0& w, const ItemConst& ic, const RowRec* __restrict__ rows) {
 #if EXPMC_L0TUNE
+    // the end half of the last row's record: (d, u), one 128-bit load
+    const double2 du = __ldg(reinterpret_cast<const double2*>(&rows[w.state].d));
     // a path that ends in a row with the entry's d has a == ea_key (the same sum of the same terms)
     double ea = ic.ea_val;
-    if (w.cur.d != ic.r0.d) {
-        const double a = __dmul_rn(ic.half_dt, __dadd_rn(ic.r0.d, w.cur.d));  // last_step_sums; 0 + a == a for every test below
+    if (du.x != ic.r0.d) {
+        const double a = __dmul_rn(ic.half_dt, __dadd_rn(ic.r0.d, du.x));  // last_step_sums; 0 + a == a for every test below
         ea = a == ic.ea_key ? ic.ea_val : exp_or_one(a);
     }
     // (sign e^a) u[end]: the sign bit xor-ed into e^a is the product by +-1
     const double sea = __hiloint2double(__double2hiint(ea) ^ static_cast<int>(w.sign), __double2loint(ea));
-    return __dmul_rn(sea, __ldg(&rows[w.state].u));
+    return __dmul_rn(sea, du.y);
 #else
     const double a = __dadd_rn(0.0, __dmul_rn(ic.half_dt, __dadd_rn(ic.r0.d, w.cur.d)));  // last_step_sums
     const double sg = static_cast<double>(w.sign);

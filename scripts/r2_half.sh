@@ -1,0 +1,22 @@
+# Row record as two 16-B halves (jump: rate, begin, deg; end: d, u) A/B: default = the in-tree
+# build, tune = the previous commit (walker0_event on the old record).  Level-0 SHA check, C2 jobs,
+# then the GPU suite on the default build.
+set -x
+V=paper_1904_12754_b200/_lib/variants
+for v in default tune; do
+  L=""; [ $v != default ] && L="EXPMC_LIB=$PWD/$V/$v.so"
+  env $L timeout 600 python scripts/level0_ab.py gpurun_out/hf_$v.sha > gpurun_out/hf_l0_$v.log 2>&1; echo "$v rc=$?"; tail -1 gpurun_out/hf_l0_$v.log
+done
+cat gpurun_out/hf_*.sha
+for rep in 1 2; do
+  for v in default tune; do
+    L=""; [ $v != default ] && L="EXPMC_LIB=$PWD/$V/$v.so"
+    env $L timeout 600 python bench.py --rows-per-step 262144 --steps 3 --warmup 2 --no-e2e --no-cpu-baseline > gpurun_out/hf_${v}_$rep.log 2>&1; echo "$v rc=$?"
+    python - gpurun_out/hf_${v}_$rep.log <<'PY'
+import json, sys
+d = json.loads(open(sys.argv[1]).read().splitlines()[-1])
+print(f"  value {d['value']:.4g} kernel_ms {d['roofline']['kernel_ms']:.1f} ms/step {d['ms_per_step']:.1f}")
+PY
+  done
+done
+timeout 2400 python -m pytest tests -m gpu -q -k "not c4-20" > gpurun_out/hf_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/hf_pytest.log
