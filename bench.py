@@ -650,9 +650,11 @@ def run_ours(args, rank, world, local):
                          "alg_bytes_per_launch": alg_bytes / launches,
                          "measured": measured,
                          "binding_resource": (None if not cap else
-                                              "instruction issue (measured issue_frac)" if cap["issue_frac"] >= 0.7 else
-                                              "random-gather latency (issue_frac below 0.7, L2 hit "
-                                              f"{cap['l2_hit']:.2f}; tables beyond L2)"),
+                                              f"the SM: issue slots {cap['issue_frac']:.2f} and L1 data pipe "
+                                              f"{cap['l1_frac']:.2f} of peak, gathers served by L1 (hit rate "
+                                              f"{cap['l1_hit']:.2f})" if cap["l1_hit"] >= 0.9 else
+                                              f"random-gather latency (issue slots {cap['issue_frac']:.2f}, L1 hit "
+                                              f"{cap['l1_hit']:.2f}, L2 hit {cap['l2_hit']:.2f}; tables beyond L2)"),
                          "gather_peak_l2_gbs": gather_l2, "gather_peak_hbm_gbs": gather_hbm,
                          "frac_of_gather_l2": (achieved / gather_l2) if gather_l2 else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(gpu_launches), "clocks": clk,

@@ -165,7 +165,7 @@ __device__ __forceinline__ bool ed_event(WK& w, const ItemConst& ic, const RowRe
     uint32_t ts;
     if (edges.erec != nullptr && !alias_row(edges, w.cur.deg)) {
         // one 32-B sector: the edge's target word and the target row's payload (EdgeRec)
-        const EdgeRec* p = edges.erec + w.cur.begin + pick_slot(edges, w.cur.begin, w.cur.deg, kv);
+        const EdgeRec* p = edges.erec + static_cast<uint32_t>(w.cur.begin + pick_slot(edges, w.cur.begin, w.cur.deg, kv));
         const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
         const double2 rd = __ldg(reinterpret_cast<const double2*>(p) + 1);
         ts = q.x;

@@ -248,23 +248,29 @@ struct Row {  // u_i is not kept in registers: walker_finish reloads it for the 
     uint32_t begin, deg;
 };
 
+// &rows[i] by one 32 x 32 -> 64-bit multiply-add (for an index that comes out of a mask the
+// compiler otherwise splits the shift over six instructions).
+__device__ __forceinline__ const RowRec* row_at(const RowRec* __restrict__ rows, uint32_t i) {
+    uint64_t p;
+    asm("mad.wide.u32 %0, %1, 32, %2;" : "=l"(p) : "r"(i), "l"(reinterpret_cast<uint64_t>(rows)));
+    return reinterpret_cast<const RowRec*>(p);
+}
+
 __device__ __forceinline__ Row load_row(const RowRec* __restrict__ rows, uint32_t i) {
-    const uint4 a = __ldg(reinterpret_cast<const uint4*>(rows + i));  // rate, begin, deg
+    const RowRec* p = row_at(rows, i);
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));  // rate, begin, deg
     Row r;
-    r.d = __ldg(&rows[i].d);
+    r.d = __ldg(&p->d);
     r.rate = __hiloint2double(static_cast<int>(a.y), static_cast<int>(a.x));
     r.begin = a.z;
     r.deg = a.w;
     return r;
 }
 
-// The jump half of a row record (rate, begin, deg) with its address formed by one 32 x 32 -> 64-bit
-// multiply-add (the compiler otherwise splits the masked state's shift over six instructions);
-// the level-0 walker reads d only when the path ends (walker0_sample).
+// The jump half of a row record (rate, begin, deg); the level-0 walker reads d only when the
+// path ends (walker0_sample).
 __device__ __forceinline__ void load_row_jump(const RowRec* __restrict__ rows, uint32_t i, Row& r) {
-    uint64_t p;
-    asm("mad.wide.u32 %0, %1, 32, %2;" : "=l"(p) : "r"(i), "l"(reinterpret_cast<uint64_t>(rows)));
-    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(row_at(rows, i)));
     r.rate = __hiloint2double(static_cast<int>(a.y), static_cast<int>(a.x));
     r.begin = a.z;
     r.deg = a.w;
@@ -304,7 +310,7 @@ __device__ __forceinline__ uint32_t pick_edge(const EdgeTables& e, uint32_t begi
         const uint4 r = __ldg(reinterpret_cast<const uint4*>(e.alias + begin + j));
         return f < __hiloint2double(static_cast<int>(r.y), static_cast<int>(r.x)) ? r.z : r.w;
     }
-    return __ldg(e.tgt + begin + pick_slot(e, begin, degf, k53));
+    return __ldg(e.tgt + static_cast<uint32_t>(begin + pick_slot(e, begin, degf, k53)));  // edges < 2^32: a 32-bit index
 }
 
 __device__ __forceinline__ uint32_t pick_slot(const EdgeTables& e, uint32_t begin, uint32_t degf, uint64_t k53) {
