@@ -8,14 +8,21 @@ product's host generators and pinned to the fixtures by a SHA-256 of their CSR a
 Rules (north_star):
   * statistical: |x_gpu - x_ref| <= 3 sqrt(SE_gpu^2 + SE_ref^2) on every component, up to a count of
     exceedances consistent with Binomial(n, p) (tail probability >= 1e-3).  p = 0.0027 (the normal
-    tail) on C2.  On the graph configs the REFERENCE ITSELF does not meet that p against a rerun of
-    itself with other row seeds (C3: 9-14 of 355 components beyond 3 combined SE, 3-4 %, with no
-    bias -- the driver's reported SE comes from sample variances of heavy-tailed level
-    corrections and understates the spread), so there p is the reference's own seed-to-seed
-    exceedance rate, from tests/golden/scale_<name>_reseed.json (scripts/scale_diag.py: the
-    reference-order sampler -- the reference draw for draw, as this file asserts -- rerun with
-    shifted row seeds), the estimates must be unbiased (mean signed z within 4 sd / sqrt(n)) and
-    the z distribution must match the reference's own (two-sample Kolmogorov-Smirnov);
+    tail) on C2.  On the graph configs the REFERENCE ITSELF meets neither that p nor eps: against
+    a rerun of itself with other row seeds 9-14 of 355 C3 components lie beyond 3 combined SE
+    (3-4 %, sd of z 1.4; on R-MAT scale 20 the estimates move by ~4 reported SE from seed to
+    seed), and against the deterministic e^{beta A} 1 its estimates carry a bias of -1.5e-3 (C3)
+    / -1.9e-3 (R-MAT 20) and an RMS error of 2.1e-3 / 3.4e-3 at eps = 1e-3 -- the driver's SE and
+    bias estimates come from sample moments of heavy-tailed level corrections (most samples of a
+    coupled level are exactly 0, a few are large) and understate both.  Parity with the reference
+    there means REPRODUCING ITS ERROR LAW, so the graph test checks, on the same components and
+    against the deterministic value (oracle dense_expmv), that the event sampler's errors have
+    the reference's mean (two-sample test, 4 sd), the reference's RMS (within 25 %) and the
+    reference's distribution (two-sample Kolmogorov-Smirnov); where reruns of the reference
+    exist (C3: tests/golden/scale_c3_reseed.json, written by scripts/scale_diag.py from the
+    reference-order sampler -- the reference draw for draw, as this file asserts -- with shifted
+    row seeds) the 3-SE rule is applied with the reference's own seed-to-seed exceedance rate as
+    p, with mean signed z within 4 sd / sqrt(n) and a KS test of |z| against the reference's own;
   * reference-order sampler (draw for draw the reference): identical decision sequences (same l0,
     L, samples per level, cost) on >= 99 % of the components and equal estimates there;
   * event-driven sampler (statistically equivalent paths): the statistical rule, plus
@@ -144,6 +151,25 @@ def _statistical_vs_null(res, est, se, label, znull, p_null):
     return np.abs(sz)
 
 
+def _same_error_law(res, est, exact, label, eps):
+    """The event sampler's errors against the deterministic value follow the reference's own error
+    law on the same components: same mean (two-sample test, 4 sd), same RMS (within 25 %), same
+    distribution (two-sample KS).  Neither has to meet eps: the reference does not on these graphs."""
+    from scipy.stats import ks_2samp
+
+    e_gpu, e_ref = res["estimate"] - exact, est - exact
+    n = len(e_gpu)
+    rms_g, rms_r = math.sqrt(float(np.mean(e_gpu ** 2))), math.sqrt(float(np.mean(e_ref ** 2)))
+    sd = math.sqrt(float(e_gpu.var() + e_ref.var()) / n)
+    ks = ks_2samp(e_gpu, e_ref)
+    print(f"{label} vs the deterministic value (eps {eps:g}): mean error {e_gpu.mean():+.2e} (reference "
+          f"{e_ref.mean():+.2e}, difference {abs(e_gpu.mean() - e_ref.mean()) / sd:.2f} sd), RMS {rms_g:.2e} "
+          f"(reference {rms_r:.2e}), KS p-value {ks.pvalue:.3f}")
+    assert abs(e_gpu.mean() - e_ref.mean()) <= 4.0 * sd
+    assert 0.8 <= rms_g / rms_r <= 1.25, (rms_g, rms_r)
+    assert ks.pvalue >= 1e-3, ks
+
+
 def test_c2_full_size_vs_reference_driver(gpu):
     """C2 at n = 2^20: 512 seed-chosen components, reference-order sampler (the config's)."""
     fx = _fixture("c2")
@@ -159,7 +185,7 @@ def test_c2_full_size_vs_reference_driver(gpu):
 
 
 @pytest.mark.parametrize("name", ["c3", "c4-20"])
-def test_graph_full_size_vs_reference_driver(gpu, name):
+def test_graph_full_size_vs_reference_driver(gpu, oracle_lib, name):
     """C3 (BA n = 1e6, full graph) and R-MAT scale 20 at eps = 1e-3 on >= 256 degree-stratified
     components, hubs included wherever the reference finished them within the fixture's cap.
 
@@ -182,10 +208,21 @@ def test_graph_full_size_vs_reference_driver(gpu, name):
             print(f"  stratum {fx['strata'][s]}: the reference finished none of {len(rs)} within "
                   f"{fx['cap_seconds']} s ({sum(bool(r.get('skipped')) for r in rs)} not attempted after "
                   f"consecutive timeouts of lighter components)")
-    znull, p_null = _reference_null(name, rows, est, se)
     res_e, _ = _solve(cfg, rows, "event")
     assert res_e["converged"].mean() >= 0.99
-    z = _statistical_vs_null(res_e, est, se, f"{name} event sampler", znull, p_null)
+    from oracle import CSR
+
+    exact = oracle_lib.dense_expmv(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val), cfg.u, cfg.beta)[rows]
+    _same_error_law(res_e, est, exact, f"{name} event sampler", 1e-3)
+    p_null = P_3SE
+    if os.path.exists(os.path.join(HERE, "golden", f"scale_{name}_reseed.json")):
+        znull, p_null = _reference_null(name, rows, est, se)
+        z = _statistical_vs_null(res_e, est, se, f"{name} event sampler", znull, p_null)
+    else:  # no rerun of the reference within reach (R-MAT 20: > 46 GPU-minutes): reported, not asserted
+        sz = (res_e["estimate"] - est) / np.sqrt(res_e["statistical_error"] ** 2 + se ** 2 + 1e-300)
+        z = np.abs(sz)
+        print(f"{name} event sampler: {int(np.sum(z > 3))} of {len(z)} beyond 3 combined SE, sd of z {sz.std():.2f} "
+              "(no reference rerun for this config; the reported SE understates the seed-to-seed spread)")
     for s in sorted(set(strata.tolist())):
         m = strata == s
         print(f"  stratum {fx['strata'][s]}: {m.sum()} components, max z {z[m].max():.2f}")
@@ -194,6 +231,7 @@ def test_graph_full_size_vs_reference_driver(gpu, name):
     print(f"{name} reference-order sampler: identical decision sequences on {same.mean():.4f}")
     assert same.mean() >= 0.99
     assert np.allclose(res_r["estimate"][same], est[same], rtol=1e-10, atol=1e-13)
+    # draw for draw the reference: the same seeds give the same estimates (z = 0 on the identical ones)
     _statistical(res_r, est, se, f"{name} reference-order sampler", p=max(p_null, P_3SE))
 
 
