@@ -103,7 +103,10 @@ def _same_decisions(res, lv, done):
 
 
 def _statistical(res, est, se, label, p=P_3SE):
-    z = np.abs(res["estimate"] - est) / np.sqrt(res["statistical_error"] ** 2 + se ** 2)
+    diff = np.abs(res["estimate"] - est)
+    # components whose samples are all equal (degree-1 rows of a graph: SE 0) agree to rounding
+    z = np.where(diff <= 1e-12 * np.maximum(1.0, np.abs(est)), 0.0,
+                 diff / np.sqrt(res["statistical_error"] ** 2 + se ** 2 + 1e-300))
     k = int(np.sum(z > 3.0))
     print(f"{label}: {len(z)} components, {k} beyond 3 combined SE (expected {p * len(z):.2f}), max z {z.max():.2f}")
     assert binomial_consistent(k, len(z), p=p), (k, len(z), np.sort(z)[-8:])
