@@ -72,13 +72,31 @@ struct EdWalkerT {
 };
 using EdWalker = EdWalkerT<Stream>;
 // k_sample_grouped's walker: the Philox key schedule comes from the warp's round-key table
-// (ItemConst::rk, one item per warp at a time), so the stream holds no key registers.
+// (ItemConst::rk, one item per warp at a time), so the stream holds no key registers.  An
+// entry-mode event consumes the stream as E_1 v_1 E_2 v_2 ... E_k (a jump draws the holding time
+// and the neighbour; the last holding time ends the path), so block b holds exactly event b + 1's
+// two words: one Philox block per event and no word queue (StreamEv) -- the same words in the
+// same order as the queued stream (EXPMC_EDEV=0), results bitwise equal.
+// EXPMC_ED_PREFETCH: a jump prefetches the landing row's u (A/B builds).
+#ifndef EXPMC_ED_PREFETCH
+#define EXPMC_ED_PREFETCH 0
+#endif
+#ifndef EXPMC_EDEV
+#define EXPMC_EDEV 1
+#endif
+#if EXPMC_EDEV
+using EdWalkerRK = EdWalkerT<StreamEv>;
+#else
 using EdWalkerRK = EdWalkerT<StreamRK>;
+#endif
 
 __device__ __forceinline__ void ed_stream_init(Stream& st, const ItemConst& ic, uint64_t sample) {
     stream_init(st, ic.seed, sample, ic.key3);
 }
 __device__ __forceinline__ void ed_stream_init(StreamRK& st, const ItemConst& ic, uint64_t sample) {
+    stream_init(st, sample, ic.key3);
+}
+__device__ __forceinline__ void ed_stream_init(StreamEv& st, const ItemConst& ic, uint64_t sample) {
     stream_init(st, sample, ic.key3);
 }
 
@@ -179,6 +197,11 @@ __device__ __forceinline__ bool ed_event(WK& w, const ItemConst& ic, const RowRe
     }
     if (ts & kSignBit) w.sign = -w.sign;
     w.state = ts & kTargetMask;
+#if EXPMC_ED_PREFETCH
+    // most jumping paths end within a jump or two: start u[state]'s sector on its way now, the
+    // path's end reads it (ed_finish) one event later at the earliest
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(&rows[w.state].u));
+#endif
     if (w.cur.d != w.dfirst) w.dconst = 0u;
     return false;
 }

@@ -233,6 +233,13 @@ __device__ __forceinline__ void stream_reserve2(StreamEv& s, const uint4* rk) {
     s.w1 = (static_cast<uint64_t>(c0) << 32) | c1;
 }
 
+// One-block stream read in order: the first pop returns the event's first word, the second its second.
+__device__ __forceinline__ uint64_t stream_pop_bits(StreamEv& s) {
+    const uint64_t bits = s.w0;
+    s.w0 = s.w1;
+    return bits >> 11;
+}
+
 // The event's words are consumed: advance the queue by u, or by u and v after a jump.
 template <class ST>
 __device__ __forceinline__ void stream_advance(ST& s, bool jump) {
