@@ -2,6 +2,7 @@
 and sample indices, isolated / absorbing rows, the multi-launch sampler window, and batches
 mixing every lane-independent request shape.  Each is checked against the oracle (bit-exact
 integer work, <= 4 ulp values, 1e-12 sums) or against a closed form."""
+import math
 import os
 import subprocess
 import sys
@@ -200,3 +201,45 @@ print("ok")
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                            cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("beta", [0.7, 900.0])
+def test_level0_walker_matches_oracle_on_every_row_kind(gpu, oracle_lib, beta):
+    """The level-0 walker (RefPolicy0 / walker0_event: level 0, base, one fine step) against the
+    oracle's run_level on a matrix with every kind of row its fast paths distinguish: uniform rows
+    of degree 1, 2, 4, 8 (one-shift pick), uniform rows of degree 3, 5, 6, 7 (exact-floor pick),
+    non-uniform rows of degree <= 4 and > 4 (CDF count / binary search), mixed signs, absorbing
+    rows, and rates spread over five decades (S-mode -> T-mode on a rate change).  beta = 900 puts
+    rate * dt past the S-mode range on the fast rows (T-mode from the first event).  Draw chains
+    are exact: cost and jump counts equal the oracle's; sums to 1e-12."""
+    rng = np.random.default_rng(29)
+    n = 72
+    dense = np.zeros((n, n))
+    for i in range(n):
+        kind = i % 6
+        if kind == 5:
+            continue  # absorbing: no off-diagonal entries
+        if kind in (0, 1):  # uniform rows: equal magnitudes, degree 1..8
+            deg = [1, 2, 4, 8, 3, 5, 6, 7][(i // 6) % 8]
+            cols = rng.choice([j for j in range(n) if j != i], size=deg, replace=False)
+            dense[i, cols] = rng.choice([-1.0, 1.0], size=deg) * (2.0 if kind == 0 else 0.37)
+        else:  # non-uniform rows, narrow and wide
+            deg = int(rng.integers(2, 5)) if kind == 2 else int(rng.integers(5, 13))
+            cols = rng.choice([j for j in range(n) if j != i], size=deg, replace=False)
+            dense[i, cols] = rng.uniform(-1.5, 1.5, deg)
+        dense[i] *= 10.0 ** rng.integers(-3, 2)  # rates over five decades
+    # d = a_ii + rate in (-0.5, 0.3): e^{beta d} and its square stay finite at beta = 900
+    np.fill_diagonal(dense, -np.abs(dense).sum(axis=1) + rng.uniform(-0.5, 0.3, n))
+    a = P.SparseMatrix.from_dense(dense)
+    u = rng.uniform(-1.0, 1.0, n)
+    och = oracle_lib.chain(CSR(a.n, a.row_ptr, a.col, a.val))
+    entries = np.arange(n)
+    count = 3000 if beta < 10 else 400  # beta = 900: hundreds of jumps per path on the fast rows
+    with P.Context(a, u) as ctx:
+        got = ctx.run_level_batch(beta, entries, 0, 1, 0, count, 77 + entries)
+    for e in entries:
+        o = och.run_level(u, int(e), beta, 0, 1, 0, count, 77 + int(e))
+        assert int(got["cost"][e]) == o["cost"] and int(got["jumps"][e]) == o["jumps"], (e, e % 6)
+        # signed terms cancel: the summation-order rounding scales with sum |x| <= sqrt(count sum x^2)
+        assert abs(float(got["sum"][e]) - o["sum"]) <= 1e-12 * max(1.0, math.sqrt(count * o["sum_sq"])), (e, e % 6)
+        assert abs(float(got["sum_sq"][e]) - o["sum_sq"]) <= 1e-12 * max(1.0, abs(o["sum_sq"])), (e, e % 6)
