@@ -198,9 +198,13 @@ __global__ void __launch_bounds__(kThreads, P::kMinBlocks) k_sample(SamplerArgs 
             my = listed ? wl[lane] : lane;
             P::start(w, ic, a.init, a.rows, lo_hi | (lo_lo + my));
         }
+        // next: work entries started so far, uncapped (min(nwork, 32) at first, + 1 per finished
+        // sample): the loop ends when every entry has finished, next == nwork + min(nwork, 32) -- a
+        // warp-uniform compare instead of a vote over the lanes' idle flags
         uint32_t next = nwork < 32u ? nwork : 32u;
+        const uint32_t next_end = nwork + next;
         uint32_t qh = 0, qn = 0;  // deferred finish: ring head and pending records (warp-uniform)
-        while (__any_sync(full, my != kIdle)) {
+        while (next != next_end) {
             const bool done = my != kIdle && P::event(w, ic, a.init, a.rows, a.edges, s_log, cost, jumps);
             const unsigned fin = __ballot_sync(full, done);
             if (done) {

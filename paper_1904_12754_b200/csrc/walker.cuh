@@ -413,6 +413,7 @@ struct ItemConst {
     Row r0;             // entry mode: the entry's row record and its fresh-step hold (the
     double h0;          //   restart of every sample reads them from here, not from the tables)
     double hold0;       // level-0 walker: the restart's hold (product form: 1 in S-mode, else h0)
+    double h0s;         // level-0 walker: the restart's threshold, h0 2^11 = S0 2^64 in S-mode (else h0, unused)
     double ea_key;      // base level: e^{ea_key} = ea_val, the exponent of a path that keeps the
     double ea_val;      //   entry's d (every interior path of C5) -- one exp per chunk, not per sample
     // event-driven entry mode: closed-form first holding interval (EdPolicy::prepare)
@@ -497,6 +498,7 @@ __device__ __forceinline__ void prepare_hold(ItemConst& ic, const RowRec* __rest
     ic.h0 = fresh_hold(ic, ic.r0.rate);
 #if EXPMC_PROD
     ic.hold0 = ic.h0 > 0.0 ? 1.0 : ic.h0;  // set_hold(w, h0)
+    ic.h0s = ic.h0 > 0.0 ? __dmul_rn(ic.h0, 0x1.0p11) : ic.h0;
 #else
     ic.hold0 = ic.h0;
 #endif
@@ -761,7 +763,7 @@ __device__ __forceinline__ void walker0_start(Walker0& w, const ItemConst& ic, u
     w.cur = ic.r0;
     w.state = ic.entry;
 #if EXPMC_L0TUNE
-    w.thr = ic.h0;  // set_hold(w, ic.h0), the product's start value prepared per item
+    w.thr = ic.h0s;  // set_hold(w, ic.h0) with the threshold as S0 2^64 (walker0_event)
     w.hold = ic.hold0;
     w.sign = 0u;
 #else
@@ -789,22 +791,26 @@ __device__ __forceinline__ bool walker0_event(Walker0& w, const ItemConst& ic, c
     bool done = true;
     if (w.cur.rate != 0.0) {  // rate == 0: absorbing row, holding time +inf (paths.cpp:50)
         ++draws;
-        const uint64_t k53 = ((static_cast<uint64_t>(c2) << 32) | c3) >> 11;  // u (rng.hpp:32-35)
-        const double m = __ull2double_rn((uint64_t{1} << 53) - k53);           // (1 - u) 2^53, exact
+        // m = (1 - u) 2^64 = 2^64 - (K << 11), K = (c2, c3) >> 11 (rng.hpp:32-35): the word with its
+        // low 11 bits cleared converts exactly (53 significant bits) and the subtraction is exact --
+        // no 64-bit shift and integer subtract.  The walker's threshold carries the same 2^11
+        // (Walker0::thr = S0 2^64): every product below is the 2^53 form's times a power of two.
+        const uint64_t uw = (static_cast<uint64_t>(c2) << 32) | (c3 & 0xFFFFF800u);
+        const double m = __dsub_rn(0x1.0p64, __ull2double_rn(uw));
         const bool smode = w.hold > 0.0;
         double t = 0.0, e = 0.0;
         bool jump;
         if (smode) {
-            t = __dmul_rn(w.hold, m);  // prod (1 - u_j) (1 - u) 2^53
+            t = __dmul_rn(w.hold, m);  // prod (1 - u_j) (1 - u) 2^64
             jump = t > w.thr;          // u < q
         } else {
-            e = -fast_log(m, -53, s_log, c_log_poly);
+            e = -fast_log(m, -64, s_log, c_log_poly);
             jump = e < __dmul_rn(w.cur.rate, -w.hold);
         }
         if (jump) {
             ++jumps;
             // S-mode: the product times (1 - u), exact rescale, > 0; T-mode: -(remaining - E / rate) (paths.cpp:54)
-            double h1 = smode ? __dmul_rn(t, 0x1.0p-53) : -__dsub_rn(-w.hold, fast_div(e, w.cur.rate));
+            double h1 = smode ? __dmul_rn(t, 0x1.0p-64) : -__dsub_rn(-w.hold, fast_div(e, w.cur.rate));
             const uint32_t degf = w.cur.deg;
             const uint32_t x = degf ^ kUniformRow;  // uniform row: its degree; other rows: bit 31 set
             uint32_t k;
@@ -823,7 +829,7 @@ __device__ __forceinline__ bool walker0_event(Walker0& w, const ItemConst& ic, c
                 // S 2^53 = S0 2^53 / prod, -remaining = log(S) / rate
                 const double rate0 = ic.r0.rate;
                 if (w.cur.rate != rate0) {
-                    h1 = fast_div(fast_log(fast_div(w.thr, h1), -53, s_log, c_log_poly), rate0);
+                    h1 = fast_div(fast_log(fast_div(__dmul_rn(w.thr, 0x1.0p-11), h1), -53, s_log, c_log_poly), rate0);
                     done = h1 == 0.0;
                 }
             } else {
@@ -879,6 +885,7 @@ __device__ __forceinline__ ItemConst load_item(const DevItem* __restrict__ items
     ic.r0 = Row{0.0, 0.0, 0u, 0u};
     ic.h0 = 0.0;
     ic.hold0 = 0.0;
+    ic.h0s = 0.0;
     ic.ea_key = 0.0;  // exp_or_one(0) = 1
     ic.ea_val = 1.0;
     return ic;
