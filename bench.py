@@ -635,8 +635,14 @@ def run_ours(args, rank, world, local):
                 "projected_gpu_hours_full_job": proj_full / cost_rate / 3600.0 * world if cost_rate > 0 else None,
                 "note": "model units the over-budget components need at this eps (driver projection, DESIGN §7b); "
                         "GPU-hours at this run's cost-unit rate on n_gpus GPUs"},
+            # achieved / frac: the contract's ALGORITHMIC bytes over the HBM copy peak (also under
+            # their own name, modelled_gbs / modelled_frac); dram_frac, l2_frac, l1_frac, issue_frac:
+            # what the config's ncu capture measured -- the kernel's real position (binding_resource)
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "modelled_gbs": achieved, "modelled_frac": achieved / peak,
+                         "dram_frac": measured and measured["dram_frac"], "l2_frac": measured and measured["l2_frac"],
+                         "l1_frac": measured and measured["l1_frac"], "issue_frac": measured and measured["issue_frac"],
                          "kernel": "k_sample_grouped" if sampler == "event" else "k_sample",
                          "sampler_launches": ctr["sampler_launches"],
                          "kernel_ms": ctr["sampler_ms"], "mean_launch_ms": mean_launch_ms,
