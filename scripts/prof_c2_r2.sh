@@ -9,7 +9,7 @@ for K in RefPolicy0 9RefPolicyILb0EEELb0E; do
   SKIP=$(python - "$K" <<'PY'
 import csv, sys
 rows = [r for r in csv.reader(open("gpurun_out/launches_c2_r2.csv")) if len(r) > 14 and "k_sample" in r[4]]
-key = "RefPolicy0" if sys.argv[1] == "RefPolicy0" else "RefPolicy<false>"
+key = "RefPolicy0" if sys.argv[1] == "RefPolicy0" else "RefPolicy<"
 sel = [float(r[14]) for r in rows if key in r[4]]
 print(max(range(len(sel)), key=sel.__getitem__))
 PY
