@@ -238,23 +238,18 @@ def test_graph_full_size_vs_reference_driver(gpu, oracle_lib, name):
     _statistical(res_r, est, se, f"{name} reference-order sampler", p=max(p_null, P_3SE))
 
 
-def test_c3_event_vs_reference_order_level_means(gpu):
-    """On the full C3 graph (l0 = 7): per-level sample means of the event-driven sampler equal the
-    reference-order sampler's (which is the reference draw for draw) at levels 7 (base) .. 10
-    (coupled), 2^18 samples each, on degree-stratified components: within 4 combined SE up to a
-    Binomial-consistent count, and unit costs within 2 %."""
-    cfg = configs.make_config("c3")
+def _level_means(name, strata, per_stratum, l0_expected, m):
+    cfg = configs.make_config(name)
     deg = np.diff(cfg.a.row_ptr)
     rng = np.random.default_rng(7)
     rows = []
-    for lo, hi in [(5, 5), (6, 7), (8, 11), (12, 19), (20, 49), (50, 199), (200, 1 << 40)]:
+    for lo, hi in strata:
         cand = np.where((deg >= lo) & (deg <= hi))[0]
-        rows += list(rng.choice(cand, size=3, replace=False))
+        rows += list(rng.choice(cand, size=per_stratum, replace=False))
     rows = np.array(rows, np.int64)
     with P.Context(cfg.a, cfg.u) as ctx:
         l0 = P.initial_level(cfg.beta, ctx.d_max)
-    assert l0 == 7
-    m = 1 << 18
+    assert l0 == l0_expected
     entry = np.repeat(rows, 4)
     level = np.tile(np.arange(l0, l0 + 4), len(rows))
     base = (level == l0).astype(np.int32)
@@ -269,8 +264,25 @@ def test_c3_event_vs_reference_order_level_means(gpu):
     vr = r["sum_sq"] / m - mr ** 2
     z = np.abs(me - mr) / np.sqrt((ve + vr) / m + 1e-300)
     k = int(np.sum(z > 4.0))
-    print(f"level means: {len(z)} (component, level) pairs, {k} beyond 4 SE, max z {z.max():.2f}")
+    print(f"{name} level means: {len(z)} (component, level) pairs, degrees {deg[rows].min()} .. {deg[rows].max()}, "
+          f"{k} beyond 4 SE, max z {z.max():.2f}")
     assert binomial_consistent(k, len(z), p=6.3e-5)
     uc_e = e["cost"].astype(np.float64).sum() / (m * len(z))
     uc_r = r["cost"].astype(np.float64).sum() / (m * len(z))
     assert uc_e == pytest.approx(uc_r, rel=0.02)
+
+
+def test_c3_event_vs_reference_order_level_means(gpu):
+    """On the full C3 graph (l0 = 7): per-level sample means of the event-driven sampler equal the
+    reference-order sampler's (which is the reference draw for draw) at levels 7 (base) .. 10
+    (coupled), 2^18 samples each, on degree-stratified components: within 4 combined SE up to a
+    Binomial-consistent count, and unit costs within 2 %."""
+    _level_means("c3", [(5, 5), (6, 7), (8, 11), (12, 19), (20, 49), (50, 199), (200, 1 << 40)], 3, 7, 1 << 18)
+
+
+def test_c4_configured_size_event_vs_reference_order_level_means(gpu):
+    """The same at C4's configured size -- R-MAT scale 24, 2^24 rows, 5.2e8 chain edges, tables and
+    edge records far beyond L2 -- where the CPU reference cannot run a driver in reasonable time
+    (its run_level rebuilds an O(n) table per call): levels l0 = 8 .. 11, 2^16 samples each, 28
+    components from degree 1 to the hubs."""
+    _level_means("c4", [(1, 1), (2, 3), (4, 7), (8, 15), (16, 63), (64, 255), (256, 1 << 40)], 4, 8, 1 << 16)
