@@ -249,7 +249,7 @@ def _level_means(name, strata, per_stratum, l0_expected, m):
     rows = np.array(rows, np.int64)
     with P.Context(cfg.a, cfg.u) as ctx:
         l0 = P.initial_level(cfg.beta, ctx.d_max)
-    assert l0 == l0_expected
+    assert l0_expected is None or l0 == l0_expected
     entry = np.repeat(rows, 4)
     level = np.tile(np.arange(l0, l0 + 4), len(rows))
     base = (level == l0).astype(np.int32)
@@ -286,3 +286,12 @@ def test_c4_configured_size_event_vs_reference_order_level_means(gpu):
     (its run_level rebuilds an O(n) table per call): levels l0 = 8 .. 11, 2^16 samples each, 28
     components from degree 1 to the hubs."""
     _level_means("c4", [(1, 1), (2, 3), (4, 7), (8, 15), (16, 63), (64, 255), (256, 1 << 40)], 4, 8, 1 << 16)
+
+
+def test_c5_configured_size_event_vs_reference_order_level_means(gpu):
+    """C5 at its configured size -- the 3-D convection-diffusion operator on 256^3 (n = 2^24,
+    non-uniform rows with mixed signs: the event sampler picks through its alias tables, the
+    reference-order sampler through the reference's CDF search): levels l0 .. l0+3, 2^16 samples
+    each, components from the corners (4 stored entries per row, the diagonal included) to the
+    interior (7)."""
+    _level_means("c5", [(4, 4), (5, 5), (6, 6), (7, 7)], 6, None, 1 << 16)
