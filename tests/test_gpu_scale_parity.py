@@ -63,6 +63,17 @@ def _csr_hash(a):
     return h.hexdigest()
 
 
+_CFG_CACHE = {}
+
+
+def _make_config(name):
+    """The configured-size graphs take a minute to generate: the tests of one run share them."""
+    if name not in _CFG_CACHE:
+        _CFG_CACHE.clear()  # one large matrix at a time (C4: 8 GB of host CSR)
+        _CFG_CACHE[name] = configs.make_config(name)
+    return _CFG_CACHE[name]
+
+
 def binomial_consistent(k, n, p=P_3SE, alpha=1e-3):
     """P(X >= k) for X ~ Binomial(n, p) is at least alpha."""
     return k == 0 or float(binom.sf(k - 1, n, p)) >= alpha
@@ -239,7 +250,7 @@ def test_graph_full_size_vs_reference_driver(gpu, oracle_lib, name):
 
 
 def _level_means(name, strata, per_stratum, l0_expected, m):
-    cfg = configs.make_config(name)
+    cfg = _make_config(name)
     deg = np.diff(cfg.a.row_ptr)
     rng = np.random.default_rng(7)
     rows = []
@@ -288,6 +299,48 @@ def test_c4_configured_size_event_vs_reference_order_level_means(gpu):
     _level_means("c4", [(1, 1), (2, 3), (4, 7), (8, 15), (16, 63), (64, 255), (256, 1 << 40)], 4, 8, 1 << 16)
 
 
+def _ulps(a, b):
+    ia, ib = np.asarray(a, np.float64).view(np.int64), np.asarray(b, np.float64).view(np.int64)
+    ia = np.where(ia < 0, np.int64(-(2 ** 63)) - ia, ia)
+    ib = np.where(ib < 0, np.int64(-(2 ** 63)) - ib, ib)
+    return np.abs(ia - ib)
+
+
+def test_c4_configured_size_per_sample_parity(gpu, oracle_lib):
+    """C4 at its configured size (R-MAT scale 24: 2^24 rows, 5.2e8 chain edges, hub rows hundreds
+    wide) against the oracle, sample by sample, at levels l0 = 8 .. 10 on components from degree 1
+    to the hubs: the reference-order sampler's cost, jump count and end state exact, values within
+    4 ulp -- the draw-for-draw pin the scale-20 fixture gives through the driver, on the full graph."""
+    from oracle import CSR
+
+    cfg = _make_config("c4")
+    och = oracle_lib.chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
+    deg = np.diff(cfg.a.row_ptr)
+    rng = np.random.default_rng(44)
+    rows = []
+    for lo, hi in [(1, 1), (2, 3), (4, 7), (8, 15), (16, 63), (64, 255), (256, 1 << 40)]:
+        cand = np.where((deg >= lo) & (deg <= hi))[0]
+        rows += list(rng.choice(cand, size=6, replace=False))
+    rows = np.array(rows, np.int64)
+    with P.Context(cfg.a, cfg.u) as ctx:
+        l0 = P.initial_level(cfg.beta, ctx.d_max)
+        for level in range(l0, l0 + 3):
+            for base in ([1] if level == l0 else [0]):
+                idx = rng.integers(0, 2 ** 40, len(rows)).astype(np.uint64)
+                got = ctx.sample_debug(cfg.beta, rows, level, base, 1000 + rows, idx)
+                for k, r in enumerate(rows):
+                    e = och.samples(cfg.u, int(r), cfg.beta, level, base, 1000 + int(r), idx[k:k + 1])
+                    assert got["cost"][k] == e["cost"][0] and got["jumps"][k] == e["jumps"][0], (r, level, base)
+                    assert got["end_state"][k] == e["end_state"][0], (r, level, base)
+                    assert _ulps(got["fine"][k], e["fine"][0]) <= 4 and _ulps(got["coarse"][k], e["coarse"][0]) <= 4
+        sel = rows[::6]  # one component per stratum through run_level (sums of 3000 samples)
+        b = ctx.run_level_batch(cfg.beta, sel, l0, 1, 0, 3000, 1000 + sel)
+        for k, r in enumerate(sel):
+            o = och.run_level(cfg.u, int(r), cfg.beta, l0, 1, 0, 3000, 1000 + int(r))
+            assert int(b["cost"][k]) == o["cost"] and int(b["jumps"][k]) == o["jumps"], r
+            assert abs(float(b["sum"][k]) - o["sum"]) <= 1e-12 * max(1.0, math.sqrt(3000 * o["sum_sq"]))
+
+
 def test_c5_configured_size_event_vs_reference_order_level_means(gpu):
     """C5 at its configured size -- the 3-D convection-diffusion operator on 256^3 (n = 2^24,
     non-uniform rows with mixed signs: the event sampler picks through its alias tables, the
@@ -295,3 +348,43 @@ def test_c5_configured_size_event_vs_reference_order_level_means(gpu):
     each, components from the corners (4 stored entries per row, the diagonal included) to the
     interior (7)."""
     _level_means("c5", [(4, 4), (5, 5), (6, 6), (7, 7)], 6, None, 1 << 16)
+
+
+def test_c5_configured_size_per_sample_parity(gpu, oracle_lib):
+    """C5 at its configured size against the oracle, sample by sample (the config has no driver
+    fixture: the reference needs hours per component at eps = 1e-4): the reference-order sampler's
+    cost, jump count and end state are exact and its values within 4 ulp on 256^3's non-uniform,
+    mixed-sign rows, at levels 0 .. 4 (base and coupled) with sample indices up to 2^40."""
+    from oracle import CSR
+
+    cfg = _make_config("c5")
+    och = oracle_lib.chain(CSR(cfg.a.n, cfg.a.row_ptr, cfg.a.col, cfg.a.val))
+    deg = np.diff(cfg.a.row_ptr)
+    rng = np.random.default_rng(55)
+    rows = np.concatenate([rng.choice(np.where(deg == k)[0], size=min(30, int(np.sum(deg == k))), replace=False)
+                           for k in (4, 5, 6, 7)])
+
+    def ulps(a, b):
+        ia, ib = np.asarray(a, np.float64).view(np.int64), np.asarray(b, np.float64).view(np.int64)
+        ia = np.where(ia < 0, np.int64(-(2 ** 63)) - ia, ia)
+        ib = np.where(ib < 0, np.int64(-(2 ** 63)) - ib, ib)
+        return np.abs(ia - ib)
+
+    with P.Context(cfg.a, cfg.u) as ctx:
+        for level in range(0, 5):
+            for base in ([1] if level == 0 else [1, 0]):
+                idx = rng.integers(0, 2 ** 40, len(rows)).astype(np.uint64)
+                got = ctx.sample_debug(cfg.beta, rows, level, base, 1000 + rows, idx)
+                for k, r in enumerate(rows):
+                    e = och.samples(cfg.u, int(r), cfg.beta, level, base, 1000 + int(r), idx[k:k + 1])
+                    assert got["cost"][k] == e["cost"][0] and got["jumps"][k] == e["jumps"][0], (r, level, base)
+                    assert got["end_state"][k] == e["end_state"][0], (r, level, base)
+                    assert ulps(got["fine"][k], e["fine"][0]) <= 4 and ulps(got["coarse"][k], e["coarse"][0]) <= 4
+        # run_level at level 0 (the level-0 walker) and level 3 (the general walker): exact counts
+        sel = rows[::10]
+        for level, base in ((0, 1), (3, 0)):
+            b = ctx.run_level_batch(cfg.beta, sel, level, base, 0, 2000, 1000 + sel)
+            for k, r in enumerate(sel):
+                o = och.run_level(cfg.u, int(r), cfg.beta, level, base, 0, 2000, 1000 + int(r))
+                assert int(b["cost"][k]) == o["cost"] and int(b["jumps"][k]) == o["jumps"], (r, level)
+                assert abs(float(b["sum"][k]) - o["sum"]) <= 1e-12 * max(1.0, math.sqrt(2000 * o["sum_sq"]))
